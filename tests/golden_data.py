@@ -1,0 +1,59 @@
+"""Loaders for the committed golden fixtures (generated from the reference by
+``tests/golden/make_golden.py``)."""
+
+from __future__ import annotations
+
+import os
+
+import numpy as np
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def _load(name):
+    return np.load(os.path.join(GOLDEN, name))
+
+
+def param_sets():
+    """List of dicts: model-derived per_token_bytes + selection scalars."""
+    z = _load("select.npz")
+    out = []
+    for L, H, D, w, cs, ob, tmpl, mc, cstep, istep in z["param_sets"]:
+        out.append(dict(per_token_bytes=int(2 * int(L) * int(H) * int(D) * float(w)),
+                        chunk_size=int(cs), out_budget=int(ob), template_tokens=int(tmpl),
+                        max_chunks=int(mc), chunk_step=int(cstep), interlen_step=int(istep)))
+    return out
+
+
+def select_rows():
+    """int64 [n, 16]: ps, methods, n_lo, n_hi, il_lo, il_hi, joint, qlen, free,
+    m, n, il, bytes, status, tie."""
+    return _load("select.npz")["rows"]
+
+
+def mapping():
+    z = _load("mapping.npz")
+    return z["profiles"], z["spaces"]
+
+
+def gate_sequences():
+    z = _load("gate.npz")
+    seqs = []
+    for i in range(int(z["count"])):
+        g = lambda k: z[f"{i}_{k}"]  # noqa: E731
+        seqs.append(dict(name=str(g("name")), profiles=g("profiles"), conf=g("conf"),
+                         expected=g("expected"), threshold=float(g("threshold")),
+                         default_space=tuple(int(x) for x in g("default_space")),
+                         max_chunks=int(g("max_chunks")),
+                         prefill=[tuple(int(x) for x in r) for r in g("prefill")]))
+    return seqs
+
+
+def latency():
+    z = _load("latency.npz")
+    return {k: z[k] for k in z.files}
+
+
+def known():
+    z = _load("known.npz")
+    return {k: z[k].item() for k in z.files}
