@@ -1,0 +1,226 @@
+/*
+ * ragsched_b200 — C ABI of the B200-native METIS per-query hot path.
+ *
+ * Drop-in boundary for the data-parallel path of the reference package
+ * `ragsched` (/root/reference/pkg/src/ragsched/):
+ *
+ *   confidence gate + Algorithm-1 pruning  profiler.py:467-486, mapping.py:106-126,
+ *                                          mapping.py:180-200 (window hull)
+ *   KV-memory + best-fit + fallback        memory.py:70-78, memory.py:164-195,
+ *                                          scheduler.py:127-191, order of
+ *                                          Scheduler._try_admit_new scheduler.py:335-378
+ *   prefill/decode delay model             sim.py:42-57, sim.py:84-92 (call_latency),
+ *                                          dispatch order sim.py:223-229
+ *   dense chunk retrieval                  absent from the reference; the
+ *                                          paper's FAISS IndexFlatL2 `index.search(q, k)`
+ *
+ *
+ * The reference has no FFI of its own (it is pure Python; its callers resolve
+ * these functions by module attribute, scheduler.py:340/:360,
+ * profiler.py:534-541).  The Python package paper_2412_10543_b200 binds this
+ * header with ctypes (see INTEGRATION.md for the binding a ragsched
+ * maintainer would add).
+ *
+ * Conventions
+ *  - every pointer argument documented "device" is a device pointer (cudaMalloc /
+ *    torch CUDA tensor data); "host" pointers are plain host memory;
+ *  - every launch takes a cudaStream_t passed as `void*` and is stream-ordered;
+ *    no entry point synchronises the device except rs_index_add/… where noted;
+ *  - return value 0 = RS_OK, otherwise an RS_ERR_* code; rs_last_error()
+ *    returns a thread-local message for the last failure.  Nothing throws.
+ *  - the library never falls back to the CPU.
+ */
+#ifndef RAGSCHED_B200_H
+#define RAGSCHED_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RS_ABI_VERSION 1
+
+enum rs_status {
+  RS_OK = 0,
+  RS_ERR_INVALID_ARG = 1, /* reference: ValueError                              */
+  RS_ERR_CUDA = 2,
+  RS_ERR_UNSUPPORTED = 3, /* e.g. no sm_100 device                              */
+  RS_ERR_OOM = 4,
+  RS_ERR_OVERFLOW = 5     /* int64 byte arithmetic would overflow               */
+};
+
+/* Synthesis-method bits in the reference grid order METHOD_ORDER (mapping.py:24). */
+enum rs_method { RS_MAP_RERANK = 1, RS_STUFF = 2, RS_MAP_REDUCE = 4 };
+
+/* Per-query decision (Scheduler._try_admit_new, scheduler.py:335-378). */
+enum rs_select_status {
+  RS_SELECT_BEST_FIT = 0,   /* best_fit_select returned a config                 */
+  RS_SELECT_FALLBACK = 1,   /* best_fit_select -> None, fallback_config -> config */
+  RS_SELECT_MUST_QUEUE = 2, /* both None: the query stays queued                 */
+  RS_SELECT_OVERFLOW = 3    /* inputs exceed the int64 byte range (error)        */
+};
+
+/* QueryProfile (mapping.py:31-48), 16 bytes. */
+typedef struct rs_profile {
+  uint8_t complexity_high;
+  uint8_t needs_joint_reasoning;
+  uint16_t pieces_required;
+  uint16_t summary_lo, summary_hi; /* summary_len_range                         */
+  double confidence;
+} rs_profile;
+
+/* PrunedConfigSpace (mapping.py:51-83), 16 bytes.  interlen_lo/hi are 0 when
+ * RS_MAP_REDUCE is not in `methods` (the reference's None range). */
+typedef struct rs_space {
+  uint16_t methods;
+  uint16_t num_chunks_lo, num_chunks_hi;
+  uint16_t interlen_lo, interlen_hi;
+  uint16_t gate_fallback; /* GateDecision.used_fallback (profiler.py:157-163)   */
+  uint32_t reserved;
+} rs_space;
+
+/* Chosen RagConfig (types.py:66-81) plus its whole-plan bytes, 16 bytes. */
+typedef struct rs_config {
+  int64_t kv_bytes;    /* plan_bytes(...) of the chosen config (memory.py:164)  */
+  uint8_t method;      /* rs_method bit; 0 when status != BEST_FIT/FALLBACK     */
+  uint8_t status;      /* rs_select_status                                      */
+  uint16_t num_chunks;
+  uint16_t interlen;   /* 0 == None                                             */
+  uint16_t reserved;
+} rs_config;
+
+/* Scalars of best_fit_select / fallback_config (scheduler.py:127-191). */
+typedef struct rs_select_params {
+  int64_t per_token_bytes; /* bytes_per_kv_token(model), memory.py:70-73          */
+  int32_t chunk_size;      /* DatasetMeta.chunk_size                              */
+  int32_t out_budget;
+  int32_t template_tokens; /* DEFAULT_TEMPLATE_TOKENS = 64 (types.py:13)          */
+  int32_t max_chunks;      /* DEFAULT_MAX_CHUNKS = 35 (types.py:12)               */
+  int32_t chunk_step;      /* EnumGranularity (mapping.py:86-95)                  */
+  int32_t interlen_step;
+  int32_t allow_fallback;  /* SchedulerParams.allow_fallback (scheduler.py:55)    */
+  int32_t reserved;
+} rs_select_params;
+
+/* CostModel latency terms (sim.py:42-57). */
+typedef struct rs_cost_model {
+  double prefill_secs_per_token;
+  double decode_secs_per_token_base;
+  double batch_slowdown_per_seq;
+} rs_cost_model;
+
+/* gate_profile parameters (profiler.py:467-477). */
+typedef struct rs_gate_params {
+  double threshold;       /* GATE_THRESHOLD = 0.90; must be in (0, 1]          */
+  rs_space default_space; /* DEFAULT_FALLBACK_SPACE = stuff [1,5]               */
+  int32_t max_chunks;
+  int32_t reserved;
+} rs_gate_params;
+
+/* Gate window carried across batches: RecentSpaceWindow (profiler.py:138-153). */
+#define RS_WINDOW_CAPACITY 10
+typedef struct rs_window {
+  rs_space spaces[RS_WINDOW_CAPACITY]; /* oldest first                           */
+  int32_t len;
+  int32_t reserved[3];
+} rs_window;
+
+/* ---- library ------------------------------------------------------------ */
+int rs_abi_version(void);
+const char* rs_last_error(void);
+/* 1 when `device` is an sm_100 part this library was compiled for. */
+int rs_device_supported(int device);
+
+/* ---- config path ---------------------------------------------------------
+ * rs_prune_gate: gate_profile applied to a batch IN ORDER (the window couples
+ * each query to the last <=10 accepted before it).  profiles/spaces_out are
+ * device arrays of n; window_io is a device rs_window read as the carry-in
+ * state and overwritten with the state after the batch; workspace is a device
+ * buffer of rs_prune_gate_workspace_size(n) bytes.  Replaces, per query,
+ * QueryProfiler.gate -> gate_profile -> map_profile | window.hull()
+ * (profiler.py:534-541, :467-486). */
+size_t rs_prune_gate_workspace_size(int64_t n);
+int rs_prune_gate(const rs_profile* profiles, int64_t n, const rs_gate_params* params /* host */,
+                  rs_window* window_io, rs_space* spaces_out, void* workspace, size_t workspace_bytes,
+                  void* stream);
+
+/* rs_select: best_fit_select then fallback_config for every query
+ * independently (scheduler.py:127-191 in the order of :335-378).  spaces,
+ * profiles (only .needs_joint_reasoning is read, by the fallback — the
+ * reference passes `pending.profile`, scheduler.py:360-369; may be NULL when
+ * allow_fallback == 0), qlen (query_token_len) and free_bytes are device
+ * arrays of n.  If `cost` is non-NULL, delay_out (device, n doubles) receives
+ * the chosen plan's critical-path delay under call_latency (sim.py:84-92)
+ * with the sim's dispatch concurrency (sim.py:223-229) starting from
+ * running_before[i] (device, may be NULL = 0). */
+int rs_select(const rs_space* spaces, const rs_profile* profiles, const int32_t* qlen,
+              const int64_t* free_bytes, int64_t n, const rs_select_params* params /* host */,
+              const rs_cost_model* cost /* host, nullable */, const int32_t* running_before,
+              double* delay_out, rs_config* out, void* stream);
+
+/* rs_call_latency: sim.call_latency (sim.py:84-92) element-wise, bit-exact
+ * IEEE double in the reference's evaluation order. */
+int rs_call_latency(const int64_t* prompt_tokens, const int64_t* max_output_tokens,
+                    const int64_t* concurrent_seqs, int64_t n, const rs_cost_model* cost /* host */,
+                    double* out, void* stream);
+
+/* rs_plan_bytes: memory.plan_bytes (memory.py:164-195) element-wise over
+ * configs (method bit, num_chunks, interlen) and query lengths. */
+int rs_plan_bytes(const uint8_t* method, const int32_t* num_chunks, const int32_t* interlen,
+                  const int32_t* qlen, int64_t n, const rs_select_params* params /* host */,
+                  int64_t* out, void* stream);
+
+/* ---- retrieval (FAISS IndexFlatL2 semantics) ----------------
+ * An index owns one corpus shard in HBM: row-major [ntotal, dim] embeddings of
+ * `dtype` plus fp32 squared norms.  Search returns, per query, the k smallest
+ * D = ||q||^2 + ||c||^2 - 2<q,c> (fp32 accumulate, clamped at 0), ascending,
+ * ties to the lower chunk id; missing entries are I = -1, D = +inf.
+ * Chunk ids are id_base + row (id_base = the shard's first global id). */
+enum rs_dtype { RS_F32 = 0, RS_BF16 = 1 };
+enum rs_algo { RS_ALGO_AUTO = 0, RS_ALGO_SIMT = 1, RS_ALGO_TCGEN05 = 2 };
+
+typedef struct rs_index rs_index;
+
+int rs_index_create(int32_t dim, int32_t dtype, int64_t capacity, int32_t device, rs_index** out);
+int rs_index_destroy(rs_index* index);
+/* Append n device rows (copied; norms computed on device). */
+int rs_index_add(rs_index* index, const void* embeddings, int64_t n, void* stream);
+int rs_index_reset(rs_index* index);
+int rs_index_ntotal(const rs_index* index, int64_t* out);
+/* Device pointers of the stored corpus / norms (read-only views). */
+int rs_index_data(const rs_index* index, const void** embeddings, const float** norms);
+int rs_index_set_algo(rs_index* index, int32_t algo);
+/* Preallocate the search workspace for up to nq_max queries of k results. */
+int rs_index_reserve(rs_index* index, int64_t nq_max, int32_t k);
+/* Search: queries device [nq, dim] of the index dtype; D device [nq,k] fp32,
+ * I device [nq,k] int64.  If `keep` (device, nq rs_config) is non-NULL only
+ * the first keep[q].num_chunks results of a selected query are returned
+ * (the join of PAPER.md:377); MustQueue queries get none. */
+int rs_index_search(rs_index* index, const void* queries, int64_t nq, int32_t k, int64_t id_base,
+                    const rs_config* keep, float* D, int64_t* I, void* stream);
+/* Same search, but emits the per-query sorted top-k as packed keys
+ * (fp32 distance bits << 32 | uint32 global id; UINT64_MAX = missing) for a
+ * later cross-shard rs_merge_topk. */
+int rs_index_search_keys(rs_index* index, const void* queries, int64_t nq, int32_t k,
+                         int64_t id_base, uint64_t* keys, void* stream);
+/* Last search's work split (segments of the corpus, query tiles, grid). */
+int rs_index_last_plan(const rs_index* index, int32_t* segments, int32_t* qtiles, int32_t* ctas,
+                       int32_t* algo);
+
+/* k-way merge of sorted key lists: list l of query q starts at
+ * keys[l*list_stride + q*k_in]; produces the k smallest by (distance, id).
+ * If `cfg` is non-NULL only the first cfg[q].num_chunks results are kept
+ * (the join "retrieve the selected number of chunks") and the
+ * rest are I = -1 / D = +inf. */
+int rs_merge_topk(const uint64_t* keys, int64_t nq, int32_t nlists, int32_t k_in, int64_t list_stride,
+                  int32_t k, const rs_config* cfg, float* D, int64_t* I, void* stream);
+
+/* Squared L2 norms of n rows of `dtype` (fp32 accumulate). */
+int rs_row_norms(const void* x, int64_t n, int32_t dim, int32_t dtype, float* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RAGSCHED_B200_H */

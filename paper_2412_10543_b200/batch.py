@@ -1,0 +1,276 @@
+"""Batched SoA entry points of the config path (the fast path).
+
+Inputs and outputs are device tensors holding the C structs of
+``include/ragsched_b200.h`` as raw bytes (``uint8 [n, 16]``); the helpers here
+pack / unpack them from the reference-style objects.  Every compute step is a
+kernel of ``libragsched_b200.so``:
+
+* :func:`prune_gate`  — ``gate_profile`` over a batch in order
+  (profiler.py:467-486) → ``rs_prune_gate``
+* :func:`select`      — ``best_fit_select`` → ``fallback_config`` per query
+  (scheduler.py:127-191, :335-378) + optional delay → ``rs_select``
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import CONFIG_DTYPE, PROFILE_DTYPE, SPACE_DTYPE, WINDOW_DTYPE
+from .types import (
+    BIT_METHOD,
+    DEFAULT_MAX_CHUNKS,
+    DEFAULT_TEMPLATE_TOKENS,
+    IntRange,
+    RagConfig,
+    SynthesisMethod,
+    method_bit,
+)
+
+GATE_THRESHOLD = 0.90  # profiler.py:30
+
+
+def bytes_per_kv_token(model) -> int:
+    """memory.py:70-73 (host scalar: a parameter of the select kernel)."""
+    return int(2 * model.num_layers * model.num_kv_heads * model.head_dim * model.bytes_per_element)
+
+
+@dataclass(frozen=True)
+class SelectParams:
+    """Host mirror of ``rs_select_params`` (the scalars of best_fit_select /
+    fallback_config, scheduler.py:127-191)."""
+
+    per_token_bytes: int
+    chunk_size: int
+    out_budget: int
+    template_tokens: int = DEFAULT_TEMPLATE_TOKENS
+    max_chunks: int = DEFAULT_MAX_CHUNKS
+    chunk_step: int = 1
+    interlen_step: int = 10
+    allow_fallback: bool = True
+
+    @classmethod
+    def from_model(cls, model, meta, out_budget, template_tokens=DEFAULT_TEMPLATE_TOKENS,
+                   max_chunks=DEFAULT_MAX_CHUNKS, granularity=None, allow_fallback=True):
+        cs = granularity.chunk_step if granularity is not None else 1
+        ist = granularity.interlen_step if granularity is not None else 10
+        return cls(bytes_per_kv_token(model), int(meta.chunk_size), int(out_budget), int(template_tokens),
+                   int(max_chunks), int(cs), int(ist), bool(allow_fallback))
+
+    def c(self) -> _lib.SelectParamsC:
+        return _lib.SelectParamsC(self.per_token_bytes, self.chunk_size, self.out_budget, self.template_tokens,
+                                  self.max_chunks, self.chunk_step, self.interlen_step,
+                                  int(self.allow_fallback), 0)
+
+
+@dataclass(frozen=True)
+class CostModel:
+    """sim.py:42-57 (the latency terms; the profiler latency is not a kernel input)."""
+
+    prefill_secs_per_token: float = 1.0e-4
+    decode_secs_per_token_base: float = 4.0e-3
+    batch_slowdown_per_seq: float = 0.01
+    profiler_latency_secs: float = 0.015
+
+    def c(self) -> _lib.CostModelC:
+        return _lib.CostModelC(self.prefill_secs_per_token, self.decode_secs_per_token_base,
+                               self.batch_slowdown_per_seq)
+
+
+# -- packing -------------------------------------------------------------------
+
+def pack_profiles(profiles) -> np.ndarray:
+    """QueryProfile-like objects -> structured array of rs_profile."""
+    a = np.zeros(len(profiles), dtype=PROFILE_DTYPE)
+    for i, p in enumerate(profiles):
+        a[i] = (bool(p.complexity_high), bool(p.needs_joint_reasoning), int(p.pieces_required),
+                int(p.summary_len_range.low), int(p.summary_len_range.high), float(p.confidence))
+    return a
+
+
+def profiles_from_arrays(complexity_high, joint, pieces, summary_lo, summary_hi, confidence) -> np.ndarray:
+    n = len(confidence)
+    a = np.zeros(n, dtype=PROFILE_DTYPE)
+    a["complexity_high"] = np.asarray(complexity_high, dtype=np.uint8)
+    a["needs_joint_reasoning"] = np.asarray(joint, dtype=np.uint8)
+    a["pieces_required"] = np.asarray(pieces, dtype=np.uint16)
+    a["summary_lo"] = np.asarray(summary_lo, dtype=np.uint16)
+    a["summary_hi"] = np.asarray(summary_hi, dtype=np.uint16)
+    a["confidence"] = np.asarray(confidence, dtype=np.float64)
+    return a
+
+
+def _u16(v, what):
+    v = int(v)
+    if not 0 <= v <= 0xFFFF:
+        raise ValueError(f"{what} {v} outside the supported range [0, 65535]")
+    return v
+
+
+def space_record(space) -> tuple:
+    """PrunedConfigSpace-like -> (methods, n_lo, n_hi, il_lo, il_hi)."""
+    m = 0
+    for x in space.synthesis_methods:
+        m |= method_bit(x)
+    il = space.intermediate_length_range
+    if m & 4 and il is not None and il.low <= 0:
+        raise ValueError("map_reduce config requires a positive intermediate_length")
+    return (m, _u16(space.num_chunks_range.low, "num_chunks"), _u16(space.num_chunks_range.high, "num_chunks"),
+            _u16(il.low, "intermediate_length") if (m & 4 and il is not None) else 0,
+            _u16(il.high, "intermediate_length") if (m & 4 and il is not None) else 0)
+
+
+def pack_spaces(spaces) -> np.ndarray:
+    a = np.zeros(len(spaces), dtype=SPACE_DTYPE)
+    for i, s in enumerate(spaces):
+        m, lo, hi, a0, b0 = space_record(s)
+        a[i]["methods"], a[i]["num_chunks_lo"], a[i]["num_chunks_hi"] = m, lo, hi
+        a[i]["interlen_lo"], a[i]["interlen_hi"] = a0, b0
+    return a
+
+
+def spaces_from_arrays(methods, n_lo, n_hi, il_lo, il_hi) -> np.ndarray:
+    a = np.zeros(len(methods), dtype=SPACE_DTYPE)
+    for f, v in (("methods", methods), ("num_chunks_lo", n_lo), ("num_chunks_hi", n_hi),
+                 ("interlen_lo", il_lo), ("interlen_hi", il_hi)):
+        a[f] = np.asarray(v, dtype=np.uint16)
+    return a
+
+
+def unpack_space(rec, *, space_cls=None, method_enum=SynthesisMethod, range_cls=IntRange):
+    from .mapping import PrunedConfigSpace
+
+    space_cls = space_cls or PrunedConfigSpace
+    m = int(rec["methods"])
+    methods = frozenset(method_enum(BIT_METHOD[b].value) for b in (1, 2, 4) if m & b)
+    il = range_cls(int(rec["interlen_lo"]), int(rec["interlen_hi"])) if m & 4 else None
+    return space_cls(methods, range_cls(int(rec["num_chunks_lo"]), int(rec["num_chunks_hi"])), il)
+
+
+def unpack_config(rec, *, config_cls=RagConfig, method_enum=SynthesisMethod):
+    """rs_config record -> RagConfig (None for MustQueue)."""
+    st = int(rec["status"])
+    if st == _lib.RS_SELECT_OVERFLOW:
+        raise OverflowError("KV byte arithmetic exceeds int64 for this query")
+    if st == _lib.RS_SELECT_MUST_QUEUE:
+        return None
+    m = BIT_METHOD[int(rec["method"])]
+    me = method_enum(m.value)
+    il = int(rec["interlen"]) if m is SynthesisMethod.MAP_REDUCE else None
+    return config_cls(me, int(rec["num_chunks"]), il)
+
+
+def to_device(arr: np.ndarray, device) -> torch.Tensor:
+    """Structured numpy array -> device uint8 tensor [n, itemsize]."""
+    raw = np.ascontiguousarray(arr).view(np.uint8).reshape(len(arr), arr.dtype.itemsize)
+    return torch.from_numpy(raw).to(device, non_blocking=False)
+
+
+def from_device(t: torch.Tensor, dtype: np.dtype) -> np.ndarray:
+    return t.detach().to("cpu").contiguous().numpy().reshape(-1).view(dtype)
+
+
+def _dev_index(t: torch.Tensor) -> int:
+    if t.device.type != "cuda":
+        raise ValueError(f"expected a CUDA tensor, got {t.device}")
+    return t.device.index if t.device.index is not None else torch.cuda.current_device()
+
+
+# -- gate window state ----------------------------------------------------------
+
+class GateWindow:
+    """Device-resident RecentSpaceWindow (profiler.py:138-153) carried across
+    batches, as the ``rs_window`` struct."""
+
+    def __init__(self, device, spaces=()):
+        rec = np.zeros(1, dtype=WINDOW_DTYPE)
+        spaces = list(spaces)[-_lib.WINDOW_CAPACITY:]
+        if spaces:
+            rec["spaces"][0, :len(spaces)] = pack_spaces(spaces)
+        rec["len"] = len(spaces)
+        self.tensor = to_device(rec, device).reshape(-1)
+
+    def records(self) -> np.ndarray:
+        rec = from_device(self.tensor, WINDOW_DTYPE)[0]
+        return rec["spaces"][: int(rec["len"])]
+
+
+# -- kernels ----------------------------------------------------------------------
+
+def prune_gate(profiles: torch.Tensor, window: GateWindow, *, threshold: float = GATE_THRESHOLD,
+               default_space=None, max_chunks: int = DEFAULT_MAX_CHUNKS, out: torch.Tensor | None = None,
+               workspace: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """gate_profile for a device batch of rs_profile (uint8 [n,16]) in order.
+    Returns device rs_space records (uint8 [n,16]); ``window`` is updated."""
+    n = profiles.shape[0]
+    dev = _dev_index(profiles)
+    lib = _lib.lib_for_device(dev)
+    if out is None:
+        out = torch.empty((n, 16), dtype=torch.uint8, device=profiles.device)
+    ws_bytes = int(lib.rs_prune_gate_workspace_size(n))
+    if workspace is None or workspace.numel() < ws_bytes:
+        workspace = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=profiles.device)
+    if default_space is None:
+        ds = (2, 1, 5, 0, 0)  # DEFAULT_FALLBACK_SPACE = stuff [1,5] (profiler.py:40-42)
+    else:
+        ds = space_record(default_space) if hasattr(default_space, "synthesis_methods") else tuple(default_space)
+    gp = _lib.GateParamsC(float(threshold), _lib.SpaceC(ds[0], ds[1], ds[2], ds[3], ds[4], 1, 0), int(max_chunks), 0)
+    _lib.check(lib.rs_prune_gate(_lib.ptr(profiles), n, ctypes.byref(gp), _lib.ptr(window.tensor), _lib.ptr(out),
+                                 _lib.ptr(workspace), workspace.numel(), _lib.stream_ptr(stream)), "rs_prune_gate")
+    return out
+
+
+def select(spaces: torch.Tensor, profiles: torch.Tensor | None, qlen: torch.Tensor, free_bytes: torch.Tensor,
+           params: SelectParams, *, cost: CostModel | None = None, running_before: torch.Tensor | None = None,
+           out: torch.Tensor | None = None, delay: torch.Tensor | None = None, stream=None):
+    """best_fit_select -> fallback_config for each query of a device batch.
+    Returns (configs uint8 [n,16] of rs_config, delay float64 [n] or None)."""
+    n = spaces.shape[0]
+    dev = _dev_index(spaces)
+    lib = _lib.lib_for_device(dev)
+    if qlen.dtype != torch.int32 or free_bytes.dtype != torch.int64:
+        raise TypeError("qlen must be int32 and free_bytes int64 device tensors")
+    if out is None:
+        out = torch.empty((n, 16), dtype=torch.uint8, device=spaces.device)
+    cp = None
+    if cost is not None:
+        cp = ctypes.byref(cost.c())
+        if delay is None:
+            delay = torch.empty(n, dtype=torch.float64, device=spaces.device)
+    pc = params.c()
+    _lib.check(lib.rs_select(_lib.ptr(spaces), _lib.ptr(profiles), _lib.ptr(qlen), _lib.ptr(free_bytes), n,
+                             ctypes.byref(pc), cp, _lib.ptr(running_before), _lib.ptr(delay) if cost else 0,
+                             _lib.ptr(out), _lib.stream_ptr(stream)), "rs_select")
+    return out, (delay if cost is not None else None)
+
+
+def call_latency_batch(prompt_tokens: torch.Tensor, max_output_tokens: torch.Tensor, concurrent: torch.Tensor,
+                       cost: CostModel, stream=None) -> torch.Tensor:
+    n = prompt_tokens.shape[0]
+    lib = _lib.lib_for_device(_dev_index(prompt_tokens))
+    out = torch.empty(n, dtype=torch.float64, device=prompt_tokens.device)
+    c = cost.c()
+    _lib.check(lib.rs_call_latency(_lib.ptr(prompt_tokens), _lib.ptr(max_output_tokens), _lib.ptr(concurrent), n,
+                                   ctypes.byref(c), _lib.ptr(out), _lib.stream_ptr(stream)), "rs_call_latency")
+    return out
+
+
+def plan_bytes_batch(method: torch.Tensor, num_chunks: torch.Tensor, interlen: torch.Tensor, qlen: torch.Tensor,
+                     params: SelectParams, stream=None) -> torch.Tensor:
+    n = method.shape[0]
+    lib = _lib.lib_for_device(_dev_index(method))
+    out = torch.empty(n, dtype=torch.int64, device=method.device)
+    pc = params.c()
+    _lib.check(lib.rs_plan_bytes(_lib.ptr(method), _lib.ptr(num_chunks), _lib.ptr(interlen), _lib.ptr(qlen), n,
+                                 ctypes.byref(pc), _lib.ptr(out), _lib.stream_ptr(stream)), "rs_plan_bytes")
+    return out
+
+
+def default_device() -> torch.device:
+    if not torch.cuda.is_available():
+        raise _lib.LibraryUnavailable("no CUDA device: paper_2412_10543_b200 runs only on a B200 (no CPU fallback)")
+    return torch.device("cuda", torch.cuda.current_device())

@@ -1,0 +1,605 @@
+// Retrieval: the index handle (rs_index_*), row norms, the CUDA-core fused
+// score+top-k kernel (fp32 corpora and a bf16 cross-check path), the k-way
+// top-k merge (K2) and the search planner.  FAISS IndexFlatL2 semantics
+// (PAPER.md:653): D = |q|^2 + |c|^2 - 2<q,c> clamped at 0, ascending, ties to
+// the lower chunk id, missing results I = -1 / D = +inf.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "retrieval.cuh"
+#include "topk_rows.cuh"
+
+namespace rs {
+namespace {
+
+template <typename T>
+__device__ __forceinline__ float to_f(T v);
+template <>
+__device__ __forceinline__ float to_f<float>(float v) {
+  return v;
+}
+template <>
+__device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 v) {
+  return __bfloat162float(v);
+}
+
+// ---- squared norms: one warp per row, fp32 accumulate ---------------------
+template <typename T>
+__global__ void __launch_bounds__(256) row_norms_kernel(const T* __restrict__ x, int64_t n, int dim,
+                                                        float* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t r = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r < n;
+       r += (int64_t(gridDim.x) * blockDim.x) >> 5) {
+    const T* row = x + r * dim;
+    float s = 0.0f;
+    for (int i = lane; i < dim; i += 32) {
+      const float v = to_f(row[i]);
+      s = fmaf(v, v, s);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (lane == 0) out[r] = s;
+  }
+}
+
+// ---- CUDA-core fused score + top-k ------------------------------------------
+// CTA = 64 queries x 64 corpus rows per tile, 256 threads each holding a 4x4
+// micro-tile of dot products; distances go through a smem tile and one thread
+// per query feeds its RowTopK.
+constexpr int BQ = kSimtBQ, BC = kSimtBC, BKS = 32;
+
+template <typename T, int KCAP, int BUF>
+__global__ void __launch_bounds__(256) score_topk_simt_kernel(const T* __restrict__ Q, const float* __restrict__ qn,
+                                                              int64_t nq, const T* __restrict__ C,
+                                                              const float* __restrict__ cn, int64_t n, int dim, int k,
+                                                              int64_t id_base, int qtiles, int segments,
+                                                              int64_t seg_rows, uint64_t* __restrict__ part) {
+  __shared__ float As[BKS][BQ + 4];
+  __shared__ float Bs[BKS][BC + 4];
+  __shared__ float Sd[BQ][BC + 1];
+  extern __shared__ uint64_t simt_dyn[];  // heap [KCAP][BQ] then buffer [BUF][BQ]
+  uint64_t* heap = simt_dyn;
+  uint64_t* bufm = simt_dyn + KCAP * BQ;
+  const int tid = threadIdx.x;
+  const int tq = tid >> 4, tc = tid & 15;
+  const int64_t units = int64_t(qtiles) * segments;
+  RowTopK<BQ, BUF> rt{heap, bufm, tid & (BQ - 1), k, 0, 0, 0.0f};
+
+  for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+    const int seg = int(u / qtiles);
+    const int qt = int(u - int64_t(seg) * qtiles);
+    const int64_t r0 = int64_t(seg) * seg_rows;
+    const int64_t r1 = std::min<int64_t>(n, r0 + seg_rows);
+    const int64_t q0 = int64_t(qt) * BQ;
+    if (tid < BQ) rt.reset();
+    for (int64_t c0 = r0; c0 < r1; c0 += BC) {
+      float acc[4][4] = {};
+      for (int k0 = 0; k0 < dim; k0 += BKS) {
+#pragma unroll
+        for (int i = 0; i < (BQ * BKS) / 256; ++i) {
+          const int idx = tid + i * 256;
+          const int rr = idx / BKS, kk = idx % BKS;
+          const int64_t qrow = q0 + rr, crow = c0 + rr;
+          const bool kin = k0 + kk < dim;
+          As[kk][rr] = (qrow < nq && kin) ? to_f(Q[qrow * dim + k0 + kk]) : 0.0f;
+          Bs[kk][rr] = (crow < r1 && kin) ? to_f(C[crow * dim + k0 + kk]) : 0.0f;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int kk = 0; kk < BKS; ++kk) {
+          float a[4], b[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            a[i] = As[kk][tq + 16 * i];
+            b[i] = Bs[kk][tc + 16 * i];
+          }
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+        }
+        __syncthreads();
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int64_t qrow = q0 + tq + 16 * i;
+        const float qv = qrow < nq ? qn[qrow] : 0.0f;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int64_t crow = c0 + tc + 16 * j;
+          const float cv = crow < r1 ? cn[crow] : 0.0f;
+          Sd[tq + 16 * i][tc + 16 * j] = l2_from_dot(qv + cv, acc[i][j]);
+        }
+      }
+      __syncthreads();
+      if (tid < BQ) {
+        const int valid = int(std::min<int64_t>(BC, r1 - c0));
+        const uint32_t id0 = uint32_t(id_base + c0);
+        for (int c = 0; c < BC; c += 16) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (c + j < valid) rt.offer(Sd[tid][c + j], id0 + c + j);
+          if (__any_sync(0xffffffffu, rt.nb > BUF - 16)) rt.flush();
+        }
+      }
+      __syncthreads();
+    }
+    if (tid < BQ && q0 + tid < nq) rt.finish(part + ((q0 + tid) * segments + seg) * k);
+  }
+}
+
+// ---- K2: k-way merge of sorted key lists (one warp per query) -----------------
+// List l of query q: keys[q * q_stride + l * list_stride + j], j < k_in, sorted
+// ascending (kEmptyKey-padded).  Tournament: every lane tracks the head of
+// lists lane, lane+32, ...; per output the warp arg-min picks the winner list
+// and only the owning lane advances and rescans.
+constexpr int kMergeWarps = 8;
+
+__device__ __forceinline__ uint64_t shfl_u64(uint64_t v, int src) {
+  const uint32_t lo = __shfl_sync(0xffffffffu, uint32_t(v), src);
+  const uint32_t hi = __shfl_sync(0xffffffffu, uint32_t(v >> 32), src);
+  return (uint64_t(hi) << 32) | lo;
+}
+
+__global__ void __launch_bounds__(kMergeWarps * 32) merge_topk_kernel(
+    const uint64_t* __restrict__ keys, int64_t nq, int nlists, int k_in, int64_t list_stride, int64_t q_stride,
+    int k, const rs_config* __restrict__ keep, float* __restrict__ D, int64_t* __restrict__ I,
+    uint64_t* __restrict__ keys_out) {
+  extern __shared__ uint8_t heads_all[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint8_t* heads = heads_all + size_t(w) * nlists;
+  for (int64_t q = int64_t(blockIdx.x) * kMergeWarps + w; q < nq; q += int64_t(gridDim.x) * kMergeWarps) {
+    const uint64_t* base = keys + q * q_stride;
+    for (int l = lane; l < nlists; l += 32) heads[l] = 0;
+    __syncwarp();
+    // lane-local minimum over its lists
+    uint64_t best = kEmptyKey;
+    int best_l = -1;
+    for (int l = lane; l < nlists; l += 32) {
+      const uint64_t v = base[int64_t(l) * list_stride];
+      if (v < best || best_l < 0) {
+        best = v;
+        best_l = l;
+      }
+    }
+    int limit = k;
+    if (keep) {
+      const rs_config c = keep[q];
+      limit = (c.status == RS_SELECT_BEST_FIT || c.status == RS_SELECT_FALLBACK) ? c.num_chunks : 0;
+      if (limit > k) limit = k;
+    }
+    for (int j = 0; j < k; ++j) {
+      uint64_t v = best;
+      int src = lane;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const uint64_t ov = shfl_u64(v, lane ^ off);
+        const int os = __shfl_xor_sync(0xffffffffu, src, off);
+        if (ov < v || (ov == v && os < src)) {
+          v = ov;
+          src = os;
+        }
+      }
+      const bool real = v != kEmptyKey && j < limit;
+      if (lane == 0) {
+        if (keys_out) keys_out[q * k + j] = real ? v : kEmptyKey;
+        if (D) D[q * k + j] = real ? key_dist(v) : __int_as_float(0x7f800000);
+        if (I) I[q * k + j] = real ? int64_t(uint32_t(v)) : int64_t(-1);
+      }
+      if (v == kEmptyKey || j + 1 >= limit) {
+        // remaining outputs are padding
+        for (int jj = j + 1 + lane; jj < k; jj += 32) {
+          if (keys_out) keys_out[q * k + jj] = kEmptyKey;
+          if (D) D[q * k + jj] = __int_as_float(0x7f800000);
+          if (I) I[q * k + jj] = -1;
+        }
+        break;
+      }
+      if (lane == src) {
+        // advance the winning list, rescan this lane's heads
+        const int h = heads[best_l] + 1;
+        heads[best_l] = (uint8_t)h;
+        best = kEmptyKey;
+        int bl = -1;
+        for (int l = lane; l < nlists; l += 32) {
+          const int hh = heads[l];
+          const uint64_t cand = hh < k_in ? base[int64_t(l) * list_stride + hh] : kEmptyKey;
+          if (cand < best || bl < 0) {
+            best = cand;
+            bl = l;
+          }
+        }
+        best_l = bl;
+      }
+      __syncwarp();
+    }
+    __syncwarp();
+  }
+}
+
+__global__ void fill_empty_kernel(int64_t n, float* D, int64_t* I, uint64_t* keys) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    if (D) D[i] = __int_as_float(0x7f800000);
+    if (I) I[i] = -1;
+    if (keys) keys[i] = kEmptyKey;
+  }
+}
+
+int launch_merge(const uint64_t* keys, int64_t nq, int nlists, int k_in, int64_t list_stride, int64_t q_stride,
+                 int k, const rs_config* keep, float* D, int64_t* I, uint64_t* keys_out, cudaStream_t st) {
+  RS_REQUIRE(nlists >= 1 && nlists <= 4096, "nlists out of range (%d)", nlists);
+  RS_REQUIRE(k_in >= 1 && k_in <= 255, "k_in out of range (%d)", k_in);
+  const size_t smem = size_t(kMergeWarps) * nlists;
+  const int64_t blocks = std::min<int64_t>(ceil_div(nq, kMergeWarps), 65535);
+  if (smem > 48 * 1024) {
+    RS_CHECK_CUDA(cudaFuncSetAttribute(merge_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
+                  "cudaFuncSetAttribute(merge_topk_kernel)");
+  }
+  merge_topk_kernel<<<(unsigned)blocks, kMergeWarps * 32, smem, st>>>(keys, nq, nlists, k_in, list_stride, q_stride,
+                                                                       k, keep, D, I, keys_out);
+  RS_CHECK_LAUNCH("merge_topk_kernel");
+  return RS_OK;
+}
+
+int launch_norms(const void* x, int64_t n, int dim, int dtype, float* out, cudaStream_t st) {
+  if (n <= 0) return RS_OK;
+  const int64_t blocks = std::min<int64_t>(ceil_div(n * 32, 256), 148 * 64);
+  if (dtype == RS_BF16)
+    row_norms_kernel<__nv_bfloat16><<<(unsigned)blocks, 256, 0, st>>>((const __nv_bfloat16*)x, n, dim, out);
+  else
+    row_norms_kernel<float><<<(unsigned)blocks, 256, 0, st>>>((const float*)x, n, dim, out);
+  RS_CHECK_LAUNCH("row_norms_kernel");
+  return RS_OK;
+}
+
+template <typename T, int KCAP, int BUF>
+constexpr size_t simt_dyn_bytes() {
+  return size_t(KCAP + BUF) * BQ * sizeof(uint64_t);
+}
+
+template <typename T, int KCAP, int BUF>
+int simt_prepare() {
+  static bool done = false;
+  if (!done) {
+    RS_CHECK_CUDA(cudaFuncSetAttribute(score_topk_simt_kernel<T, KCAP, BUF>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(simt_dyn_bytes<T, KCAP, BUF>())),
+                  "cudaFuncSetAttribute(score_topk_simt_kernel)");
+    done = true;
+  }
+  return RS_OK;
+}
+
+template <typename T, int KCAP, int BUF>
+int launch_simt_t(const void* Q, const float* qn, int64_t nq, const void* C, const float* cn, int64_t n, int dim,
+                  int k, int64_t id_base, const SearchPlan& plan, uint64_t* part, cudaStream_t st) {
+  int rc = simt_prepare<T, KCAP, BUF>();
+  if (rc) return rc;
+  score_topk_simt_kernel<T, KCAP, BUF><<<plan.ctas, 256, simt_dyn_bytes<T, KCAP, BUF>(), st>>>(
+      (const T*)Q, qn, nq, (const T*)C, cn, n, dim, k, id_base, plan.qtiles, plan.segments, plan.seg_rows, part);
+  RS_CHECK_LAUNCH("score_topk_simt_kernel");
+  return RS_OK;
+}
+
+template <typename T, int KCAP, int BUF>
+int simt_occ() {
+  int occ = 1;
+  simt_prepare<T, KCAP, BUF>();
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, score_topk_simt_kernel<T, KCAP, BUF>, 256,
+                                                simt_dyn_bytes<T, KCAP, BUF>());
+  return occ > 0 ? occ : 1;
+}
+
+int simt_ctas_per_sm(int dtype, int k) {
+  if (dtype == RS_BF16) return k <= 40 ? simt_occ<__nv_bfloat16, 40, 32>() : simt_occ<__nv_bfloat16, 128, 32>();
+  return k <= 40 ? simt_occ<float, 40, 32>() : simt_occ<float, 128, 32>();
+}
+
+int launch_simt(int dtype, const void* Q, const float* qn, int64_t nq, const void* C, const float* cn, int64_t n,
+                int dim, int k, int64_t id_base, const SearchPlan& plan, uint64_t* part, cudaStream_t st) {
+  if (dtype == RS_BF16)
+    return k <= 40 ? launch_simt_t<__nv_bfloat16, 40, 32>(Q, qn, nq, C, cn, n, dim, k, id_base, plan, part, st)
+                   : launch_simt_t<__nv_bfloat16, 128, 32>(Q, qn, nq, C, cn, n, dim, k, id_base, plan, part, st);
+  return k <= 40 ? launch_simt_t<float, 40, 32>(Q, qn, nq, C, cn, n, dim, k, id_base, plan, part, st)
+                 : launch_simt_t<float, 128, 32>(Q, qn, nq, C, cn, n, dim, k, id_base, plan, part, st);
+}
+
+}  // namespace
+
+// ---- planner -----------------------------------------------------------------
+SearchPlan plan_search(int64_t nq, int64_t n, int bq, int bn, int ctas_capacity, int64_t row_bytes, bool share_l2) {
+  SearchPlan best;
+  const int64_t qt = ceil_div(std::max<int64_t>(nq, 1), bq);
+  const int64_t nt = ceil_div(std::max<int64_t>(n, 1), bn);
+  // With several query tiles the CTAs of one round share a segment through L2:
+  // cap the segment so the concurrently streamed window stays L2-resident.
+  int64_t max_tps = nt;
+  if (share_l2 && qt > 1) max_tps = std::max<int64_t>(1, (int64_t(48) << 20) / (int64_t(bn) * row_bytes));
+  double best_cost = 1e300;
+  for (int64_t tps = nt; tps >= 1;) {
+    const int64_t segs = ceil_div(nt, tps);
+    if (segs > 4096) break;
+    if (tps <= max_tps) {
+      const int64_t units = qt * segs;
+      const int64_t rounds = ceil_div(units, ctas_capacity);
+      // per-unit overhead ~1 tile (pipeline fill + list write); merge cost ~ lists
+      const double cost = double(rounds) * double(tps + 1) + 1e-3 * double(segs);
+      if (cost < best_cost) {
+        best_cost = cost;
+        best.qtiles = int32_t(qt);
+        best.segments = int32_t(segs);
+        best.seg_rows = tps * bn;
+        best.ctas = int32_t(std::min<int64_t>(units, ctas_capacity));
+      }
+    }
+    // next distinct segment count
+    const int64_t nxt = ceil_div(nt, segs + 1);
+    tps = (nxt < tps) ? nxt : tps - 1;
+  }
+  return best;
+}
+
+}  // namespace rs
+
+// ============================ rs_index =========================================
+struct rs_index {
+  int32_t dim = 0, dtype = 0, device = 0, algo = RS_ALGO_AUTO;
+  int64_t capacity = 0, ntotal = 0;
+  void* data = nullptr;
+  float* norms = nullptr;
+  float* qnorm = nullptr;
+  int64_t qnorm_cap = 0;
+  uint64_t* part = nullptr;
+  size_t part_cap = 0;  // bytes
+  rs::SearchPlan last;
+  int32_t last_algo = 0;
+};
+
+namespace {
+size_t esize(int dtype) { return dtype == RS_BF16 ? 2 : 4; }
+
+int ensure_ws(rs_index* ix, int64_t nq, size_t part_bytes) {
+  if (nq > ix->qnorm_cap) {
+    if (ix->qnorm) cudaFree(ix->qnorm);
+    ix->qnorm = nullptr;
+    RS_CHECK_CUDA(cudaMalloc(&ix->qnorm, sizeof(float) * nq), "cudaMalloc(qnorm)");
+    ix->qnorm_cap = nq;
+  }
+  if (part_bytes > ix->part_cap) {
+    if (ix->part) cudaFree(ix->part);
+    ix->part = nullptr;
+    RS_CHECK_CUDA(cudaMalloc(&ix->part, part_bytes), "cudaMalloc(partial top-k)");
+    ix->part_cap = part_bytes;
+  }
+  return RS_OK;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+bool use_tc(const rs_index* ix, int k) {
+  if (ix->algo == RS_ALGO_SIMT) return false;
+  return ix->dtype == RS_BF16 && ix->dim % 8 == 0 && k <= rs::kTcMaxK;
+}
+
+// partial lists for (queries x this shard) -> part; returns the plan
+int run_partial(rs_index* ix, const void* queries, int64_t nq, int k, int64_t id_base, cudaStream_t st,
+                rs::SearchPlan* plan_out) {
+  using namespace rs;
+  const bool tc = use_tc(ix, k);
+  RS_REQUIRE(!(ix->algo == RS_ALGO_TCGEN05 && !tc), "tcgen05 path needs bf16, dim %% 8 == 0 and k <= %d",
+             kTcMaxK);
+  const int sms = sm_count(ix->device);
+  SearchPlan plan;
+  if (tc) {
+    plan = plan_search(nq, ix->ntotal, kTcBM, kTcBN, sms, int64_t(ix->dim) * 2, true);
+  } else {
+    plan = plan_search(nq, ix->ntotal, kSimtBQ, kSimtBC, sms * simt_ctas_per_sm(ix->dtype, k),
+                       int64_t(ix->dim) * esize(ix->dtype), true);
+  }
+  const size_t part_bytes = size_t(nq) * plan.segments * k * sizeof(uint64_t);
+  int rc = ensure_ws(ix, nq, part_bytes);
+  if (rc) return rc;
+  rc = launch_norms(queries, nq, ix->dim, ix->dtype, ix->qnorm, st);
+  if (rc) return rc;
+  if (tc) {
+    CUtensorMap tmq, tmc;
+    rc = encode_kmajor_bf16_map(&tmq, queries, nq, ix->dim, kTcBM);
+    if (rc) return rc;
+    rc = encode_kmajor_bf16_map(&tmc, ix->data, ix->ntotal, ix->dim, kTcBN);
+    if (rc) return rc;
+    rc = launch_score_topk_tc(tmq, tmc, ix->qnorm, ix->norms, nq, ix->ntotal, ix->dim, k, id_base, plan, ix->part, st);
+  } else {
+    rc = launch_simt(ix->dtype, queries, ix->qnorm, nq, ix->data, ix->norms, ix->ntotal, ix->dim, k, id_base, plan,
+                     ix->part, st);
+  }
+  if (rc) return rc;
+  ix->last = plan;
+  ix->last_algo = tc ? RS_ALGO_TCGEN05 : RS_ALGO_SIMT;
+  *plan_out = plan;
+  return RS_OK;
+}
+
+int check_search_args(const rs_index* ix, const void* q, int64_t nq, int32_t k, int64_t id_base) {
+  RS_REQUIRE(ix != nullptr, "index is NULL");
+  RS_REQUIRE(nq >= 0, "nq must be non-negative");
+  RS_REQUIRE(k >= 1 && k <= 128, "k must be in [1, 128], got %d", k);
+  RS_REQUIRE(nq == 0 || q != nullptr, "queries is NULL");
+  RS_REQUIRE(id_base >= 0 && id_base + ix->ntotal < (int64_t(1) << 32) - 1,
+             "global chunk ids must fit in uint32 (id_base %lld + ntotal %lld)", (long long)id_base,
+             (long long)ix->ntotal);
+  return RS_OK;
+}
+}  // namespace
+
+extern "C" int rs_index_create(int32_t dim, int32_t dtype, int64_t capacity, int32_t device, rs_index** out) {
+  RS_REQUIRE(out != nullptr, "out is NULL");
+  RS_REQUIRE(dim >= 1 && dim <= 65536, "dim out of range");
+  RS_REQUIRE(dtype == RS_F32 || dtype == RS_BF16, "dtype must be RS_F32 or RS_BF16");
+  RS_REQUIRE(capacity >= 0, "capacity must be non-negative");
+  if (!rs_device_supported(device)) {
+    rs::set_error("device %d is not an sm_100 (B200) GPU", device);
+    return RS_ERR_UNSUPPORTED;
+  }
+  DeviceGuard g(device);
+  rs_index* ix = new rs_index();
+  ix->dim = dim;
+  ix->dtype = dtype;
+  ix->device = device;
+  ix->capacity = capacity;
+  if (capacity > 0) {
+    cudaError_t e = cudaMalloc(&ix->data, size_t(capacity) * dim * esize(dtype));
+    if (e == cudaSuccess) e = cudaMalloc(&ix->norms, sizeof(float) * capacity);
+    if (e != cudaSuccess) {
+      rs::set_error("cudaMalloc(corpus %lld x %d): %s", (long long)capacity, dim, cudaGetErrorString(e));
+      if (ix->data) cudaFree(ix->data);
+      delete ix;
+      return RS_ERR_OOM;
+    }
+  }
+  *out = ix;
+  return RS_OK;
+}
+
+extern "C" int rs_index_destroy(rs_index* ix) {
+  if (!ix) return RS_OK;
+  DeviceGuard g(ix->device);
+  cudaFree(ix->data);
+  cudaFree(ix->norms);
+  cudaFree(ix->qnorm);
+  cudaFree(ix->part);
+  delete ix;
+  return RS_OK;
+}
+
+extern "C" int rs_index_add(rs_index* ix, const void* emb, int64_t n, void* stream) {
+  RS_REQUIRE(ix != nullptr, "index is NULL");
+  RS_REQUIRE(n >= 0, "n must be non-negative");
+  if (n == 0) return RS_OK;
+  RS_REQUIRE(emb != nullptr, "embeddings is NULL");
+  RS_REQUIRE(ix->ntotal + n <= ix->capacity, "index capacity exceeded (%lld + %lld > %lld)",
+             (long long)ix->ntotal, (long long)n, (long long)ix->capacity);
+  DeviceGuard g(ix->device);
+  cudaStream_t st = rs::as_stream(stream);
+  const size_t row = size_t(ix->dim) * esize(ix->dtype);
+  RS_CHECK_CUDA(cudaMemcpyAsync((char*)ix->data + size_t(ix->ntotal) * row, emb, size_t(n) * row,
+                                cudaMemcpyDeviceToDevice, st),
+                "cudaMemcpyAsync(add)");
+  int rc = rs::launch_norms((char*)ix->data + size_t(ix->ntotal) * row, n, ix->dim, ix->dtype,
+                            ix->norms + ix->ntotal, st);
+  if (rc) return rc;
+  ix->ntotal += n;
+  return RS_OK;
+}
+
+extern "C" int rs_index_reset(rs_index* ix) {
+  RS_REQUIRE(ix != nullptr, "index is NULL");
+  ix->ntotal = 0;
+  return RS_OK;
+}
+
+extern "C" int rs_index_ntotal(const rs_index* ix, int64_t* out) {
+  RS_REQUIRE(ix && out, "NULL argument");
+  *out = ix->ntotal;
+  return RS_OK;
+}
+
+extern "C" int rs_index_data(const rs_index* ix, const void** emb, const float** norms) {
+  RS_REQUIRE(ix != nullptr, "index is NULL");
+  if (emb) *emb = ix->data;
+  if (norms) *norms = ix->norms;
+  return RS_OK;
+}
+
+extern "C" int rs_index_set_algo(rs_index* ix, int32_t algo) {
+  RS_REQUIRE(ix != nullptr, "index is NULL");
+  RS_REQUIRE(algo >= RS_ALGO_AUTO && algo <= RS_ALGO_TCGEN05, "unknown algo %d", algo);
+  ix->algo = algo;
+  return RS_OK;
+}
+
+extern "C" int rs_index_reserve(rs_index* ix, int64_t nq_max, int32_t k) {
+  using namespace rs;
+  RS_REQUIRE(ix != nullptr && nq_max >= 0 && k >= 1, "bad arguments");
+  DeviceGuard g(ix->device);
+  const bool tc = use_tc(ix, k);
+  const int sms = sm_count(ix->device);
+  // worst case over the expected corpus size (capacity)
+  SearchPlan plan = tc ? plan_search(nq_max, std::max<int64_t>(ix->capacity, 1), kTcBM, kTcBN, sms,
+                                     int64_t(ix->dim) * 2, true)
+                       : plan_search(nq_max, std::max<int64_t>(ix->capacity, 1), kSimtBQ, kSimtBC,
+                                     sms * simt_ctas_per_sm(ix->dtype, k), int64_t(ix->dim) * esize(ix->dtype), true);
+  return ensure_ws(ix, nq_max, size_t(nq_max) * plan.segments * k * sizeof(uint64_t));
+}
+
+extern "C" int rs_index_last_plan(const rs_index* ix, int32_t* segments, int32_t* qtiles, int32_t* ctas,
+                                  int32_t* algo) {
+  RS_REQUIRE(ix != nullptr, "index is NULL");
+  if (segments) *segments = ix->last.segments;
+  if (qtiles) *qtiles = ix->last.qtiles;
+  if (ctas) *ctas = ix->last.ctas;
+  if (algo) *algo = ix->last_algo;
+  return RS_OK;
+}
+
+static int search_impl(rs_index* ix, const void* queries, int64_t nq, int32_t k, int64_t id_base,
+                       const rs_config* keep, float* D, int64_t* I, uint64_t* keys, void* stream) {
+  using namespace rs;
+  int rc = check_search_args(ix, queries, nq, k, id_base);
+  if (rc) return rc;
+  if (nq == 0) return RS_OK;
+  DeviceGuard g(ix->device);
+  cudaStream_t st = as_stream(stream);
+  if (ix->ntotal == 0) {
+    fill_empty_kernel<<<(unsigned)std::min<int64_t>(ceil_div(nq * k, 256), 4096), 256, 0, st>>>(nq * k, D, I, keys);
+    RS_CHECK_LAUNCH("fill_empty_kernel");
+    return RS_OK;
+  }
+  SearchPlan plan;
+  rc = run_partial(ix, queries, nq, k, id_base, st, &plan);
+  if (rc) return rc;
+  return launch_merge(ix->part, nq, plan.segments, k, /*list_stride=*/k, /*q_stride=*/int64_t(plan.segments) * k, k,
+                      keep, D, I, keys, st);
+}
+
+extern "C" int rs_index_search(rs_index* ix, const void* queries, int64_t nq, int32_t k, int64_t id_base,
+                               const rs_config* keep, float* D, int64_t* I, void* stream) {
+  RS_REQUIRE(D != nullptr && I != nullptr, "D/I are NULL");
+  return search_impl(ix, queries, nq, k, id_base, keep, D, I, nullptr, stream);
+}
+
+extern "C" int rs_index_search_keys(rs_index* ix, const void* queries, int64_t nq, int32_t k, int64_t id_base,
+                                    uint64_t* keys, void* stream) {
+  RS_REQUIRE(keys != nullptr, "keys is NULL");
+  return search_impl(ix, queries, nq, k, id_base, nullptr, nullptr, nullptr, keys, stream);
+}
+
+extern "C" int rs_merge_topk(const uint64_t* keys, int64_t nq, int32_t nlists, int32_t k_in, int64_t list_stride,
+                             int32_t k, const rs_config* cfg, float* D, int64_t* I, void* stream) {
+  RS_REQUIRE(nq >= 0 && k >= 1 && k <= 128, "bad arguments");
+  RS_REQUIRE(D && I, "D/I are NULL");
+  if (nq == 0) return RS_OK;
+  return rs::launch_merge(keys, nq, nlists, k_in, list_stride, /*q_stride=*/k_in, k, cfg, D, I, nullptr,
+                          rs::as_stream(stream));
+}
+
+extern "C" int rs_row_norms(const void* x, int64_t n, int32_t dim, int32_t dtype, float* out, void* stream) {
+  RS_REQUIRE(n >= 0 && dim >= 1 && (dtype == RS_F32 || dtype == RS_BF16), "bad arguments");
+  if (n == 0) return RS_OK;
+  return rs::launch_norms(x, n, dim, dtype, out, rs::as_stream(stream));
+}

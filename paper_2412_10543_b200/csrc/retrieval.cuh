@@ -1,0 +1,42 @@
+// Internal interfaces between the retrieval translation units.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "rs_common.cuh"
+
+namespace rs {
+
+// Work split of one search over a corpus shard: the corpus is cut into
+// `segments` contiguous row ranges of `seg_rows` rows (a multiple of the
+// kernel's column tile) and the queries into `qtiles` row tiles; a unit is
+// (query tile, segment) and writes one sorted top-k list per query row to
+// part[(row * segments + segment) * k].  Units are ordered segment-major so the
+// CTAs that run concurrently stream the same corpus segment (L2 reuse).
+struct SearchPlan {
+  int32_t qtiles = 0;
+  int32_t segments = 0;
+  int64_t seg_rows = 0;
+  int32_t ctas = 0;
+};
+
+SearchPlan plan_search(int64_t nq, int64_t n, int bq, int bn, int ctas_capacity, int64_t row_bytes,
+                       bool share_l2);
+
+// tcgen05/TMA/TMEM bf16 kernel (score_topk_sm100.cu).
+constexpr int kTcMaxK = 40;
+constexpr int kTcBM = 128;
+constexpr int kTcBN = 256;
+size_t tc_smem_bytes();
+int launch_score_topk_tc(const CUtensorMap& tmq, const CUtensorMap& tmc, const float* qn, const float* cn,
+                         int64_t nq, int64_t n, int dim, int k, int64_t id_base, const SearchPlan& plan,
+                         uint64_t* part, cudaStream_t st);
+int encode_kmajor_bf16_map(CUtensorMap* map, const void* base, int64_t rows, int dim, int box_rows);
+
+// CUDA-core kernel for fp32 (and bf16 cross-checks), retrieval.cu.
+constexpr int kSimtBQ = 64;
+constexpr int kSimtBC = 64;
+
+}  // namespace rs

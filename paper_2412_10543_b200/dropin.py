@@ -1,0 +1,63 @@
+"""Install the GPU hot path into the reference package ``ragsched``.
+
+The reference resolves its hot-path functions by module attribute
+(``Scheduler._try_admit_new`` calls ``best_fit_select`` / ``fallback_config``
+from ``ragsched.scheduler``, scheduler.py:340/:360; ``QueryProfiler.gate``
+calls ``gate_profile`` from ``ragsched.profiler``, profiler.py:534-541).
+``install(ragsched)`` rebinds those names to wrappers that run this package's
+kernels and return the reference's own classes (``RagConfig``,
+``PrunedConfigSpace``, ``GateDecision``), so dataclass equality and the rest
+of the reference pipeline are unchanged.
+"""
+
+from __future__ import annotations
+
+import functools
+
+from . import mapping as _mapping
+from . import memory as _memory
+from . import profiler as _profiler
+from . import scheduler as _scheduler
+from . import sim as _sim
+
+
+def install(ragsched_pkg) -> dict:
+    """Patch ``ragsched.{scheduler,profiler,mapping,memory,sim}``.  Returns the
+    originals (for ``uninstall``)."""
+    import importlib
+
+    sched = importlib.import_module(ragsched_pkg.__name__ + ".scheduler")
+    prof = importlib.import_module(ragsched_pkg.__name__ + ".profiler")
+    mapping = importlib.import_module(ragsched_pkg.__name__ + ".mapping")
+    memory = importlib.import_module(ragsched_pkg.__name__ + ".memory")
+    sim = importlib.import_module(ragsched_pkg.__name__ + ".sim")
+    types = importlib.import_module(ragsched_pkg.__name__ + ".types")
+    kw_cfg = dict(config_cls=types.RagConfig, method_enum=types.SynthesisMethod)
+    kw_space = dict(space_cls=mapping.PrunedConfigSpace, method_enum=types.SynthesisMethod,
+                    range_cls=types.IntRange)
+
+    originals = {
+        (sched, "best_fit_select"): sched.best_fit_select,
+        (sched, "fallback_config"): sched.fallback_config,
+        (prof, "gate_profile"): prof.gate_profile,
+        (prof, "map_profile"): prof.map_profile,
+        (mapping, "map_profile"): mapping.map_profile,
+        (memory, "plan_bytes"): memory.plan_bytes,
+        (sim, "call_latency"): sim.call_latency,
+    }
+
+    sched.best_fit_select = functools.partial(_scheduler.best_fit_select, **kw_cfg)
+    sched.fallback_config = functools.partial(_scheduler.fallback_config, **kw_cfg)
+    prof.gate_profile = functools.partial(_profiler.gate_profile, decision_cls=prof.GateDecision,
+                                          default_space=prof.DEFAULT_FALLBACK_SPACE, **kw_space)
+    mp = functools.partial(_mapping.map_profile, **kw_space)
+    prof.map_profile = mp
+    mapping.map_profile = mp
+    memory.plan_bytes = _memory.plan_bytes
+    sim.call_latency = _sim.call_latency
+    return originals
+
+
+def uninstall(originals: dict) -> None:
+    for (mod, name), fn in originals.items():
+        setattr(mod, name, fn)

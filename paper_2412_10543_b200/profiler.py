@@ -1,0 +1,106 @@
+"""Confidence gate (reference ``profiler.py:467-486``) on the GPU.
+
+``gate_profile`` keeps the reference signature and semantics; the decision
+(accept → Algorithm-1 space, reject → hull of the last <= 10 accepted spaces
+or the default space) is computed by the ``rs_prune_gate`` kernel with the
+caller's window contents as carry-in state.  For streams of queries use
+:func:`paper_2412_10543_b200.batch.prune_gate`, which gates a whole batch in
+one launch sequence.
+"""
+
+from __future__ import annotations
+
+from collections import deque
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import batch as _b
+from .mapping import PrunedConfigSpace, hull_of_spaces
+from .types import DEFAULT_MAX_CHUNKS, IntRange, SynthesisMethod
+
+GATE_THRESHOLD = 0.90                 # profiler.py:30
+WINDOW_CAPACITY = 10                  # profiler.py:31
+DEFAULT_FALLBACK_SPACE = PrunedConfigSpace(frozenset({SynthesisMethod.STUFF}), IntRange(1, 5))  # :40-42
+
+
+class RecentSpaceWindow:
+    """Ring buffer of the most recently accepted spaces (profiler.py:138-153)."""
+
+    def __init__(self, capacity: int = WINDOW_CAPACITY) -> None:
+        self._spaces: deque = deque(maxlen=capacity)
+
+    def push(self, space) -> None:
+        self._spaces.append(space)
+
+    def hull(self):
+        return hull_of_spaces(list(self._spaces)) if self._spaces else None
+
+    def spaces(self) -> list:
+        return list(self._spaces)
+
+    def __len__(self) -> int:
+        return len(self._spaces)
+
+
+@dataclass(frozen=True)
+class GateDecision:
+    """profiler.py:156-163."""
+
+    space: PrunedConfigSpace
+    used_fallback: bool
+    confidence: float
+
+
+def _window_spaces(window) -> list:
+    if window is None:
+        return []
+    if hasattr(window, "spaces") and callable(window.spaces):
+        return window.spaces()
+    return list(getattr(window, "_spaces", ()))  # the reference's RecentSpaceWindow
+
+
+def _gate_one(profile, window_spaces, *, threshold, default_space, max_chunks, space_cls=None,
+              method_enum=None, range_cls=None):
+    """Run the gate kernel on one profile.  threshold=None means "always
+    accept" (plain map_profile).  Returns (space, used_fallback)."""
+    import torch
+
+    dev = _b.default_device()
+    space_cls = space_cls or PrunedConfigSpace
+    method_enum = method_enum or SynthesisMethod
+    range_cls = range_cls or IntRange
+    rec = _b.pack_profiles([profile])
+    thr = float(threshold) if threshold is not None else 1.0
+    if threshold is None:
+        rec["confidence"] = 1.0
+    window = _b.GateWindow(dev, window_spaces)
+    out = _b.prune_gate(_b.to_device(rec, dev), window, threshold=thr,
+                        default_space=default_space if default_space is not None else DEFAULT_FALLBACK_SPACE,
+                        max_chunks=max_chunks)
+    r = _b.from_device(out, _b.SPACE_DTYPE)[0]
+    torch.cuda.current_stream().synchronize()
+    if int(r["gate_fallback"]) and default_space is not None and not window_spaces:
+        return default_space, True  # `window.hull() or default_space` returns the object itself
+    return _b.unpack_space(r, space_cls=space_cls, method_enum=method_enum, range_cls=range_cls), bool(r["gate_fallback"])
+
+
+def gate_profile(out, window, threshold: float = GATE_THRESHOLD, *, default_space=DEFAULT_FALLBACK_SPACE,
+                 max_chunks: int = DEFAULT_MAX_CHUNKS, decision_cls=GateDecision, space_cls=None,
+                 method_enum=None, range_cls=None):
+    """profiler.py:467-486 — accept the profile's space when confident, else
+    the window hull (or ``default_space`` when nothing was accepted yet).
+    Accepted spaces are pushed into ``window``."""
+    if not 0.0 < threshold <= 1.0:
+        raise ValueError(f"threshold must be in (0, 1], got {threshold}")
+    profile = out.profile
+    space, fb = _gate_one(profile, _window_spaces(window), threshold=threshold, default_space=default_space,
+                          max_chunks=max_chunks, space_cls=space_cls, method_enum=method_enum,
+                          range_cls=range_cls)
+    if not fb:
+        window.push(space)
+    return decision_cls(space=space, used_fallback=fb, confidence=profile.confidence)
+
+
+def window_records(window) -> np.ndarray:
+    return _b.pack_spaces(_window_spaces(window))

@@ -1,0 +1,114 @@
+"""CPU checks of the C-ABI boundary: the library loads, exports every symbol
+``include/ragsched_b200.h`` declares, and the ctypes / numpy struct mirrors
+have the header's sizes.  No compute calls (no GPU here)."""
+
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from paper_2412_10543_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not os.path.exists(_lib.LIB_PATH):
+        from paper_2412_10543_b200 import build
+
+        build.build()
+    return _lib.load()
+
+
+def test_header_declares_expected_entry_points():
+    syms = _lib.header_symbols()
+    for name in ("rs_select", "rs_prune_gate", "rs_index_search", "rs_merge_topk", "rs_call_latency",
+                 "rs_plan_bytes", "rs_index_create", "rs_index_add"):
+        assert name in syms
+    assert set(syms) == set(_lib.SIGNATURES), set(syms) ^ set(_lib.SIGNATURES)
+
+
+def test_library_exports_every_header_symbol(lib):
+    for name in _lib.header_symbols():
+        assert hasattr(lib, name), name
+    out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\bT (rs_\w+)", out))
+    assert set(_lib.header_symbols()) <= exported
+
+
+def test_abi_version_and_error_channel(lib):
+    assert lib.rs_abi_version() == 1
+    assert isinstance(lib.rs_last_error(), bytes)
+
+
+def test_struct_sizes_match_header():
+    src = r"""
+#include <stdio.h>
+#include <stddef.h>
+#include "ragsched_b200.h"
+int main(void) {
+  printf("%zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(rs_profile), sizeof(rs_space), sizeof(rs_config),
+         sizeof(rs_select_params), sizeof(rs_cost_model), sizeof(rs_gate_params), sizeof(rs_window),
+         offsetof(rs_profile, confidence));
+  return 0;
+}
+"""
+    tmp = os.path.join(ROOT, "oracle", "_build")
+    os.makedirs(tmp, exist_ok=True)
+    c = os.path.join(tmp, "sizes.c")
+    exe = os.path.join(tmp, "sizes")
+    open(c, "w").write(src)
+    subprocess.check_call(["/usr/bin/gcc", "-I", os.path.join(ROOT, "include"), c, "-o", exe])
+    sizes = [int(x) for x in subprocess.check_output([exe]).split()]
+    assert sizes == [_lib.PROFILE_DTYPE.itemsize, _lib.SPACE_DTYPE.itemsize, _lib.CONFIG_DTYPE.itemsize,
+                     ctypes.sizeof(_lib.SelectParamsC), ctypes.sizeof(_lib.CostModelC),
+                     ctypes.sizeof(_lib.GateParamsC), _lib.WINDOW_DTYPE.itemsize,
+                     _lib.PROFILE_DTYPE.fields["confidence"][1]]
+
+
+def test_sass_contains_tcgen05_and_tma():
+    """The retrieval kernel is a real tcgen05/TMA/TMEM kernel (SASS mnemonics
+    per B200_PROFILING.md), not an mma.sync fallback."""
+    if not os.path.exists(_lib.LIB_PATH):
+        pytest.skip("library not built")
+    r = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", _lib.LIB_PATH], capture_output=True, text=True)
+    sass = r.stdout
+    assert "UTCHMMA" in sass and "UTMALDG" in sass and "LDTM" in sass
+    assert "HMMA" not in re.sub(r"UTCHMMA", "", sass)
+
+
+def test_gpu_entry_points_refuse_without_device():
+    """No CUDA device here: the compute API must fail loudly, never fall back."""
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    from paper_2412_10543_b200 import batch
+
+    with pytest.raises(_lib.LibraryUnavailable):
+        batch.default_device()
+
+
+def test_packing_roundtrip():
+    from paper_2412_10543_b200 import batch, mapping, types
+
+    s = mapping.PrunedConfigSpace(frozenset({types.SynthesisMethod.STUFF, types.SynthesisMethod.MAP_REDUCE}),
+                                  types.IntRange(3, 9), types.IntRange(40, 120))
+    rec = batch.pack_spaces([s])
+    assert batch.unpack_space(rec[0]) == s
+    raw = np.zeros(1, dtype=_lib.CONFIG_DTYPE)
+    raw["method"], raw["status"], raw["num_chunks"], raw["interlen"] = 4, 0, 7, 60
+    assert batch.unpack_config(raw[0]) == types.RagConfig(types.SynthesisMethod.MAP_REDUCE, 7, 60)
+    raw["status"] = 2
+    assert batch.unpack_config(raw[0]) is None
+    raw["status"] = 3
+    with pytest.raises(OverflowError):
+        batch.unpack_config(raw[0])
+    p = mapping.QueryProfile(True, True, 4, types.IntRange(30, 90), 0.93)
+    pr = batch.pack_profiles([p])[0]
+    assert (pr["complexity_high"], pr["needs_joint_reasoning"], pr["pieces_required"], pr["summary_lo"],
+            pr["summary_hi"], pr["confidence"]) == (1, 1, 4, 30, 90, 0.93)
