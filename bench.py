@@ -1,0 +1,443 @@
+"""Benchmark of the METIS per-query hot path: retrieval + config selection.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg4] [--impl ours|reference]
+
+One step = one batch of the workload's queries through the whole path:
+confidence gate + Algorithm-1 pruning, best-fit / fallback selection with the
+KV-memory and delay cost models, exact top-k retrieval over the corpus, and
+the join (each query's chunk ids truncated to its chosen ``num_chunks``).
+For N > 1 (``torchrun``, one process per GPU, NCCL) the corpus is sharded
+across the GPUs (strong scaling: the workload is fixed), the per-shard top-k
+lists are exchanged with one all-gather and merged per query slice, and the
+config stage is sharded by query.
+
+Prints ONE JSON line (rank 0).  Inputs are synthetic (seeded), larger than L2.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "queries/sec retrieval+config-select at 1/2/4/8 B200; % HBM/tensor roofline"
+
+# SURVEY.md §8(d) / BASELINE.json configs
+LENGTHS = {  # workload.py:53-58 (input range, output range); out_budget = top of output range
+    "single_hop_qa": ((400, 2000), (5, 10)),
+    "multihop_qa": ((1000, 5000), (5, 20)),
+    "doc_level_qa": ((4000, 10000), (20, 40)),
+    "summarization_qa": ((4000, 12000), (20, 60)),
+}
+WORKLOADS = {
+    "cfg1": dict(desc="reference CPU workload: 1,000 queries, 100k x 768 fp32, k<=35, 3 methods",
+                 nq=1000, n=100_000, d=768, dtype="fp32", truth="default", lengths="single_hop_qa", chunk=1000),
+    "cfg2": dict(desc="SQuAD-shaped: 10k queries, 1M x 768 bf16, stuff/map_rerank pruned space",
+                 nq=10_000, n=1_000_000, d=768, dtype="bf16", truth="squad", lengths="single_hop_qa", chunk=1000),
+    "cfg3": dict(desc="MuSiQue-shaped: 10k queries, 2M x 1024 bf16, full map_reduce interlen sweep",
+                 nq=10_000, n=2_000_000, d=1024, dtype="bf16", truth="musique", lengths="multihop_qa", chunk=1000),
+    "cfg4": dict(desc="QMSUM/FinSec-shaped long-doc: 8,192 queries, 10M x 1024 bf16 corpus sharded over the GPUs",
+                 nq=8192, n=10_000_000, d=1024, dtype="bf16", truth="default", lengths="doc_level_qa", chunk=1024),
+}
+K = 35  # DEFAULT_MAX_CHUNKS: the largest num_chunks any selected config can ask for
+BLOCK = 262_144  # corpus generation block (rows); block b is seeded independently
+
+
+# ---------------------------------------------------------------------------------
+# synthetic workload (host side, deterministic)
+
+def make_profiles(cfg, nq, seed):
+    """Profiles per SURVEY §8(d): TruthDistribution sampling (workload.py:61-81),
+    profile_from_truth embedding (profiler.py:166-176) and ~5% low-confidence
+    corrupted profiles (the default mock noise, profiler.py:99-106, 257-309)."""
+    rng = np.random.default_rng(seed)
+    if cfg["truth"] == "musique":
+        joint = np.ones(nq, bool)
+        cx = np.ones(nq, bool)
+        pieces = rng.integers(1, 11, nq)
+        lo = np.full(nq, 30)
+        hi = np.full(nq, 200)
+    else:
+        pc_j, pc_s = (0.0, 0.0) if cfg["truth"] == "squad" else (0.6, 0.1)
+        joint = rng.random(nq) < 0.5
+        cx = rng.random(nq) < np.where(joint, pc_j, pc_s)
+        pieces = np.where(joint, rng.integers(2, 11, nq), rng.integers(1, 4, nq))
+        lo = rng.integers(60, 181, nq)
+        hi = np.minimum(200, lo + 60)
+    conf = np.full(nq, 0.99)
+    noisy = rng.random(nq) < 0.049
+    conf[noisy] = np.round(rng.uniform(0.55, 0.88, noisy.sum()), 4)
+    flip = noisy & (rng.random(nq) < 0.5)
+    joint = np.where(flip, ~joint, joint)
+    pieces = np.where(noisy & ~flip, np.clip(pieces + rng.choice([-1, 1], nq), 1, 10), pieces)
+    (qlo, qhi), (_, out_budget) = LENGTHS[cfg["lengths"]]
+    qlen = rng.integers(qlo, qhi + 1, nq).astype(np.int32)
+    # free KV bytes ~ U[0, 2 x the largest candidate of the query's mapped space] (A2 mixture)
+    per_tok, C, T, O = 131072, cfg["chunk"], 64, out_budget
+    buf = lambda t: (102 * t.astype(np.int64) * per_tok + 99) // 100  # noqa: E731
+    n_hi = np.minimum(3 * pieces, 35)
+    q = qlen.astype(np.int64)
+    b_rr = n_hi * buf(q + C + T + O)
+    b_st = buf(q + n_hi * C + T + O)
+    b_mr = n_hi * buf(q + C + T + hi) + buf(q + n_hi * hi + T + O)
+    maxb = np.where(~joint, b_rr, np.where(cx, np.maximum(b_st, b_mr), b_st))
+    free = (rng.random(nq) * 2 * maxb).astype(np.int64)
+    return dict(cx=cx, joint=joint, pieces=pieces, lo=lo, hi=hi, conf=conf, qlen=qlen, free=free,
+                out_budget=out_budget)
+
+
+def corpus_block_torch(b, d, seed, device):
+    import torch
+
+    g = torch.Generator(device=device).manual_seed(seed * 1_000_003 + b)
+    x = torch.randn(BLOCK, d, generator=g, device=device)
+    return torch.nn.functional.normalize(x, dim=1)
+
+
+# ---------------------------------------------------------------------------------
+# measurement helpers
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        p = json.load(open(path))
+        return p["hbm_gbs"], p["bf16_tflops"], p.get("bf16_tflops_sustained", p["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, 1400.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self):
+        self.lines, self.proc, self.t = [], None, None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=lambda: [self.lines.append(l) for l in self.proc.stdout], daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def stop(self, gpus):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        self.t.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9 or not f[0].isdigit() or int(f[0]) not in gpus:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for name, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        under_load = [s for s in sm if smax and s > 0.3 * smax] or sm
+        return {"sm_mhz": statistics.median(under_load) if under_load else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------------
+# CPU baseline: the oracle port (FAISS-style fp32 BLAS search + C config path)
+
+def cpu_sample(cfg, prof, seed, n_rows=262_144, n_q=128, threads=None):
+    """Time a bounded sample of the workload on the host cores and extrapolate
+    to the full workload.  Returns (queries/s, sample description, cores)."""
+    import torch
+
+    from oracle import c_oracle
+    from oracle import config_oracle as co
+    from oracle import retrieval_oracle as ro
+
+    d, n_full, nq = cfg["d"], cfg["n"], cfg["nq"]
+    cores = threads or os.cpu_count()
+    torch.set_num_threads(cores)
+    n_rows = min(n_rows, n_full)
+    g = torch.Generator().manual_seed(seed)
+    c = torch.nn.functional.normalize(torch.randn(n_rows, d, generator=g), dim=1)
+    qv = torch.nn.functional.normalize(torch.randn(n_q, d, generator=g), dim=1)
+    if cfg["dtype"] == "bf16":
+        c, qv = c.bfloat16().float(), qv.bfloat16().float()
+    c, qv = c.numpy(), qv.numpy()
+    cn = np.einsum("ij,ij->i", c, c)
+    t0 = time.perf_counter()
+    ro.search_blas_fp32(qv, c, K, corpus_norms=cn)
+    t_ret = time.perf_counter() - t0
+    # config path for the whole batch: gate (serial) + select (all threads)
+    p = co.SelectParams(chunk_size=cfg["chunk"], out_budget=prof["out_budget"])
+    pr = np.stack([prof["cx"], prof["joint"], prof["pieces"], prof["lo"], prof["hi"]], 1).astype(np.int32)
+    t0 = time.perf_counter()
+    spaces, fb, _ = c_oracle.gate_batch(pr, prof["conf"])
+    c_oracle.select_batch(spaces, prof["joint"], prof["qlen"], prof["free"], p, nthreads=cores)
+    t_sel = time.perf_counter() - t0
+    per_query = t_ret / n_q * (n_full / n_rows) + t_sel / nq
+    desc = (f"{n_q} queries x {n_rows} rows x {d} fp32 BLAS exact search (extrapolated x{n_full / n_rows:.1f} "
+            f"to {n_full} rows) + gate/select of all {nq} queries (C port)")
+    return 1.0 / per_query, desc, cores, per_query
+
+
+def run_reference(args, cfg, rank):
+    """--impl reference: the CPU port of the reference path on the host cores."""
+    if rank != 0:
+        return
+    prof = make_profiles(cfg, cfg["nq"], args.seed)
+    times = []
+    desc = cores = None
+    for i in range(args.warmup + args.steps):
+        v, desc, cores, per_q = cpu_sample(cfg, prof, args.seed + i)
+        if i >= args.warmup:
+            times.append(per_q * cfg["nq"])
+    total = sum(times)
+    value = cfg["nq"] * len(times) / total
+    line = {
+        "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
+        "config": {"workload": f"{args.workload}: {cfg['desc']}", "k": K},
+        "cpu_baseline": {"value": value, "unit": "queries/s", "cores": cores, "kind": "port", "sample": desc},
+        "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------------
+# our arm
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg4", choices=sorted(WORKLOADS))
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--corpus-rows", type=int, default=None, help="override the corpus size (debug)")
+    args = ap.parse_args()
+    cfg = dict(WORKLOADS[args.workload])
+    if args.corpus_rows:
+        cfg["n"] = args.corpus_rows
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, cfg, rank)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2412_10543_b200 import _lib, batch
+    from paper_2412_10543_b200 import dist as rdist
+    from paper_2412_10543_b200.pipeline import RetrieveSelect
+    from paper_2412_10543_b200.retriever import IndexFlatL2
+
+    rank, world = rdist.init_from_env("nccl")
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    nq, n, d = cfg["nq"], cfg["n"], cfg["d"]
+    tdtype = torch.bfloat16 if cfg["dtype"] == "bf16" else torch.float32
+    esize = 2 if cfg["dtype"] == "bf16" else 4
+
+    # ---- corpus shard (global rows [r0, r1), ids r0..) ----
+    r0, r1 = rdist.shard_range(n, rank, world)
+    index = IndexFlatL2(d, dtype=tdtype, capacity=r1 - r0, device=dev, id_base=r0)
+    qloc0, qloc1 = rdist.shard_range(nq, rank, world)
+    nql = qloc1 - qloc0
+    grng = torch.Generator(device=dev).manual_seed(args.seed + 17 * rank + 1)
+    src = torch.randint(r0, r1, (nql,), generator=grng, device=dev)  # neighbour sources (local rows)
+    q_local = torch.nn.functional.normalize(torch.randn(nql, d, generator=grng, device=dev), dim=1)
+    is_nb = torch.arange(nql, device=dev) % 2 == 0
+    for b in range(r0 // BLOCK, (r1 - 1) // BLOCK + 1):
+        blk = corpus_block_torch(b, d, args.seed, dev)
+        lo, hi = max(r0, b * BLOCK), min(r1, (b + 1) * BLOCK)
+        rows = blk[lo - b * BLOCK: hi - b * BLOCK]
+        index.add(rows.to(tdtype))
+        m = is_nb & (src >= lo) & (src < hi)
+        if m.any():  # noisy neighbours normalize(c_j + 0.5 z)
+            q_local[m] = torch.nn.functional.normalize(
+                blk[src[m] - b * BLOCK] + 0.5 * q_local[m] / d ** 0.5, dim=1)
+        del blk, rows
+    torch.cuda.synchronize()
+    if world > 1:
+        parts = [torch.empty(rdist.shard_range(nq, r, world)[1] - rdist.shard_range(nq, r, world)[0], d,
+                             device=dev) for r in range(world)]
+        dist.all_gather(parts, q_local.contiguous())
+        queries = torch.cat(parts).to(tdtype)
+    else:
+        queries = q_local.to(tdtype)
+
+    prof = make_profiles(cfg, nq, args.seed + 1)
+    prof_np = batch.profiles_from_arrays(prof["cx"], prof["joint"], prof["pieces"], prof["lo"], prof["hi"],
+                                         prof["conf"])
+    profiles = batch.to_device(prof_np, dev)
+    qlen = torch.as_tensor(prof["qlen"], device=dev)
+    free = torch.as_tensor(prof["free"], device=dev)
+    params = batch.SelectParams(per_token_bytes=131072, chunk_size=cfg["chunk"], out_budget=prof["out_budget"])
+    cost = batch.CostModel()
+    index.reserve(nq, K)
+
+    if world == 1:
+        pipe = RetrieveSelect(index, params, k=K, cost=cost)
+
+        def step():
+            return pipe.run(queries, profiles, qlen, free)
+    else:
+        window = batch.GateWindow(dev)
+        ops = rdist.gpu_ops(index, params, window, cost=cost)
+
+        def step():
+            return rdist.sharded_retrieve_select(ops, queries, profiles, qlen, free, K)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x):
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    # ---- device-resident timing ----
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    index.enable_timing(True)
+    index.kernel_times_ms()
+    clocks = ClockSampler()
+    if rank == 0:
+        clocks.start()
+    barrier()
+    torch.cuda.synchronize()
+    l0 = _lib.launch_count()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(args.steps):
+        step()
+    ev1.record()
+    torch.cuda.synchronize()
+    barrier()
+    launches = _lib.launch_count() - l0
+    ms = ev0.elapsed_time(ev1)
+    kt = index.kernel_times_ms()
+    index.enable_timing(False)
+    clk = clocks.stop(gpus=list(range(world))) if rank == 0 else None
+    ms_max = max_over_ranks(ms)
+    launches_total = int(sum_over_ranks(launches))
+    kernel_ms = max_over_ranks(statistics.mean(kt) if kt else float("nan"))
+    value = nq * args.steps / (ms_max / 1e3)
+
+    # ---- end-to-end through the public API with pinned host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        q_host = queries.cpu().pin_memory()
+        p_host = profiles.cpu().pin_memory()
+        ql_host, fr_host = qlen.cpu().pin_memory(), free.cpu().pin_memory()
+        outbufs = {}
+
+        def e2e_step():
+            if world == 1:
+                return pipe.run_host(q_host, p_host, ql_host, fr_host, pinned_out=outbufs)
+            qd, pd = q_host.to(dev, non_blocking=True), p_host.to(dev, non_blocking=True)
+            qld, frd = ql_host.to(dev, non_blocking=True), fr_host.to(dev, non_blocking=True)
+            q0, q1, cfgs, D, I = rdist.sharded_retrieve_select(ops, qd, pd, qld, frd, K)
+            out = (cfgs.cpu(), I.cpu())
+            torch.cuda.synchronize()
+            return out
+
+        for _ in range(max(1, args.warmup // 2)):
+            e2e_step()
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        e2e_s = max_over_ranks(time.perf_counter() - t0)
+        h2d = q_host.numel() * q_host.element_size() + p_host.numel() + 4 * nq + 8 * nq
+        nq_slice = nq if world == 1 else (qloc1 - qloc0)
+        d2h = nq_slice * 16 + nq_slice * K * 8
+        e2e = {"value": nq * args.steps / e2e_s, "unit": "queries/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h)}
+
+    # ---- roofline of the dominant kernel (fused score + top-k) ----
+    hbm, tf_burst, tf_sust, peak_src = measured_peaks()
+    n_shard = r1 - r0
+    flops = 2.0 * nq * n_shard * d
+    bytes_alg = n_shard * d * esize + 4 * n_shard + nq * d * esize + nq * K * 12
+    t_tensor = flops / (tf_sust * 1e12)
+    t_hbm = bytes_alg / (hbm * 1e9)
+    if cfg["dtype"] == "bf16" and t_tensor >= t_hbm:
+        roof = {"bound": "tensor", "achieved": flops / (kernel_ms * 1e-3) / 1e12, "peak": tf_sust,
+                "unit": "TFLOP/s"}
+    else:
+        roof = {"bound": "hbm", "achieved": bytes_alg / (kernel_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = None
+    roof["kernel"] = "score_topk_tc_kernel" if cfg["dtype"] == "bf16" else "score_topk_simt_kernel"
+    roof["kernel_ms"] = kernel_ms
+    roof["kernel_share_of_step"] = kernel_ms / (ms_max / args.steps)
+    roof["peak_source"] = f"{peak_src}, {'sustained' if roof['bound'] == 'tensor' else 'copy'}"
+    prof_path = os.path.join(ROOT, "profiles", f"ncu_{args.workload}_n{world}.json")
+    if os.path.exists(prof_path):
+        try:
+            roof["traffic"] = json.load(open(prof_path)).get("dram_bytes_per_launch")
+        except Exception:
+            pass
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, desc, cores, _ = cpu_sample(cfg, prof, args.seed)
+        cpu = {"value": v, "unit": "queries/s", "cores": cores, "kind": "port", "sample": desc}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic",
+            "config": {"workload": f"{args.workload}: {cfg['desc']}", "queries_per_step": nq, "corpus_rows": n,
+                       "dim": d, "k": K, "corpus_shard_rows": n_shard,
+                       "parallelism": f"corpus-sharded x{world}, query-sharded config stage",
+                       "l2": "inputs larger than L2 (corpus shard >> 126 MB), no flush"},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_total,
+            "clocks": clk, "plan": index.last_plan(),
+        }
+        print(json.dumps(line), flush=True)
+    index.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

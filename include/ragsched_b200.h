@@ -220,6 +220,15 @@ int rs_merge_topk(const uint64_t* keys, int64_t nq, int32_t nlists, int32_t k_in
 /* Squared L2 norms of n rows of `dtype` (fp32 accumulate). */
 int rs_row_norms(const void* x, int64_t n, int32_t dim, int32_t dtype, float* out, void* stream);
 
+/* ---- measurement hooks (bench / profiling) --------------------------------
+ * Kernels launched by this library since load (all entry points). */
+uint64_t rs_launch_count(void);
+/* When enabled, every search brackets its fused score kernel with CUDA events
+ * on the launching stream; rs_index_kernel_times returns the durations (ms)
+ * recorded since the previous call (the streams must be synchronised). */
+int rs_index_enable_timing(rs_index* index, int32_t enable);
+int rs_index_kernel_times(rs_index* index, float* ms_out, int32_t max, int32_t* count);
+
 #ifdef __cplusplus
 }
 #endif

@@ -98,7 +98,15 @@ SIGNATURES = {
                                           ctypes.POINTER(_I32), ctypes.POINTER(_I32)]),
     "rs_merge_topk": (ctypes.c_int, [_P, _I64, _I32, _I32, _I64, _I32, _P, _P, _P, _P]),
     "rs_row_norms": (ctypes.c_int, [_P, _I64, _I32, _I32, _P, _P]),
+    "rs_launch_count": (ctypes.c_uint64, []),
+    "rs_index_enable_timing": (ctypes.c_int, [_P, _I32]),
+    "rs_index_kernel_times": (ctypes.c_int, [_P, _P, _I32, ctypes.POINTER(_I32)]),
 }
+
+
+def launch_count() -> int:
+    """Kernels launched by libragsched_b200 in this process."""
+    return int(load().rs_launch_count())
 
 
 class RagschedError(RuntimeError):

@@ -1,6 +1,7 @@
 // Library-level C ABI entry points: version, error reporting, device checks.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <mutex>
@@ -11,6 +12,9 @@
 namespace rs {
 
 static thread_local char g_err[1024] = "";
+static std::atomic<uint64_t> g_launches{0};
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -38,6 +42,8 @@ int sm_count(int device) {
 }  // namespace rs
 
 extern "C" int rs_abi_version(void) { return RS_ABI_VERSION; }
+
+extern "C" uint64_t rs_launch_count(void) { return rs::g_launches.load(std::memory_order_relaxed); }
 
 extern "C" const char* rs_last_error(void) { return rs::last_error(); }
 

@@ -358,6 +358,11 @@ struct rs_index {
   size_t part_cap = 0;  // bytes
   rs::SearchPlan last;
   int32_t last_algo = 0;
+  // optional per-search timing of the fused score kernel (event ring)
+  bool timing = false;
+  static constexpr int kRing = 512;
+  cudaEvent_t ev_start[kRing] = {}, ev_stop[kRing] = {};
+  int ev_next = 0, ev_pending = 0;
 };
 
 namespace {
@@ -417,6 +422,14 @@ int run_partial(rs_index* ix, const void* queries, int64_t nq, int k, int64_t id
   if (rc) return rc;
   rc = launch_norms(queries, nq, ix->dim, ix->dtype, ix->qnorm, st);
   if (rc) return rc;
+  const int slot = ix->ev_next;
+  if (ix->timing) {
+    if (!ix->ev_start[slot]) {
+      RS_CHECK_CUDA(cudaEventCreate(&ix->ev_start[slot]), "cudaEventCreate");
+      RS_CHECK_CUDA(cudaEventCreate(&ix->ev_stop[slot]), "cudaEventCreate");
+    }
+    RS_CHECK_CUDA(cudaEventRecord(ix->ev_start[slot], st), "cudaEventRecord");
+  }
   if (tc) {
     CUtensorMap tmq, tmc;
     rc = encode_kmajor_bf16_map(&tmq, queries, nq, ix->dim, kTcBM);
@@ -429,6 +442,11 @@ int run_partial(rs_index* ix, const void* queries, int64_t nq, int k, int64_t id
                      ix->part, st);
   }
   if (rc) return rc;
+  if (ix->timing) {
+    RS_CHECK_CUDA(cudaEventRecord(ix->ev_stop[slot], st), "cudaEventRecord");
+    ix->ev_next = (slot + 1) % rs_index::kRing;
+    if (ix->ev_pending < rs_index::kRing) ++ix->ev_pending;
+  }
   ix->last = plan;
   ix->last_algo = tc ? RS_ALGO_TCGEN05 : RS_ALGO_SIMT;
   *plan_out = plan;
@@ -476,9 +494,36 @@ extern "C" int rs_index_create(int32_t dim, int32_t dtype, int64_t capacity, int
   return RS_OK;
 }
 
+extern "C" int rs_index_enable_timing(rs_index* ix, int32_t enable) {
+  RS_REQUIRE(ix != nullptr, "index is NULL");
+  ix->timing = enable != 0;
+  ix->ev_pending = 0;
+  return RS_OK;
+}
+
+extern "C" int rs_index_kernel_times(rs_index* ix, float* ms_out, int32_t max, int32_t* count) {
+  RS_REQUIRE(ix != nullptr && count != nullptr, "NULL argument");
+  DeviceGuard g(ix->device);
+  const int n = ix->ev_pending < max ? ix->ev_pending : max;
+  for (int i = 0; i < n; ++i) {
+    // oldest first
+    const int slot = (ix->ev_next - ix->ev_pending + i + rs_index::kRing) % rs_index::kRing;
+    float ms = 0.0f;
+    RS_CHECK_CUDA(cudaEventElapsedTime(&ms, ix->ev_start[slot], ix->ev_stop[slot]), "cudaEventElapsedTime");
+    if (ms_out) ms_out[i] = ms;
+  }
+  *count = n;
+  ix->ev_pending = 0;
+  return RS_OK;
+}
+
 extern "C" int rs_index_destroy(rs_index* ix) {
   if (!ix) return RS_OK;
   DeviceGuard g(ix->device);
+  for (int i = 0; i < rs_index::kRing; ++i) {
+    if (ix->ev_start[i]) cudaEventDestroy(ix->ev_start[i]);
+    if (ix->ev_stop[i]) cudaEventDestroy(ix->ev_stop[i]);
+  }
   cudaFree(ix->data);
   cudaFree(ix->norms);
   cudaFree(ix->qnorm);
@@ -579,21 +624,21 @@ static int search_impl(rs_index* ix, const void* queries, int64_t nq, int32_t k,
 
 extern "C" int rs_index_search(rs_index* ix, const void* queries, int64_t nq, int32_t k, int64_t id_base,
                                const rs_config* keep, float* D, int64_t* I, void* stream) {
-  RS_REQUIRE(D != nullptr && I != nullptr, "D/I are NULL");
+  RS_REQUIRE(nq == 0 || (D != nullptr && I != nullptr), "D/I are NULL");
   return search_impl(ix, queries, nq, k, id_base, keep, D, I, nullptr, stream);
 }
 
 extern "C" int rs_index_search_keys(rs_index* ix, const void* queries, int64_t nq, int32_t k, int64_t id_base,
                                     uint64_t* keys, void* stream) {
-  RS_REQUIRE(keys != nullptr, "keys is NULL");
+  RS_REQUIRE(nq == 0 || keys != nullptr, "keys is NULL");
   return search_impl(ix, queries, nq, k, id_base, nullptr, nullptr, nullptr, keys, stream);
 }
 
 extern "C" int rs_merge_topk(const uint64_t* keys, int64_t nq, int32_t nlists, int32_t k_in, int64_t list_stride,
                              int32_t k, const rs_config* cfg, float* D, int64_t* I, void* stream) {
   RS_REQUIRE(nq >= 0 && k >= 1 && k <= 128, "bad arguments");
-  RS_REQUIRE(D && I, "D/I are NULL");
   if (nq == 0) return RS_OK;
+  RS_REQUIRE(D && I, "D/I are NULL");
   return rs::launch_merge(keys, nq, nlists, k_in, list_stride, /*q_stride=*/k_in, k, cfg, D, I, nullptr,
                           rs::as_stream(stream));
 }

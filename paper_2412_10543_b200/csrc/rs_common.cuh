@@ -17,9 +17,13 @@ const char* last_error();
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Count of kernels this library launched (rs_launch_count).
+void count_launch();
+
 // Launch-error check used right after every <<<>>> launch.
 #define RS_CHECK_LAUNCH(what)                                                     \
   do {                                                                            \
+    ::rs::count_launch();                                                         \
     cudaError_t _e = cudaGetLastError();                                          \
     if (_e != cudaSuccess) {                                                      \
       ::rs::set_error("%s: %s", what, cudaGetErrorString(_e));                    \

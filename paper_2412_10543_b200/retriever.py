@@ -117,6 +117,17 @@ class IndexFlatL2:
         return {"segments": s.value, "qtiles": q.value, "ctas": c.value,
                 "algo": {v: k for k, v in ALGOS.items()}.get(a.value, "none")}
 
+    def enable_timing(self, enable: bool = True) -> None:
+        """Bracket the fused score kernel of every search with CUDA events."""
+        _lib.check(self._lib.rs_index_enable_timing(self._h, int(enable)))
+
+    def kernel_times_ms(self) -> list[float]:
+        """Durations of the score kernels since the last call (streams synced)."""
+        buf = (ctypes.c_float * 512)()
+        cnt = ctypes.c_int32()
+        _lib.check(self._lib.rs_index_kernel_times(self._h, buf, 512, ctypes.byref(cnt)), "rs_index_kernel_times")
+        return [float(buf[i]) for i in range(cnt.value)]
+
     def close(self) -> None:
         if getattr(self, "_h", None):
             self._lib.rs_index_destroy(self._h)
