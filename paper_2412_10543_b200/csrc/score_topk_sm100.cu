@@ -79,11 +79,41 @@ __device__ __forceinline__ void unit_coords(int64_t u, const Params& p, int& qt,
   if (r1 > p.n) r1 = p.n;
 }
 
+// Epilogue fast path for 8 columns of one query row: 3 instructions per score
+// (FADD |q|^2+|c|^2, FFMA -2<q,c>, FSETP d <= tau) plus one warp vote per
+// group; the candidate append + heap maintenance only run when some lane of
+// the warp has a candidate (rare once the heaps are full).  Exact: the filter
+// uses the same rounded distance that is stored.
+template <bool FULL>
+__device__ __forceinline__ void epi_group(RowTopK<BM, BUF>& rt, const uint32_t* r, const float* cn, float qnv,
+                                          uint32_t id, int lim) {
+  const float4 a = *reinterpret_cast<const float4*>(cn);
+  const float4 b = *reinterpret_cast<const float4*>(cn + 4);
+  const float cv[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+  float e[8];
+  bool hit = false;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    e[j] = fmaf(-2.0f, __uint_as_float(r[j]), qnv + cv[j]);
+    hit |= (FULL || j < lim) && e[j] <= rt.tau;
+  }
+  if (__any_sync(0xffffffffu, hit)) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if ((FULL || j < lim) && e[j] <= rt.tau) rt.append(e[j] > 0.0f ? e[j] : 0.0f, id + j);
+    if (__any_sync(0xffffffffu, rt.nb > BUF - CHECK)) rt.flush();
+  }
+}
+
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     score_topk_tc_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmc,
                          const Params p) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // The kernel has no static shared memory, so the dynamic window starts at
+  // the CTA's shared-memory base (1024-aligned, as SWIZZLE_128B requires);
+  // indexing the array directly keeps every access in the shared window
+  // (LDS/STS rather than generic loads).
+  extern __shared__ __align__(1024) uint8_t smem[];
+  if ((smem_u32(smem) & 1023u) != 0) __trap();
   SmemTail* tail = reinterpret_cast<SmemTail*>(smem + OFF_TAIL);
   uint64_t* heap = reinterpret_cast<uint64_t*>(smem + OFF_HEAP);
   uint64_t* buf = reinterpret_cast<uint64_t*>(smem + OFF_BUF);
@@ -212,24 +242,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           tmem_wait_ld();
           if (ch * 32 + 32 <= valid) {
 #pragma unroll
-            for (int g = 0; g < 32; g += CHECK) {
-#pragma unroll
-              for (int j = g; j < g + CHECK; ++j) {
-                const int c = ch * 32 + j;
-                rt.offer(l2_from_dot(qnv + cn_t[c], __uint_as_float(r[j])), id0 + c);
-              }
-              if (__any_sync(0xffffffffu, rt.nb > BUF - CHECK)) rt.flush();
-            }
+            for (int g = 0; g < 32; g += CHECK)
+              epi_group<true>(rt, r + g, cn_t + ch * 32 + g, qnv, id0 + ch * 32 + g, CHECK);
           } else {
 #pragma unroll
-            for (int g = 0; g < 32; g += CHECK) {
-#pragma unroll
-              for (int j = g; j < g + CHECK; ++j) {
-                const int c = ch * 32 + j;
-                if (c < valid) rt.offer(l2_from_dot(qnv + cn_t[c], __uint_as_float(r[j])), id0 + c);
-              }
-              if (__any_sync(0xffffffffu, rt.nb > BUF - CHECK)) rt.flush();
-            }
+            for (int g = 0; g < 32; g += CHECK)
+              epi_group<false>(rt, r + g, cn_t + ch * 32 + g, qnv, id0 + ch * 32 + g, valid - ch * 32 - g);
           }
         }
         tc_fence_before();

@@ -43,10 +43,11 @@ struct RowTopK {
 
   // Predicated append of one candidate.
   __device__ __forceinline__ void offer(float d, uint32_t id) {
-    if (d <= tau) {
-      buf[nb * ROWS + row] = make_key(d, id);
-      ++nb;
-    }
+    if (d <= tau) append(d, id);
+  }
+  __device__ __forceinline__ void append(float d, uint32_t id) {
+    buf[nb * ROWS + row] = make_key(d, id);
+    ++nb;
   }
 
   __device__ void push(uint64_t key) {
