@@ -482,7 +482,9 @@ extern "C" int rs_index_create(int32_t dim, int32_t dtype, int64_t capacity, int
   ix->capacity = capacity;
   if (capacity > 0) {
     cudaError_t e = cudaMalloc(&ix->data, size_t(capacity) * dim * esize(dtype));
-    if (e == cudaSuccess) e = cudaMalloc(&ix->norms, sizeof(float) * capacity);
+    // + one column tile of padding: the fused kernel bulk-copies whole 16-byte
+    // granules of norms past the last row of a partial tile
+    if (e == cudaSuccess) e = cudaMalloc(&ix->norms, sizeof(float) * (capacity + rs::kTcBN));
     if (e != cudaSuccess) {
       rs::set_error("cudaMalloc(corpus %lld x %d): %s", (long long)capacity, dim, cudaGetErrorString(e));
       if (ix->data) cudaFree(ix->data);

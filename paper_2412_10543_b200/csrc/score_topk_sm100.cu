@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_init(&tail->empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
-      mbar_init(&tail->tfull[a], 1);
+      mbar_init(&tail->tfull[a], 2);  // cnorm bulk copy (expect_tx) + MMA commit
       mbar_init(&tail->tempty[a], 128);
     }
     fence_barrier_init();
@@ -189,6 +189,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint32_t acc = tile_iter & 1;
           mbar_wait(&tail->tempty[acc], ((tile_iter >> 1) & 1) ^ 1);
           tc_fence_after();
+          {
+            // stage this tile's corpus norms for the epilogue (the index pads
+            // the norms array, so rounding the copy up to 16 B stays in bounds)
+            const int valid = int(r1 - c0 < BN ? r1 - c0 : BN);
+            const uint32_t bytes = uint32_t((valid + 3) & ~3) * 4u;
+            mbar_arrive_expect_tx(&tail->tfull[acc], bytes);
+            bulk_copy_g2s(cns + acc * BN, p.cn + c0, bytes, &tail->tfull[acc]);
+          }
           const uint32_t d_tmem = tmem_base + acc * BN;
           for (int kb = 0; kb < p.kblocks; ++kb) {
             mbar_wait(&tail->full[stage], phase);
@@ -226,9 +234,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int64_t c0 = r0; c0 < r1; c0 += BN, ++tile_iter) {
         const uint32_t acc = tile_iter & 1;
         const int valid = int(r1 - c0 < BN ? r1 - c0 : BN);
-        float* cn_t = cns + acc * BN;
-        for (int c = row; c < BN; c += 128) cn_t[c] = c < valid ? p.cn[c0 + c] : 0.0f;
-        named_bar_sync(1, 128);
+        const float* cn_t = cns + acc * BN;
         mbar_wait(&tail->tfull[acc], (tile_iter >> 1) & 1);
         tc_fence_after();
         const uint32_t t_row = tmem_base + (uint32_t(ew * 32) << 16) + acc * BN;
