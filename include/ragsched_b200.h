@@ -179,7 +179,9 @@ int rs_plan_bytes(const uint8_t* method, const int32_t* num_chunks, const int32_
  * ties to the lower chunk id; missing entries are I = -1, D = +inf.
  * Chunk ids are id_base + row (id_base = the shard's first global id). */
 enum rs_dtype { RS_F32 = 0, RS_BF16 = 1 };
-enum rs_algo { RS_ALGO_AUTO = 0, RS_ALGO_SIMT = 1, RS_ALGO_TCGEN05 = 2 };
+/* RS_ALGO_TCGEN05: CTA-pair tcgen05 kernel (default for bf16);
+ * RS_ALGO_TCGEN05_1SM: single-CTA tcgen05 kernel; RS_ALGO_SIMT: CUDA cores. */
+enum rs_algo { RS_ALGO_AUTO = 0, RS_ALGO_SIMT = 1, RS_ALGO_TCGEN05 = 2, RS_ALGO_TCGEN05_1SM = 3 };
 
 typedef struct rs_index rs_index;
 

@@ -23,7 +23,7 @@ RS_OK, RS_ERR_INVALID_ARG, RS_ERR_CUDA, RS_ERR_UNSUPPORTED, RS_ERR_OOM, RS_ERR_O
 RS_MAP_RERANK, RS_STUFF, RS_MAP_REDUCE = 1, 2, 4
 RS_SELECT_BEST_FIT, RS_SELECT_FALLBACK, RS_SELECT_MUST_QUEUE, RS_SELECT_OVERFLOW = range(4)
 RS_F32, RS_BF16 = 0, 1
-RS_ALGO_AUTO, RS_ALGO_SIMT, RS_ALGO_TCGEN05 = 0, 1, 2
+RS_ALGO_AUTO, RS_ALGO_SIMT, RS_ALGO_TCGEN05, RS_ALGO_TCGEN05_1SM = 0, 1, 2, 3
 WINDOW_CAPACITY = 10
 
 # numpy mirrors of the C structs (packed exactly like the C layout)

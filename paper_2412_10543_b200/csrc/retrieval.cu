@@ -397,26 +397,31 @@ struct DeviceGuard {
   }
 };
 
-bool use_tc(const rs_index* ix, int k) {
-  if (ix->algo == RS_ALGO_SIMT) return false;
-  return ix->dtype == RS_BF16 && ix->dim % 8 == 0 && k <= rs::kTcMaxK;
+// Concrete kernel for a search: the CTA-pair tcgen05 kernel for bf16 (default),
+// the single-CTA tcgen05 kernel on request, else the CUDA-core kernel.
+int choose_algo(const rs_index* ix, int k) {
+  const bool tc_ok = ix->dtype == RS_BF16 && ix->dim % 8 == 0 && k <= rs::kTcMaxK;
+  if (ix->algo == RS_ALGO_SIMT || !tc_ok) return RS_ALGO_SIMT;
+  return ix->algo == RS_ALGO_TCGEN05_1SM ? RS_ALGO_TCGEN05_1SM : RS_ALGO_TCGEN05;
+}
+
+rs::SearchPlan make_plan(const rs_index* ix, int algo, int64_t nq, int64_t n, int k) {
+  using namespace rs;
+  const int sms = sm_count(ix->device);
+  if (algo == RS_ALGO_TCGEN05) return plan_search(nq, n, 2 * kTcBM, kTcBN, sms / 2, int64_t(ix->dim) * 2, true);
+  if (algo == RS_ALGO_TCGEN05_1SM) return plan_search(nq, n, kTcBM, kTcBN, sms, int64_t(ix->dim) * 2, true);
+  return plan_search(nq, n, kSimtBQ, kSimtBC, sms * simt_ctas_per_sm(ix->dtype, k),
+                     int64_t(ix->dim) * esize(ix->dtype), true);
 }
 
 // partial lists for (queries x this shard) -> part; returns the plan
 int run_partial(rs_index* ix, const void* queries, int64_t nq, int k, int64_t id_base, cudaStream_t st,
                 rs::SearchPlan* plan_out) {
   using namespace rs;
-  const bool tc = use_tc(ix, k);
-  RS_REQUIRE(!(ix->algo == RS_ALGO_TCGEN05 && !tc), "tcgen05 path needs bf16, dim %% 8 == 0 and k <= %d",
-             kTcMaxK);
-  const int sms = sm_count(ix->device);
-  SearchPlan plan;
-  if (tc) {
-    plan = plan_search(nq, ix->ntotal, kTcBM, kTcBN, sms, int64_t(ix->dim) * 2, true);
-  } else {
-    plan = plan_search(nq, ix->ntotal, kSimtBQ, kSimtBC, sms * simt_ctas_per_sm(ix->dtype, k),
-                       int64_t(ix->dim) * esize(ix->dtype), true);
-  }
+  const int algo = choose_algo(ix, k);
+  RS_REQUIRE(!((ix->algo == RS_ALGO_TCGEN05 || ix->algo == RS_ALGO_TCGEN05_1SM) && algo == RS_ALGO_SIMT),
+             "tcgen05 path needs bf16, dim %% 8 == 0 and k <= %d", kTcMaxK);
+  const SearchPlan plan = make_plan(ix, algo, nq, ix->ntotal, k);
   const size_t part_bytes = size_t(nq) * plan.segments * k * sizeof(uint64_t);
   int rc = ensure_ws(ix, nq, part_bytes);
   if (rc) return rc;
@@ -430,13 +435,17 @@ int run_partial(rs_index* ix, const void* queries, int64_t nq, int k, int64_t id
     }
     RS_CHECK_CUDA(cudaEventRecord(ix->ev_start[slot], st), "cudaEventRecord");
   }
-  if (tc) {
+  if (algo != RS_ALGO_SIMT) {
+    const bool pair = algo == RS_ALGO_TCGEN05;
     CUtensorMap tmq, tmc;
     rc = encode_kmajor_bf16_map(&tmq, queries, nq, ix->dim, kTcBM);
     if (rc) return rc;
-    rc = encode_kmajor_bf16_map(&tmc, ix->data, ix->ntotal, ix->dim, kTcBN);
+    rc = encode_kmajor_bf16_map(&tmc, ix->data, ix->ntotal, ix->dim, pair ? kTcBN / 2 : kTcBN);
     if (rc) return rc;
-    rc = launch_score_topk_tc(tmq, tmc, ix->qnorm, ix->norms, nq, ix->ntotal, ix->dim, k, id_base, plan, ix->part, st);
+    rc = pair ? launch_score_topk_pair(tmq, tmc, ix->qnorm, ix->norms, nq, ix->ntotal, ix->dim, k, id_base, plan,
+                                       ix->part, st)
+              : launch_score_topk_tc(tmq, tmc, ix->qnorm, ix->norms, nq, ix->ntotal, ix->dim, k, id_base, plan,
+                                     ix->part, st);
   } else {
     rc = launch_simt(ix->dtype, queries, ix->qnorm, nq, ix->data, ix->norms, ix->ntotal, ix->dim, k, id_base, plan,
                      ix->part, st);
@@ -448,7 +457,7 @@ int run_partial(rs_index* ix, const void* queries, int64_t nq, int k, int64_t id
     if (ix->ev_pending < rs_index::kRing) ++ix->ev_pending;
   }
   ix->last = plan;
-  ix->last_algo = tc ? RS_ALGO_TCGEN05 : RS_ALGO_SIMT;
+  ix->last_algo = algo;
   *plan_out = plan;
   return RS_OK;
 }
@@ -575,7 +584,7 @@ extern "C" int rs_index_data(const rs_index* ix, const void** emb, const float**
 
 extern "C" int rs_index_set_algo(rs_index* ix, int32_t algo) {
   RS_REQUIRE(ix != nullptr, "index is NULL");
-  RS_REQUIRE(algo >= RS_ALGO_AUTO && algo <= RS_ALGO_TCGEN05, "unknown algo %d", algo);
+  RS_REQUIRE(algo >= RS_ALGO_AUTO && algo <= RS_ALGO_TCGEN05_1SM, "unknown algo %d", algo);
   ix->algo = algo;
   return RS_OK;
 }
@@ -584,13 +593,8 @@ extern "C" int rs_index_reserve(rs_index* ix, int64_t nq_max, int32_t k) {
   using namespace rs;
   RS_REQUIRE(ix != nullptr && nq_max >= 0 && k >= 1, "bad arguments");
   DeviceGuard g(ix->device);
-  const bool tc = use_tc(ix, k);
-  const int sms = sm_count(ix->device);
   // worst case over the expected corpus size (capacity)
-  SearchPlan plan = tc ? plan_search(nq_max, std::max<int64_t>(ix->capacity, 1), kTcBM, kTcBN, sms,
-                                     int64_t(ix->dim) * 2, true)
-                       : plan_search(nq_max, std::max<int64_t>(ix->capacity, 1), kSimtBQ, kSimtBC,
-                                     sms * simt_ctas_per_sm(ix->dtype, k), int64_t(ix->dim) * esize(ix->dtype), true);
+  const SearchPlan plan = make_plan(ix, choose_algo(ix, k), nq_max, std::max<int64_t>(ix->capacity, 1), k);
   return ensure_ws(ix, nq_max, size_t(nq_max) * plan.segments * k * sizeof(uint64_t));
 }
 

@@ -79,30 +79,10 @@ __device__ __forceinline__ void unit_coords(int64_t u, const Params& p, int& qt,
   if (r1 > p.n) r1 = p.n;
 }
 
-// Epilogue fast path for 8 columns of one query row: 3 instructions per score
-// (FADD |q|^2+|c|^2, FFMA -2<q,c>, FSETP d <= tau) plus one warp vote per
-// group; the candidate append + heap maintenance only run when some lane of
-// the warp has a candidate (rare once the heaps are full).  Exact: the filter
-// uses the same rounded distance that is stored.
 template <bool FULL>
 __device__ __forceinline__ void epi_group(RowTopK<BM, BUF>& rt, const uint32_t* r, const float* cn, float qnv,
                                           uint32_t id, int lim) {
-  const float4 a = *reinterpret_cast<const float4*>(cn);
-  const float4 b = *reinterpret_cast<const float4*>(cn + 4);
-  const float cv[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-  float e[8];
-  bool hit = false;
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    e[j] = fmaf(-2.0f, __uint_as_float(r[j]), qnv + cv[j]);
-    hit |= (FULL || j < lim) && e[j] <= rt.tau;
-  }
-  if (__any_sync(0xffffffffu, hit)) {
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-      if ((FULL || j < lim) && e[j] <= rt.tau) rt.append(e[j] > 0.0f ? e[j] : 0.0f, id + j);
-    if (__any_sync(0xffffffffu, rt.nb > BUF - CHECK)) rt.flush();
-  }
+  epi_group8<BM, BUF, CHECK, FULL>(rt, r, cn, qnv, id, lim);
 }
 
 __global__ void __launch_bounds__(NUM_THREADS, 1)

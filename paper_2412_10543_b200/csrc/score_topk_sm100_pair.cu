@@ -1,0 +1,291 @@
+// K1 score_topk, CTA-pair variant (sm_100a, cta_group::2) — the default bf16
+// retrieval kernel.
+//
+// Same fused exact-L2 + streaming top-k as score_topk_sm100.cu, but two CTAs
+// on the two SMs of a TPC cooperate on a 256-query x 256-chunk tile with one
+// tcgen05.mma.cta_group::2 (M=256, N=256, K=16):
+//   * CTA r stages query rows [256*qt + 128*r, +128) (A half) and corpus rows
+//     [c0 + 128*r, +128) (B half) per k-block — each SM pulls 32 KB per
+//     512-cycle k-block (64 B/clk) instead of the 48 KB (96 B/clk) of the
+//     single-CTA tile, and the freed shared memory buys a 5-deep TMA ring;
+//   * the leader CTA (rank 0) issues the MMAs; its TMEM receives query rows
+//     0-127 of the tile and the peer's TMEM rows 128-255, all 256 chunk
+//     columns each, so every CTA's epilogue owns 128 queries x 256 chunks.
+//
+// Synchronisation (all mbarriers):
+//   full[s]   leader only; the leader's producer arms 2 x 32 KB, both CTAs'
+//             TMA loads complete on it (.cta_group::2 TMA, mapa address)
+//   empty[s]  both CTAs; leader MMA commit multicasts to both
+//   tfull[a]  both CTAs; 2 arrivals: the local norm bulk-copy (expect_tx) and
+//             the leader's MMA commit (multicast)
+//   tempty[a] leader: 8 warp arrivals (4 local + 4 remote from the peer);
+//             peer: its 4 local warps (gates its own norm copy)
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "retrieval.cuh"
+#include "sm100_ptx.cuh"
+#include "topk_rows.cuh"
+
+namespace rs {
+namespace {
+
+using namespace sm100;
+
+constexpr int BM = 128;         // query rows per CTA (TMEM lanes)
+constexpr int PM = 2 * BM;      // query rows per pair tile
+constexpr int BN = kTcBN;       // corpus columns per tile (both CTAs)
+constexpr int HB = BN / 2;      // corpus rows staged per CTA
+constexpr int BK = 64;
+constexpr int STAGES = 5;
+constexpr int KCAP = kTcMaxK;
+constexpr int BUF = 8;
+constexpr int CHECK = 8;
+constexpr int A_BYTES = BM * BK * 2;
+constexpr int B_BYTES = HB * BK * 2;
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int TMEM_COLS = 2 * BN;
+constexpr int NUM_THREADS = 256;
+constexpr int EPI_WARP0 = 4;
+constexpr uint32_t IDESC = umma_idesc_bf16_f32(PM, BN);
+
+struct __align__(8) SmemTail {
+  uint64_t full[STAGES];
+  uint64_t empty[STAGES];
+  uint64_t tfull[2];
+  uint64_t tempty[2];
+  uint32_t tmem_base;
+};
+
+constexpr size_t OFF_HEAP = size_t(STAGES) * STAGE_BYTES;
+constexpr size_t OFF_BUF = OFF_HEAP + size_t(KCAP) * BM * 8;
+constexpr size_t OFF_CN = OFF_BUF + size_t(BUF) * BM * 8;
+constexpr size_t OFF_TAIL = OFF_CN + 2 * BN * sizeof(float);
+constexpr size_t SMEM_BYTES = OFF_TAIL + sizeof(SmemTail);
+static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
+
+struct Params {
+  const float* qn;
+  const float* cn;
+  int64_t nq, n;
+  int32_t kblocks;
+  int32_t k;
+  int64_t id_base;
+  int32_t qtiles, segments;
+  int64_t seg_rows;
+  uint64_t* part;
+};
+
+__device__ __forceinline__ void unit_coords(int64_t u, const Params& p, int& qt, int& seg, int64_t& r0,
+                                            int64_t& r1) {
+  seg = int(u / p.qtiles);
+  qt = int(u - int64_t(seg) * p.qtiles);
+  r0 = int64_t(seg) * p.seg_rows;
+  r1 = r0 + p.seg_rows;
+  if (r1 > p.n) r1 = p.n;
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+    score_topk_pair_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmc,
+                           const Params p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  SmemTail* tail = reinterpret_cast<SmemTail*>(smem + OFF_TAIL);
+  uint64_t* heap = reinterpret_cast<uint64_t*>(smem + OFF_HEAP);
+  uint64_t* buf = reinterpret_cast<uint64_t*>(smem + OFF_BUF);
+  float* cns = reinterpret_cast<float*>(smem + OFF_CN);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int64_t units = int64_t(p.qtiles) * p.segments;
+  const int64_t pair = blockIdx.x >> 1;
+  const int64_t npairs = gridDim.x >> 1;
+  if ((smem_u32(smem) & 1023u) != 0) __trap();
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmq);
+    tma_prefetch_desc(&tmc);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&tail->full[s], 1);
+      mbar_init(&tail->empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tail->tfull[a], 2);
+      mbar_init(&tail->tempty[a], leader ? 8 : 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    tmem_alloc_pair(&tail->tmem_base, TMEM_COLS);
+    tmem_relinquish_pair();
+  }
+  tc_fence_before();
+  cluster_sync();  // barriers of both CTAs initialised, TMEM allocated
+  tc_fence_after();
+  const uint32_t tmem_base = tail->tmem_base;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===== TMA producer (both CTAs): own A half + own B half per k-block =====
+      const uint64_t pol_q = policy_evict_last();
+      const uint64_t pol_c = p.qtiles == 1 ? policy_evict_first() : policy_evict_normal();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t u = pair; u < units; u += npairs) {
+        int qt, seg;
+        int64_t r0, r1;
+        unit_coords(u, p, qt, seg, r0, r1);
+        for (int64_t c0 = r0; c0 < r1; c0 += BN) {
+          for (int kb = 0; kb < p.kblocks; ++kb) {
+            mbar_wait(&tail->empty[stage], phase ^ 1);
+            uint8_t* sa = smem + size_t(stage) * STAGE_BYTES;
+            const uint32_t full_leader = mapa_shared(smem_u32(&tail->full[stage]), 0);
+            if (leader) mbar_arrive_expect_tx(&tail->full[stage], 2 * STAGE_BYTES);
+            tma_load_2d_pair(&tmq, full_leader, sa, kb * BK, qt * PM + int(rank) * BM, pol_q);
+            tma_load_2d_pair(&tmc, full_leader, sa + A_BYTES, kb * BK, int32_t(c0) + int(rank) * HB, pol_c);
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ===== leader: MMA issuer; both: corpus-norm staging per tile =====
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t tile_iter = 0;
+      for (int64_t u = pair; u < units; u += npairs) {
+        int qt, seg;
+        int64_t r0, r1;
+        unit_coords(u, p, qt, seg, r0, r1);
+        for (int64_t c0 = r0; c0 < r1; c0 += BN, ++tile_iter) {
+          const uint32_t acc = tile_iter & 1;
+          // leader: both epilogues released TMEM buffer acc; peer: own epilogue released cns[acc]
+          mbar_wait(&tail->tempty[acc], ((tile_iter >> 1) & 1) ^ 1);
+          tc_fence_after();
+          {
+            const int valid = int(r1 - c0 < BN ? r1 - c0 : BN);
+            const uint32_t bytes = uint32_t((valid + 3) & ~3) * 4u;
+            mbar_arrive_expect_tx(&tail->tfull[acc], bytes);
+            bulk_copy_g2s(cns + acc * BN, p.cn + c0, bytes, &tail->tfull[acc]);
+          }
+          if (!leader) continue;
+          const uint32_t d_tmem = tmem_base + acc * BN;
+          for (int kb = 0; kb < p.kblocks; ++kb) {
+            mbar_wait(&tail->full[stage], phase);
+            tc_fence_after();
+            const uint32_t a_addr = smem_u32(smem + size_t(stage) * STAGE_BYTES);
+            const uint32_t b_addr = a_addr + A_BYTES;
+#pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk) {
+              umma_bf16_ss_pair(d_tmem, umma_desc_sw128(a_addr + kk * 32), umma_desc_sw128(b_addr + kk * 32),
+                                IDESC, (kb | kk) != 0);
+            }
+            umma_commit_pair_mc(&tail->empty[stage], 0x3);
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+          umma_commit_pair_mc(&tail->tfull[acc], 0x3);
+        }
+      }
+    }
+  } else if (warp >= EPI_WARP0) {
+    // ===== epilogue (both CTAs): 128 queries x 256 chunks per tile =====
+    const int ew = warp - EPI_WARP0;
+    const int row = ew * 32 + lane;
+    RowTopK<BM, BUF> rt{heap, buf, row, p.k, 0, 0, 0.0f};
+    const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tail->tempty[0]), 0);
+    const uint32_t tempty_leader1 = mapa_shared(smem_u32(&tail->tempty[1]), 0);
+    uint32_t tile_iter = 0;
+    for (int64_t u = pair; u < units; u += npairs) {
+      int qt, seg;
+      int64_t r0, r1;
+      unit_coords(u, p, qt, seg, r0, r1);
+      const int64_t qrow = int64_t(qt) * PM + int64_t(rank) * BM + row;
+      const float qnv = qrow < p.nq ? p.qn[qrow] : 0.0f;
+      rt.reset();
+      for (int64_t c0 = r0; c0 < r1; c0 += BN, ++tile_iter) {
+        const uint32_t acc = tile_iter & 1;
+        const int valid = int(r1 - c0 < BN ? r1 - c0 : BN);
+        const float* cn_t = cns + acc * BN;
+        mbar_wait(&tail->tfull[acc], (tile_iter >> 1) & 1);
+        tc_fence_after();
+        const uint32_t t_row = tmem_base + (uint32_t(ew * 32) << 16) + acc * BN;
+        const uint32_t id0 = uint32_t(p.id_base + c0);
+#pragma unroll 1
+        for (int ch = 0; ch < BN / 32; ++ch) {
+          if (ch * 32 >= valid) break;  // warp-uniform
+          uint32_t r[32];
+          __syncwarp();
+          tmem_ld_32x32b_x32(t_row + ch * 32, r);
+          tmem_wait_ld();
+          if (ch * 32 + 32 <= valid) {
+#pragma unroll
+            for (int g = 0; g < 32; g += 8)
+              epi_group8<BM, BUF, CHECK, true>(rt, r + g, cn_t + ch * 32 + g, qnv, id0 + ch * 32 + g, 8);
+          } else {
+#pragma unroll
+            for (int g = 0; g < 32; g += 8)
+              epi_group8<BM, BUF, CHECK, false>(rt, r + g, cn_t + ch * 32 + g, qnv, id0 + ch * 32 + g,
+                                                valid - ch * 32 - g);
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&tail->tempty[acc]);
+          if (!leader) mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
+        }
+      }
+      if (qrow < p.nq) rt.finish(p.part + (qrow * p.segments + seg) * p.k);
+    }
+  }
+
+  __syncwarp();
+  tc_fence_before();
+  cluster_sync();  // the peer's smem / TMEM stay alive until the leader's MMAs are done
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem_base, TMEM_COLS);
+  }
+}
+
+}  // namespace
+
+int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap& tmc, const float* qn, const float* cn,
+                           int64_t nq, int64_t n, int dim, int k, int64_t id_base, const SearchPlan& plan,
+                           uint64_t* part, cudaStream_t st) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    RS_CHECK_CUDA(cudaFuncSetAttribute(score_topk_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(SMEM_BYTES)),
+                  "cudaFuncSetAttribute(score_topk_pair_kernel)");
+    attr_set = true;
+  }
+  Params p{};
+  p.qn = qn;
+  p.cn = cn;
+  p.nq = nq;
+  p.n = n;
+  p.kblocks = (dim + BK - 1) / BK;
+  p.k = k;
+  p.id_base = id_base;
+  p.qtiles = plan.qtiles;
+  p.segments = plan.segments;
+  p.seg_rows = plan.seg_rows;
+  p.part = part;
+  score_topk_pair_kernel<<<2 * plan.ctas, NUM_THREADS, SMEM_BYTES, st>>>(tmq, tmc, p);
+  RS_CHECK_LAUNCH("score_topk_pair_kernel");
+  return RS_OK;
+}
+
+}  // namespace rs

@@ -117,6 +117,35 @@ struct RowTopK {
   }
 };
 
+// Epilogue fast path for 8 columns of one query row (fp32 dots `r` from
+// TMEM, corpus norms `cn` in smem): 3 instructions per score (FADD
+// |q|^2+|c|^2, FFMA -2<q,c>, FSETP d <= tau, the compiler folds the 8 compares
+// into FMNMX3 + one FSETP) plus one warp vote per group; candidate append and
+// heap maintenance only run when some lane of the warp has a candidate (rare
+// once the heaps are full).  Exact: the filter uses the same rounded distance
+// that is stored.
+template <int ROWS, int BUF, int CHECK, bool FULL>
+__device__ __forceinline__ void epi_group8(RowTopK<ROWS, BUF>& rt, const uint32_t* r, const float* cn, float qnv,
+                                           uint32_t id, int lim) {
+  static_assert(BUF >= CHECK, "buffer must hold one group");
+  const float4 a = *reinterpret_cast<const float4*>(cn);
+  const float4 b = *reinterpret_cast<const float4*>(cn + 4);
+  const float cv[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+  float e[8];
+  bool hit = false;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    e[j] = fmaf(-2.0f, __uint_as_float(r[j]), qnv + cv[j]);
+    hit |= (FULL || j < lim) && e[j] <= rt.tau;
+  }
+  if (__any_sync(0xffffffffu, hit)) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if ((FULL || j < lim) && e[j] <= rt.tau) rt.append(e[j] > 0.0f ? e[j] : 0.0f, id + j);
+    if (__any_sync(0xffffffffu, rt.nb > BUF - CHECK)) rt.flush();
+  }
+}
+
 // Distance from the fused epilogue: ||q||^2 + ||c||^2 - 2<q,c>, negative
 // round-off clamped to 0 (FAISS exhaustive_L2sqr_blas); NaN maps to 0 too.
 __device__ __forceinline__ float l2_from_dot(float qn_plus_cn, float dot) {

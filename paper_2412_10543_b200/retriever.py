@@ -18,7 +18,8 @@ import torch
 from . import _lib
 
 _DTYPES = {torch.bfloat16: _lib.RS_BF16, torch.float32: _lib.RS_F32}
-ALGOS = {"auto": _lib.RS_ALGO_AUTO, "simt": _lib.RS_ALGO_SIMT, "tcgen05": _lib.RS_ALGO_TCGEN05}
+ALGOS = {"auto": _lib.RS_ALGO_AUTO, "simt": _lib.RS_ALGO_SIMT, "tcgen05": _lib.RS_ALGO_TCGEN05,
+         "tcgen05_1sm": _lib.RS_ALGO_TCGEN05_1SM}
 
 
 class IndexFlatL2:
