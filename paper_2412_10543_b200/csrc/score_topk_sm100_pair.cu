@@ -40,7 +40,10 @@ constexpr int HB = BN / 2;      // corpus rows staged per CTA
 constexpr int BK = 64;
 constexpr int STAGES = 5;
 constexpr int KCAP = kTcMaxK;
-constexpr int BUF = 8;
+// Candidate buffer per row: flushing only when some lane holds > BUF - CHECK
+// entries makes each heap-maintenance pass batch many candidates across the
+// warp's lanes (a flush on every hit would serialise per-lane heap pushes).
+constexpr int BUF = 24;
 constexpr int CHECK = 8;
 constexpr int A_BYTES = BM * BK * 2;
 constexpr int B_BYTES = HB * BK * 2;
