@@ -16,7 +16,8 @@ import threading
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libragsched_b200.so")
+# RAGSCHED_B200_LIB selects a tuning variant built by build.build(defines=..., out=...)
+LIB_PATH = os.environ.get("RAGSCHED_B200_LIB") or os.path.join(HERE, "libragsched_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "ragsched_b200.h")
 
 RS_OK, RS_ERR_INVALID_ARG, RS_ERR_CUDA, RS_ERR_UNSUPPORTED, RS_ERR_OOM, RS_ERR_OVERFLOW = range(6)

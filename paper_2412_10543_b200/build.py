@@ -50,36 +50,46 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def _compile(src, verbose):
-    obj = os.path.join(OBJ, src.replace(".cu", ".o"))
+def _compile(src, verbose, objdir=None, defines=()):
+    objdir = objdir or OBJ
+    obj = os.path.join(objdir, src.replace(".cu", ".o"))
     if not _stale(obj, _deps(src)):
         return obj, ""
-    cmd = [nvcc(), *_flags(), "-c", os.path.join(CSRC, src), "-o", obj]
+    cmd = [nvcc(), *_flags(), *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, src), "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
     return obj, r.stderr
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    os.makedirs(OBJ, exist_ok=True)
+def build(verbose: bool = False, force: bool = False, *, defines=(), out: str | None = None) -> str:
+    """Build the library.  ``defines``/``out`` build a tuning variant (e.g.
+    ``RS_PAIR_EPI_COLS=64``) into its own object dir and .so, selected at
+    run time with ``RAGSCHED_B200_LIB=<path>``."""
+    lib = out or LIB
+    objdir = OBJ if not defines else os.path.join(OBJ, "_".join(d.replace("=", "") for d in defines))
+    os.makedirs(objdir, exist_ok=True)
     if force:
-        for f in os.listdir(OBJ):
-            os.remove(os.path.join(OBJ, f))
+        for f in os.listdir(objdir):
+            p = os.path.join(objdir, f)
+            if os.path.isfile(p):
+                os.remove(p)
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
-        results = list(ex.map(lambda s: _compile(s, verbose), SOURCES))
+        results = list(ex.map(lambda s: _compile(s, verbose, objdir, defines), SOURCES))
     objs = [o for o, _ in results]
     if verbose:
         for _, log in results:
             if log:
                 sys.stderr.write(log)
-    if force or _stale(LIB, objs):
-        cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-ccbin", "/usr/bin/g++", *objs, "-o", LIB]
+    if force or _stale(lib, objs):
+        cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-ccbin", "/usr/bin/g++", *objs, "-o", lib]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    outs = [a[6:] for a in sys.argv[1:] if a.startswith("--out=")]
+    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv, defines=defs, out=outs[0] if outs else None))

@@ -31,8 +31,9 @@ __device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 v) {
 // ---- squared norms: one warp per row, fp32 accumulate ---------------------
 template <typename T>
 __global__ void __launch_bounds__(256) row_norms_kernel(const T* __restrict__ x, int64_t n, int dim,
-                                                        float* __restrict__ out) {
+                                                        float* __restrict__ out, unsigned int* __restrict__ max_bits) {
   const int lane = threadIdx.x & 31;
+  float mx = 0.0f;
   for (int64_t r = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r < n;
        r += (int64_t(gridDim.x) * blockDim.x) >> 5) {
     const T* row = x + r * dim;
@@ -44,7 +45,10 @@ __global__ void __launch_bounds__(256) row_norms_kernel(const T* __restrict__ x,
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
     if (lane == 0) out[r] = s;
+    mx = fmaxf(mx, s);
   }
+  // running max of the (non-negative) norms: unsigned order == float order
+  if (max_bits && lane == 0 && mx > 0.0f) atomicMax(max_bits, __float_as_uint(mx));
 }
 
 // ---- CUDA-core fused score + top-k ------------------------------------------
@@ -246,13 +250,15 @@ int launch_merge(const uint64_t* keys, int64_t nq, int nlists, int k_in, int64_t
   return RS_OK;
 }
 
-int launch_norms(const void* x, int64_t n, int dim, int dtype, float* out, cudaStream_t st) {
+int launch_norms(const void* x, int64_t n, int dim, int dtype, float* out, cudaStream_t st,
+                 float* max_out = nullptr) {
   if (n <= 0) return RS_OK;
   const int64_t blocks = std::min<int64_t>(ceil_div(n * 32, 256), 148 * 64);
+  unsigned int* mb = reinterpret_cast<unsigned int*>(max_out);
   if (dtype == RS_BF16)
-    row_norms_kernel<__nv_bfloat16><<<(unsigned)blocks, 256, 0, st>>>((const __nv_bfloat16*)x, n, dim, out);
+    row_norms_kernel<__nv_bfloat16><<<(unsigned)blocks, 256, 0, st>>>((const __nv_bfloat16*)x, n, dim, out, mb);
   else
-    row_norms_kernel<float><<<(unsigned)blocks, 256, 0, st>>>((const float*)x, n, dim, out);
+    row_norms_kernel<float><<<(unsigned)blocks, 256, 0, st>>>((const float*)x, n, dim, out, mb);
   RS_CHECK_LAUNCH("row_norms_kernel");
   return RS_OK;
 }
@@ -352,6 +358,7 @@ struct rs_index {
   int64_t capacity = 0, ntotal = 0;
   void* data = nullptr;
   float* norms = nullptr;
+  float* norm_max = nullptr;  // device scalar: max squared norm over the shard
   float* qnorm = nullptr;
   int64_t qnorm_cap = 0;
   uint64_t* part = nullptr;
@@ -494,6 +501,8 @@ extern "C" int rs_index_create(int32_t dim, int32_t dtype, int64_t capacity, int
     // + one column tile of padding: the fused kernel bulk-copies whole 16-byte
     // granules of norms past the last row of a partial tile
     if (e == cudaSuccess) e = cudaMalloc(&ix->norms, sizeof(float) * (capacity + rs::kTcBN));
+    if (e == cudaSuccess) e = cudaMalloc(&ix->norm_max, sizeof(float));
+    if (e == cudaSuccess) e = cudaMemset(ix->norm_max, 0, sizeof(float));
     if (e != cudaSuccess) {
       rs::set_error("cudaMalloc(corpus %lld x %d): %s", (long long)capacity, dim, cudaGetErrorString(e));
       if (ix->data) cudaFree(ix->data);
@@ -537,6 +546,7 @@ extern "C" int rs_index_destroy(rs_index* ix) {
   }
   cudaFree(ix->data);
   cudaFree(ix->norms);
+  cudaFree(ix->norm_max);
   cudaFree(ix->qnorm);
   cudaFree(ix->part);
   delete ix;
@@ -557,7 +567,7 @@ extern "C" int rs_index_add(rs_index* ix, const void* emb, int64_t n, void* stre
                                 cudaMemcpyDeviceToDevice, st),
                 "cudaMemcpyAsync(add)");
   int rc = rs::launch_norms((char*)ix->data + size_t(ix->ntotal) * row, n, ix->dim, ix->dtype,
-                            ix->norms + ix->ntotal, st);
+                            ix->norms + ix->ntotal, st, ix->norm_max);
   if (rc) return rc;
   ix->ntotal += n;
   return RS_OK;
@@ -566,6 +576,10 @@ extern "C" int rs_index_add(rs_index* ix, const void* emb, int64_t n, void* stre
 extern "C" int rs_index_reset(rs_index* ix) {
   RS_REQUIRE(ix != nullptr, "index is NULL");
   ix->ntotal = 0;
+  if (ix->norm_max) {
+    DeviceGuard g(ix->device);
+    RS_CHECK_CUDA(cudaMemset(ix->norm_max, 0, sizeof(float)), "cudaMemset(norm_max)");
+  }
   return RS_OK;
 }
 

@@ -7,10 +7,14 @@
 //   * CTA r stages query rows [256*qt + 128*r, +128) (A half) and corpus rows
 //     [c0 + 128*r, +128) (B half) per k-block — each SM pulls 32 KB per
 //     512-cycle k-block (64 B/clk) instead of the 48 KB (96 B/clk) of the
-//     single-CTA tile, and the freed shared memory buys a 5-deep TMA ring;
+//     single-CTA tile, and the freed shared memory buys a deeper TMA ring;
 //   * the leader CTA (rank 0) issues the MMAs; its TMEM receives query rows
 //     0-127 of the tile and the peer's TMEM rows 128-255, all 256 chunk
-//     columns each, so every CTA's epilogue owns 128 queries x 256 chunks.
+//     columns each, so every CTA's epilogue owns 128 queries x 256 chunks;
+//   * the epilogue keeps each query's running top-k in REGISTERS (RegTopK,
+//     topk_rows.cuh): a branch-free 3-instruction-per-score filter appends
+//     candidates to a small smem buffer, flushed in warp-wide batches into a
+//     sorted register list (no shared-memory heap latency chains).
 //
 // Synchronisation (all mbarriers):
 //   full[s]   leader only; the leader's producer arms 2 x 32 KB, both CTAs'
@@ -33,18 +37,25 @@ namespace {
 
 using namespace sm100;
 
+#ifndef RS_PAIR_STAGES
+#define RS_PAIR_STAGES 6
+#endif
+#ifndef RS_PAIR_BUF
+#define RS_PAIR_BUF 16  // swept 8..48 with 5/6 stages on B200: 6 stages x 16 best
+#endif
+
 constexpr int BM = 128;         // query rows per CTA (TMEM lanes)
 constexpr int PM = 2 * BM;      // query rows per pair tile
 constexpr int BN = kTcBN;       // corpus columns per tile (both CTAs)
 constexpr int HB = BN / 2;      // corpus rows staged per CTA
 constexpr int BK = 64;
-constexpr int STAGES = 5;
-constexpr int KCAP = kTcMaxK;
-// Candidate buffer per row: flushing only when some lane holds > BUF - CHECK
-// entries makes each heap-maintenance pass batch many candidates across the
-// warp's lanes (a flush on every hit would serialise per-lane heap pushes).
-constexpr int BUF = 24;
+constexpr int STAGES = RS_PAIR_STAGES;
+constexpr int KREG = kTcMaxK;   // register top-k capacity (k <= 40)
+// candidate buffer per row; a warp flushes when one of its lanes holds more
+// than BUF - CHECK entries, so every flush batches many candidates per lane
+constexpr int BUF = RS_PAIR_BUF;
 constexpr int CHECK = 8;
+constexpr int EPI_COLS = 32;    // TMEM columns per tcgen05.ld / wait
 constexpr int A_BYTES = BM * BK * 2;
 constexpr int B_BYTES = HB * BK * 2;
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -61,12 +72,13 @@ struct __align__(8) SmemTail {
   uint32_t tmem_base;
 };
 
-constexpr size_t OFF_HEAP = size_t(STAGES) * STAGE_BYTES;
-constexpr size_t OFF_BUF = OFF_HEAP + size_t(KCAP) * BM * 8;
+constexpr size_t OFF_BUF = size_t(STAGES) * STAGE_BYTES;
 constexpr size_t OFF_CN = OFF_BUF + size_t(BUF) * BM * 8;
 constexpr size_t OFF_TAIL = OFF_CN + 2 * BN * sizeof(float);
 constexpr size_t SMEM_BYTES = OFF_TAIL + sizeof(SmemTail);
 static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
+
+using TopK = RegTopK<KREG, BM, BUF>;
 
 struct Params {
   const float* qn;
@@ -89,13 +101,30 @@ __device__ __forceinline__ void unit_coords(int64_t u, const Params& p, int& qt,
   if (r1 > p.n) r1 = p.n;
 }
 
+// Optional per-role cycle accounting (tuning builds: -DRS_PAIR_PROFILE=1;
+// read back with tools/pair_profile.py).
+#ifndef RS_PAIR_PROFILE
+#define RS_PAIR_PROFILE 0
+#endif
+#if RS_PAIR_PROFILE
+__device__ unsigned long long g_pair_prof[1024][8];
+#define PROF(slot, stmt)                       \
+  do {                                         \
+    const long long _t0 = clock64();           \
+    stmt;                                      \
+    prof[slot] += clock64() - _t0;             \
+  } while (0)
+#else
+#define PROF(slot, stmt) stmt
+#endif
+
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     score_topk_pair_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmc,
                            const Params p) {
+  // no static shared memory: the dynamic window starts at the CTA's shared
+  // base, 1024-aligned as SWIZZLE_128B requires
   extern __shared__ __align__(1024) uint8_t smem[];
   SmemTail* tail = reinterpret_cast<SmemTail*>(smem + OFF_TAIL);
-  uint64_t* heap = reinterpret_cast<uint64_t*>(smem + OFF_HEAP);
-  uint64_t* buf = reinterpret_cast<uint64_t*>(smem + OFF_BUF);
   float* cns = reinterpret_cast<float*>(smem + OFF_CN);
 
   const int warp = threadIdx.x >> 5;
@@ -130,6 +159,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   cluster_sync();  // barriers of both CTAs initialised, TMEM allocated
   tc_fence_after();
   const uint32_t tmem_base = tail->tmem_base;
+#if RS_PAIR_PROFILE
+  unsigned long long prof[8] = {};
+  const long long t_start = clock64();
+#endif
 
   if (warp == 0) {
     if (lane == 0) {
@@ -144,12 +177,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         unit_coords(u, p, qt, seg, r0, r1);
         for (int64_t c0 = r0; c0 < r1; c0 += BN) {
           for (int kb = 0; kb < p.kblocks; ++kb) {
-            mbar_wait(&tail->empty[stage], phase ^ 1);
+            PROF(0, mbar_wait(&tail->empty[stage], phase ^ 1));
             uint8_t* sa = smem + size_t(stage) * STAGE_BYTES;
             const uint32_t full_leader = mapa_shared(smem_u32(&tail->full[stage]), 0);
+#ifdef RS_PAIR_NO_TMA  // timing experiment only: MMA pipeline with no operand traffic
+            (void)sa;
+            (void)full_leader;
+            if (leader) mbar_arrive(&tail->full[stage]);
+#else
             if (leader) mbar_arrive_expect_tx(&tail->full[stage], 2 * STAGE_BYTES);
             tma_load_2d_pair(&tmq, full_leader, sa, kb * BK, qt * PM + int(rank) * BM, pol_q);
             tma_load_2d_pair(&tmc, full_leader, sa + A_BYTES, kb * BK, int32_t(c0) + int(rank) * HB, pol_c);
+#endif
             if (++stage == STAGES) {
               stage = 0;
               phase ^= 1;
@@ -171,9 +210,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         for (int64_t c0 = r0; c0 < r1; c0 += BN, ++tile_iter) {
           const uint32_t acc = tile_iter & 1;
           // leader: both epilogues released TMEM buffer acc; peer: own epilogue released cns[acc]
-          mbar_wait(&tail->tempty[acc], ((tile_iter >> 1) & 1) ^ 1);
+          PROF(1, mbar_wait(&tail->tempty[acc], ((tile_iter >> 1) & 1) ^ 1));
           tc_fence_after();
           {
+            // this tile's corpus norms for the epilogue (the index pads the
+            // norms array, so rounding the copy up to 16 B stays in bounds)
             const int valid = int(r1 - c0 < BN ? r1 - c0 : BN);
             const uint32_t bytes = uint32_t((valid + 3) & ~3) * 4u;
             mbar_arrive_expect_tx(&tail->tfull[acc], bytes);
@@ -182,7 +223,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           if (!leader) continue;
           const uint32_t d_tmem = tmem_base + acc * BN;
           for (int kb = 0; kb < p.kblocks; ++kb) {
-            mbar_wait(&tail->full[stage], phase);
+            PROF(2, mbar_wait(&tail->full[stage], phase));
             tc_fence_after();
             const uint32_t a_addr = smem_u32(smem + size_t(stage) * STAGE_BYTES);
             const uint32_t b_addr = a_addr + A_BYTES;
@@ -203,9 +244,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp >= EPI_WARP0) {
     // ===== epilogue (both CTAs): 128 queries x 256 chunks per tile =====
-    const int ew = warp - EPI_WARP0;
+    const int ew = warp - EPI_WARP0;  // == warp % 4: the TMEM lane quadrant this warp may read
     const int row = ew * 32 + lane;
-    RowTopK<BM, BUF> rt{heap, buf, row, p.k, 0, 0, 0.0f};
+    TopK rt;
+    rt.k = p.k;
+    rt.wbase = smem_u32(smem + OFF_BUF) + uint32_t(row) * 8u;
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tail->tempty[0]), 0);
     const uint32_t tempty_leader1 = mapa_shared(smem_u32(&tail->tempty[1]), 0);
     uint32_t tile_iter = 0;
@@ -214,44 +257,59 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       int64_t r0, r1;
       unit_coords(u, p, qt, seg, r0, r1);
       const int64_t qrow = int64_t(qt) * PM + int64_t(rank) * BM + row;
-      const float qnv = qrow < p.nq ? p.qn[qrow] : 0.0f;
+      rt.qn = qrow < p.nq ? p.qn[qrow] : 0.0f;
       rt.reset();
       for (int64_t c0 = r0; c0 < r1; c0 += BN, ++tile_iter) {
         const uint32_t acc = tile_iter & 1;
         const int valid = int(r1 - c0 < BN ? r1 - c0 : BN);
         const float* cn_t = cns + acc * BN;
-        mbar_wait(&tail->tfull[acc], (tile_iter >> 1) & 1);
+        PROF(3, mbar_wait(&tail->tfull[acc], (tile_iter >> 1) & 1));
         tc_fence_after();
         const uint32_t t_row = tmem_base + (uint32_t(ew * 32) << 16) + acc * BN;
         const uint32_t id0 = uint32_t(p.id_base + c0);
 #pragma unroll 1
-        for (int ch = 0; ch < BN / 32; ++ch) {
-          if (ch * 32 >= valid) break;  // warp-uniform
-          uint32_t r[32];
+        for (int base = 0; base < BN; base += EPI_COLS) {
+          if (base >= valid) break;  // warp-uniform
+          uint32_t r[EPI_COLS];
           __syncwarp();
-          tmem_ld_32x32b_x32(t_row + ch * 32, r);
+          tmem_ld_32x32b_x32(t_row + base, r);
           tmem_wait_ld();
-          if (ch * 32 + 32 <= valid) {
+#ifdef RS_PAIR_EPI_NOP  // timing experiment only: the MMA pipeline without the top-k work
+          if (__uint_as_float(r[0]) == 12345.0f) rt.append_raw(0.0f, id0);
+          continue;
+#endif
+          if (base + EPI_COLS <= valid) {
 #pragma unroll
-            for (int g = 0; g < 32; g += 8)
-              epi_group8<BM, BUF, CHECK, true>(rt, r + g, cn_t + ch * 32 + g, qnv, id0 + ch * 32 + g, 8);
+            for (int g = 0; g < EPI_COLS; g += 8)
+              epi_group8r<KREG, BM, BUF, CHECK, true>(rt, r + g, cn_t + base + g, id0 + base + g, 8);
           } else {
 #pragma unroll
-            for (int g = 0; g < 32; g += 8)
-              epi_group8<BM, BUF, CHECK, false>(rt, r + g, cn_t + ch * 32 + g, qnv, id0 + ch * 32 + g,
-                                                valid - ch * 32 - g);
+            for (int g = 0; g < EPI_COLS; g += 8)
+              epi_group8r<KREG, BM, BUF, CHECK, false>(rt, r + g, cn_t + base + g, id0 + base + g,
+                                                       valid - base - g);
           }
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
+          // the TMEM reads completed (tcgen05.wait::ld), so a relaxed remote
+          // arrive suffices (a release at cluster scope costs a MEMBAR.GPU)
           mbar_arrive(&tail->tempty[acc]);
-          if (!leader) mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
+          if (!leader) mbar_arrive_cluster_relaxed(acc ? tempty_leader1 : tempty_leader0);
         }
       }
+      // every lane flushes (warp-collective), then writes its row if it is a real query
+      PROF(5, rt.flush());
       if (qrow < p.nq) rt.finish(p.part + (qrow * p.segments + seg) * p.k);
     }
   }
+#if RS_PAIR_PROFILE
+  prof[7] = clock64() - t_start;
+  if (lane == 0 && warp < 8 && blockIdx.x < 1024) {
+    for (int i = 0; i < 8; ++i)
+      if (prof[i]) atomicAdd(&g_pair_prof[blockIdx.x][i], prof[i] / ((warp >= EPI_WARP0 && i == 7) ? 4 : 1));
+  }
+#endif
 
   __syncwarp();
   tc_fence_before();
@@ -263,6 +321,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 }
 
 }  // namespace
+
+#if RS_PAIR_PROFILE
+extern "C" int rs_debug_pair_profile(unsigned long long* host_out, int nblocks) {
+  cudaDeviceSynchronize();
+  return int(cudaMemcpyFromSymbol(host_out, g_pair_prof, sizeof(unsigned long long) * 8 * nblocks));
+}
+extern "C" int rs_debug_pair_profile_reset() {
+  static unsigned long long zeros[1024][8];
+  return int(cudaMemcpyToSymbol(g_pair_prof, zeros, sizeof(zeros)));
+}
+#endif
 
 int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap& tmc, const float* qn, const float* cn,
                            int64_t nq, int64_t n, int dim, int k, int64_t id_base, const SearchPlan& plan,

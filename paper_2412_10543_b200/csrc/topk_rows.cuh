@@ -3,12 +3,12 @@
 // One thread owns one query row.  Scores arrive in ascending chunk-id order.
 // A candidate passes a register threshold test (d <= tau, tau = current k-th
 // best distance) and is appended to a small per-row buffer in shared memory
-// (a predicated store — no divergence on the common reject path).  When any
-// lane of the warp nears a full buffer the whole warp flushes in lockstep:
-// each lane pushes its buffered keys into its own bounded max-heap (root =
-// current k-th best), then refreshes tau.  Keys are packed u64
-// (fp32 distance bits << 32 | uint32 chunk id) so the heap order is exactly
-// (distance asc, id asc) — the north star's lower-index tie rule.
+// (predicated stores through a running write pointer — no divergence on the
+// reject path).  When any lane of the warp nears a full buffer the whole warp
+// flushes in lockstep: each lane pushes its buffered keys into its own bounded
+// max-heap (root = current k-th best), then refreshes tau.  Keys are packed
+// u64 (fp32 distance bits << 32 | uint32 chunk id) so the heap order is
+// exactly (distance asc, id asc) — the north star's lower-index tie rule.
 //
 // Shared-memory layout is slot-major ([slot][row]) so lanes touching the
 // same slot hit consecutive 8-byte words.
@@ -32,16 +32,23 @@ struct RowTopK {
   int nk;  // heap size
   int nb;  // buffered candidates
   float tau;
+  float qn = 0.0f;      // this row's |q|^2 (epilogues that compute distances here)
+  uint32_t wp = 0;      // shared-window byte address of the next buffer slot (append_raw)
+
+  __device__ __forceinline__ uint32_t buf_base() const {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(buf + row));
+  }
 
   __device__ __forceinline__ void reset() {
     nk = 0;
     nb = 0;
     tau = __int_as_float(0x7f800000);  // +inf
+    wp = buf_base();
   }
 
   __device__ __forceinline__ uint64_t& H(int i) { return heap[i * ROWS + row]; }
 
-  // Predicated append of one candidate.
+  // Predicated append of one clamped candidate.
   __device__ __forceinline__ void offer(float d, uint32_t id) {
     if (d <= tau) append(d, id);
   }
@@ -49,6 +56,13 @@ struct RowTopK {
     buf[nb * ROWS + row] = make_key(d, id);
     ++nb;
   }
+  // Append an unclamped distance through the write pointer (2 instructions
+  // when predicated); negative round-off is clamped to 0 at flush time.
+  __device__ __forceinline__ void append_raw(float e, uint32_t id) {
+    asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(wp), "r"(id), "r"(__float_as_uint(e)) : "memory");
+    wp += ROWS * 8;
+  }
+  __device__ __forceinline__ int buffered() const { return nb + int((wp - buf_base()) / (ROWS * 8)); }
 
   __device__ void push(uint64_t key) {
     if (nk < k) {  // sift up
@@ -82,9 +96,26 @@ struct RowTopK {
     }
   }
 
+#ifdef RS_TOPK_PROFILE
+  unsigned long long flush_cycles = 0, flushes = 0;
   __device__ void flush() {
-    for (int j = 0; j < nb; ++j) push(buf[j * ROWS + row]);
+    const long long t0 = clock64();
+    flush_impl();
+    flush_cycles += clock64() - t0;
+    ++flushes;
+  }
+  __device__ void flush_impl() {
+#else
+  __device__ void flush() {
+#endif
+    const int n = buffered();
+    for (int j = 0; j < n; ++j) {
+      uint64_t key = buf[j * ROWS + row];
+      if (!(key_dist(key) > 0.0f)) key &= 0xffffffffull;  // clamp negative / -0 distances to +0
+      push(key);
+    }
     nb = 0;
+    wp = buf_base();
     if (nk == k) tau = key_dist(H(0));
   }
 
@@ -121,9 +152,8 @@ struct RowTopK {
 // TMEM, corpus norms `cn` in smem): 3 instructions per score (FADD
 // |q|^2+|c|^2, FFMA -2<q,c>, FSETP d <= tau, the compiler folds the 8 compares
 // into FMNMX3 + one FSETP) plus one warp vote per group; candidate append and
-// heap maintenance only run when some lane of the warp has a candidate (rare
-// once the heaps are full).  Exact: the filter uses the same rounded distance
-// that is stored.
+// heap maintenance only run when some lane of the warp has a candidate.
+// Exact: the filter uses the same rounded distance that is stored.
 template <int ROWS, int BUF, int CHECK, bool FULL>
 __device__ __forceinline__ void epi_group8(RowTopK<ROWS, BUF>& rt, const uint32_t* r, const float* cn, float qnv,
                                            uint32_t id, int lim) {
@@ -144,6 +174,180 @@ __device__ __forceinline__ void epi_group8(RowTopK<ROWS, BUF>& rt, const uint32_
       if ((FULL || j < lim) && e[j] <= rt.tau) rt.append(e[j] > 0.0f ? e[j] : 0.0f, id + j);
     if (__any_sync(0xffffffffu, rt.nb > BUF - CHECK)) rt.flush();
   }
+}
+
+// Packed-pair variant: the exact distances of 8 columns with 4 FADD2 + 4 FFMA2
+// (|q|^2 + |c|^2 pairs, then -2<q,c> + that), min-folded to one compare; the
+// slow path (some lane of the warp has a candidate — frequent at warp scale,
+// rare per lane) is 3 predicated instructions per column: compare, store
+// through the write pointer, bump the pointer.  Distances are bit-identical
+// to epi_group8 (same fl(fl(qn + cn) - 2s) rounding, clamp at flush).
+template <int ROWS, int BUF, int CHECK, bool FULL>
+__device__ __forceinline__ void epi_group8x(RowTopK<ROWS, BUF>& rt, const uint32_t* r, const float* cn,
+                                            uint32_t id, int lim) {
+  static_assert(BUF >= CHECK, "buffer must hold one group");
+  const float4 a = *reinterpret_cast<const float4*>(cn);
+  const float4 b = *reinterpret_cast<const float4*>(cn + 4);
+  const float2 q2 = make_float2(rt.qn, rt.qn);
+  const float2 m2 = make_float2(-2.0f, -2.0f);
+  const float2 e0 = __ffma2_rn(make_float2(__uint_as_float(r[0]), __uint_as_float(r[1])), m2,
+                               __fadd2_rn(q2, make_float2(a.x, a.y)));
+  const float2 e1 = __ffma2_rn(make_float2(__uint_as_float(r[2]), __uint_as_float(r[3])), m2,
+                               __fadd2_rn(q2, make_float2(a.z, a.w)));
+  const float2 e2 = __ffma2_rn(make_float2(__uint_as_float(r[4]), __uint_as_float(r[5])), m2,
+                               __fadd2_rn(q2, make_float2(b.x, b.y)));
+  const float2 e3 = __ffma2_rn(make_float2(__uint_as_float(r[6]), __uint_as_float(r[7])), m2,
+                               __fadd2_rn(q2, make_float2(b.z, b.w)));
+  const float e[8] = {e0.x, e0.y, e1.x, e1.y, e2.x, e2.y, e3.x, e3.y};
+  float mn = __int_as_float(0x7f800000);
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    if (FULL || j < lim) mn = fminf(mn, e[j]);
+  if (__any_sync(0xffffffffu, mn <= rt.tau)) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if ((FULL || j < lim) && e[j] <= rt.tau) rt.append_raw(e[j], id + j);
+    if (__any_sync(0xffffffffu, rt.buffered() > BUF - CHECK)) rt.flush();
+  }
+}
+
+// Branch-free variant: at warp scale nearly every 8-column group holds some
+// lane's candidate (k ln(n/k) hits per row over n columns, x 32 rows), so the
+// vote + slow path of epi_group8x is almost always taken; here every column
+// is compare + predicated store + predicated pointer bump, with one warp vote
+// per group only for the (rare) buffer flush.
+template <int ROWS, int BUF, int CHECK, bool FULL>
+__device__ __forceinline__ void epi_group8p(RowTopK<ROWS, BUF>& rt, const uint32_t* r, const float* cn,
+                                            uint32_t id, int lim) {
+  static_assert(BUF >= CHECK, "buffer must hold one group");
+  const float4 a = *reinterpret_cast<const float4*>(cn);
+  const float4 b = *reinterpret_cast<const float4*>(cn + 4);
+  const float2 q2 = make_float2(rt.qn, rt.qn);
+  const float2 m2 = make_float2(-2.0f, -2.0f);
+  const float2 e0 = __ffma2_rn(make_float2(__uint_as_float(r[0]), __uint_as_float(r[1])), m2,
+                               __fadd2_rn(q2, make_float2(a.x, a.y)));
+  const float2 e1 = __ffma2_rn(make_float2(__uint_as_float(r[2]), __uint_as_float(r[3])), m2,
+                               __fadd2_rn(q2, make_float2(a.z, a.w)));
+  const float2 e2 = __ffma2_rn(make_float2(__uint_as_float(r[4]), __uint_as_float(r[5])), m2,
+                               __fadd2_rn(q2, make_float2(b.x, b.y)));
+  const float2 e3 = __ffma2_rn(make_float2(__uint_as_float(r[6]), __uint_as_float(r[7])), m2,
+                               __fadd2_rn(q2, make_float2(b.z, b.w)));
+  const float e[8] = {e0.x, e0.y, e1.x, e1.y, e2.x, e2.y, e3.x, e3.y};
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    if ((FULL || j < lim) && e[j] <= rt.tau) rt.append_raw(e[j], id + j);
+  if (__any_sync(0xffffffffu, rt.buffered() > BUF - CHECK)) rt.flush();
+}
+
+// ---------------------------------------------------------------------------
+// Register-resident streaming top-k (the CTA-pair kernel's epilogue state).
+//
+// Profiling the smem heap showed each epilogue warp spending ~30% of the
+// kernel in flushes: a heap sift is a chain of dependent shared-memory loads
+// (~500 cycles per push) and one warp per scheduler cannot hide it.  Here the
+// current best KREG (distance, id) pairs live in registers as a sorted list;
+// inserting a candidate is a fully unrolled, branch-free compare/select sweep
+// (each slot depends only on the old values of itself and its predecessor, so
+// all KREG updates issue back to back).  Candidates still go through the smem
+// append buffer (cheap predicated stores) and are inserted in batches.
+//
+// Order: candidates of a row arrive with strictly increasing chunk ids, so a
+// new element goes after existing equal distances — a strict "<" realises
+// the (distance asc, id asc) tie rule without comparing ids.
+template <int KREG, int ROWS, int BUF>
+struct RegTopK {
+  float d[KREG];
+  uint32_t id[KREG];
+  int k;          // <= KREG
+  float tau;      // d[k-1] (current k-th best), +inf until k candidates seen
+  float qn;       // this row's |q|^2
+  uint32_t wbase; // shared-window byte address of this row's buffer slot 0
+  uint32_t wp;    // next free buffer slot
+
+  __device__ __forceinline__ void reset() {
+#pragma unroll
+    for (int j = 0; j < KREG; ++j) {
+      d[j] = __int_as_float(0x7f800000);
+      id[j] = 0xffffffffu;
+    }
+    tau = __int_as_float(0x7f800000);
+    wp = wbase;
+  }
+
+  __device__ __forceinline__ void append_raw(float e, uint32_t cid) {
+    asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(wp), "r"(cid), "r"(__float_as_uint(e)) : "memory");
+    wp += ROWS * 8;
+  }
+  __device__ __forceinline__ int buffered() const { return int((wp - wbase) / (ROWS * 8)); }
+
+  __device__ __forceinline__ void insert(float xd, uint32_t xid) {
+#pragma unroll
+    for (int j = KREG - 1; j >= 1; --j) {
+      const bool lt_prev = xd < d[j - 1];
+      const bool lt_cur = xd < d[j];
+      id[j] = lt_prev ? id[j - 1] : (lt_cur ? xid : id[j]);
+      d[j] = lt_prev ? d[j - 1] : (lt_cur ? xd : d[j]);
+    }
+    const bool lt0 = xd < d[0];
+    id[0] = lt0 ? xid : id[0];
+    d[0] = lt0 ? xd : d[0];
+  }
+
+  __device__ __forceinline__ void refresh_tau() {
+    float t = d[0];
+#pragma unroll
+    for (int j = 1; j < KREG; ++j)
+      if (j == k - 1) t = d[j];
+    tau = t;
+  }
+
+  // Warp-collective: every lane inserts its buffered candidates (lockstep over
+  // the warp's largest buffer; lanes past their own count insert +inf = no-op).
+  __device__ __forceinline__ void flush() {
+    const int n = buffered();
+    const int nmax = __reduce_max_sync(0xffffffffu, n);
+    for (int j = 0; j < nmax; ++j) {
+      uint32_t lo = 0, hi = 0x7f800000u;
+      if (j < n) asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(lo), "=r"(hi) : "r"(wbase + j * ROWS * 8));
+      float xd = __uint_as_float(hi);
+      xd = xd > 0.0f ? xd : (j < n ? 0.0f : xd);  // clamp negative round-off (and -0) to +0
+      if (__any_sync(0xffffffffu, xd < tau)) insert(xd < tau ? xd : __int_as_float(0x7f800000), lo);
+    }
+    wp = wbase;
+    refresh_tau();
+  }
+
+  // Write the k best keys (call the warp-collective flush() first, with the
+  // whole warp converged; this part is per lane).
+  __device__ __forceinline__ void finish(uint64_t* __restrict__ out) const {
+#pragma unroll
+    for (int j = 0; j < KREG; ++j)
+      if (j < k) out[j] = isinf(d[j]) ? ~0ull : make_key(d[j], id[j]);
+  }
+};
+
+// Branch-free fast path over 8 columns for RegTopK (see epi_group8p).
+template <int KREG, int ROWS, int BUF, int CHECK, bool FULL>
+__device__ __forceinline__ void epi_group8r(RegTopK<KREG, ROWS, BUF>& rt, const uint32_t* r, const float* cn,
+                                            uint32_t id, int lim) {
+  static_assert(BUF >= CHECK, "buffer must hold one group");
+  const float4 a = *reinterpret_cast<const float4*>(cn);
+  const float4 b = *reinterpret_cast<const float4*>(cn + 4);
+  const float2 q2 = make_float2(rt.qn, rt.qn);
+  const float2 m2 = make_float2(-2.0f, -2.0f);
+  const float2 e0 = __ffma2_rn(make_float2(__uint_as_float(r[0]), __uint_as_float(r[1])), m2,
+                               __fadd2_rn(q2, make_float2(a.x, a.y)));
+  const float2 e1 = __ffma2_rn(make_float2(__uint_as_float(r[2]), __uint_as_float(r[3])), m2,
+                               __fadd2_rn(q2, make_float2(a.z, a.w)));
+  const float2 e2 = __ffma2_rn(make_float2(__uint_as_float(r[4]), __uint_as_float(r[5])), m2,
+                               __fadd2_rn(q2, make_float2(b.x, b.y)));
+  const float2 e3 = __ffma2_rn(make_float2(__uint_as_float(r[6]), __uint_as_float(r[7])), m2,
+                               __fadd2_rn(q2, make_float2(b.z, b.w)));
+  const float e[8] = {e0.x, e0.y, e1.x, e1.y, e2.x, e2.y, e3.x, e3.y};
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    if ((FULL || j < lim) && e[j] <= rt.tau) rt.append_raw(e[j], id + j);
+  if (__any_sync(0xffffffffu, rt.buffered() > BUF - CHECK)) rt.flush();
 }
 
 // Distance from the fused epilogue: ||q||^2 + ||c||^2 - 2<q,c>, negative

@@ -1,0 +1,50 @@
+"""Per-role cycle accounting of the CTA-pair kernel (tuning build with
+-DRS_PAIR_PROFILE=1, selected via RAGSCHED_B200_LIB).  Prints, for leader and
+peer CTAs, the share of kernel time each role spends waiting."""
+
+import ctypes
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+from paper_2412_10543_b200 import IndexFlatL2, _lib  # noqa: E402
+
+
+def main(n=2_000_000, nq=8192, d=1024):
+    lib = _lib.load()
+    g = torch.Generator(device="cuda").manual_seed(0)
+    c = torch.nn.functional.normalize(torch.randn(n, d, generator=g, device="cuda"), dim=1).bfloat16()
+    q = torch.nn.functional.normalize(torch.randn(nq, d, generator=g, device="cuda"), dim=1).bfloat16()
+    ix = IndexFlatL2(d, capacity=n)
+    ix.add(c)
+    ix.search_keys(q, 35)
+    torch.cuda.synchronize()
+    lib.rs_debug_pair_profile_reset()
+    ix.search_keys(q, 35)
+    torch.cuda.synchronize()
+    buf = (ctypes.c_ulonglong * (1024 * 8))()
+    lib.rs_debug_pair_profile(buf, 1024)
+    a = np.frombuffer(buf, dtype=np.uint64).reshape(1024, 8).astype(np.float64)
+    plan = ix.last_plan()
+    ctas = 2 * plan["ctas"]
+    a = a[:ctas]
+    # slot 7 = kernel cycles from warps 0, 1 and the 4 epilogue warps (each /4);
+    # warps 2, 3 finish immediately and add ~0
+    names = {0: "producer wait empty", 1: "mma wait tempty", 3: "epilogue wait tfull (4 warps)",
+             5: "epilogue finish (4 warps)", 6: "epilogue TMEM ld wait (4 warps)",
+             2: "epilogue flush + mma wait full"}
+    for label, rows in (("leader", a[0::2]), ("peer", a[1::2])):
+        total = rows[:, 7] / 3.0
+        print(f"{label}: kernel {total.mean() / 1e6:.2f} Mcycles; flushes/warp {rows[:, 4].mean() / 4:.0f}")
+        for i, nm in names.items():
+            denom = total * (4 if i in (3, 5, 6) else 1)
+            print(f"   {nm:32s} {100 * (rows[:, i] / denom).mean():5.1f}%")
+    print(plan)
+
+
+if __name__ == "__main__":
+    main()
