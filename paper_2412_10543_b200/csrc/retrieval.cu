@@ -323,18 +323,29 @@ SearchPlan plan_search(int64_t nq, int64_t n, int bq, int bn, int ctas_capacity,
   const int64_t qt = ceil_div(std::max<int64_t>(nq, 1), bq);
   const int64_t nt = ceil_div(std::max<int64_t>(n, 1), bn);
   // With several query tiles the CTAs of one round share a segment through L2:
-  // cap the segment so the concurrently streamed window stays L2-resident.
+  // about ceil(ctas/qtiles)+1 segments are streamed at once, and together they
+  // must stay L2-resident (ncu at 10M x 1024: 48 MB segments re-read the
+  // corpus 17x from DRAM).  Budget 64 MB of the 126 MB L2 for the corpus
+  // window (the query tiles are pinned evict_last next to it).
   int64_t max_tps = nt;
-  if (share_l2 && qt > 1) max_tps = std::max<int64_t>(1, (int64_t(48) << 20) / (int64_t(bn) * row_bytes));
+  if (share_l2 && qt > 1) {
+    const int64_t concurrent = ceil_div(ctas_capacity, qt) + 1;
+    max_tps = std::max<int64_t>(1, (int64_t(64) << 20) / (concurrent * int64_t(bn) * row_bytes));
+  }
+  // partial lists (8-byte keys, written then merged) must stay a small
+  // fraction of the work: <= 4 GB, costed against the GEMM time below
+  const int64_t list_bytes_per_seg = qt * int64_t(bq) * 40 * 8 * 2;
+  const double tile_secs = 2.0 * bq * bn * (row_bytes / 2) / (1.2e15 / std::max(ctas_capacity, 1));
   double best_cost = 1e300;
   for (int64_t tps = nt; tps >= 1;) {
     const int64_t segs = ceil_div(nt, tps);
     if (segs > 4096) break;
-    if (tps <= max_tps) {
+    if (tps <= max_tps && (segs * list_bytes_per_seg <= (int64_t(4) << 30) || best_cost == 1e300)) {
       const int64_t units = qt * segs;
       const int64_t rounds = ceil_div(units, ctas_capacity);
-      // per-unit overhead ~1 tile (pipeline fill + list write); merge cost ~ lists
-      const double cost = double(rounds) * double(tps + 1) + 1e-3 * double(segs);
+      // per-unit overhead ~1 tile (pipeline fill + list write) + the merge's HBM traffic
+      const double list_cost = double(segs * list_bytes_per_seg) / 6.5e12 / tile_secs;
+      const double cost = double(rounds) * double(tps + 1) + list_cost;
       if (cost < best_cost) {
         best_cost = cost;
         best.qtiles = int32_t(qt);
@@ -359,6 +370,7 @@ struct rs_index {
   void* data = nullptr;
   float* norms = nullptr;
   float* norm_max = nullptr;  // device scalar: max squared norm over the shard
+  int32_t* sched_counter = nullptr;  // device scalar: dynamic unit scheduler of the pair kernel
   float* qnorm = nullptr;
   int64_t qnorm_cap = 0;
   uint64_t* part = nullptr;
@@ -450,7 +462,7 @@ int run_partial(rs_index* ix, const void* queries, int64_t nq, int k, int64_t id
     rc = encode_kmajor_bf16_map(&tmc, ix->data, ix->ntotal, ix->dim, pair ? kTcBN / 2 : kTcBN);
     if (rc) return rc;
     rc = pair ? launch_score_topk_pair(tmq, tmc, ix->qnorm, ix->norms, nq, ix->ntotal, ix->dim, k, id_base, plan,
-                                       ix->part, st)
+                                       ix->part, ix->sched_counter, st)
               : launch_score_topk_tc(tmq, tmc, ix->qnorm, ix->norms, nq, ix->ntotal, ix->dim, k, id_base, plan,
                                      ix->part, st);
   } else {
@@ -502,6 +514,7 @@ extern "C" int rs_index_create(int32_t dim, int32_t dtype, int64_t capacity, int
     // granules of norms past the last row of a partial tile
     if (e == cudaSuccess) e = cudaMalloc(&ix->norms, sizeof(float) * (capacity + rs::kTcBN));
     if (e == cudaSuccess) e = cudaMalloc(&ix->norm_max, sizeof(float));
+    if (e == cudaSuccess) e = cudaMalloc(&ix->sched_counter, sizeof(int32_t));
     if (e == cudaSuccess) e = cudaMemset(ix->norm_max, 0, sizeof(float));
     if (e != cudaSuccess) {
       rs::set_error("cudaMalloc(corpus %lld x %d): %s", (long long)capacity, dim, cudaGetErrorString(e));
@@ -547,6 +560,7 @@ extern "C" int rs_index_destroy(rs_index* ix) {
   cudaFree(ix->data);
   cudaFree(ix->norms);
   cudaFree(ix->norm_max);
+  cudaFree(ix->sched_counter);
   cudaFree(ix->qnorm);
   cudaFree(ix->part);
   delete ix;

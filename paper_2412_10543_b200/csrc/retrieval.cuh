@@ -36,7 +36,7 @@ int launch_score_topk_tc(const CUtensorMap& tmq, const CUtensorMap& tmc, const f
 // CTA-pair (cta_group::2) variant, 256 queries per pair tile (score_topk_sm100_pair.cu).
 int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap& tmc, const float* qn, const float* cn,
                            int64_t nq, int64_t n, int dim, int k, int64_t id_base, const SearchPlan& plan,
-                           uint64_t* part, cudaStream_t st);
+                           uint64_t* part, int32_t* counter, cudaStream_t st);
 int encode_kmajor_bf16_map(CUtensorMap* map, const void* base, int64_t rows, int dim, int box_rows);
 
 // CUDA-core kernel for fp32 (and bf16 cross-checks), retrieval.cu.

@@ -14,7 +14,14 @@
 //   * the epilogue keeps each query's running top-k in REGISTERS (RegTopK,
 //     topk_rows.cuh): a branch-free 3-instruction-per-score filter appends
 //     candidates to a small smem buffer, flushed in warp-wide batches into a
-//     sorted register list (no shared-memory heap latency chains).
+//     sorted register list (no shared-memory heap latency chains);
+//   * units (query tile, corpus segment) are handed out DYNAMICALLY in
+//     segment-major order (one atomic per unit, published to both CTAs of
+//     the pair through a 4-deep smem ring): the units in flight are always
+//     consecutive, so the CTAs streaming a segment for different query tiles
+//     stay together and the segment is read from HBM about once (a static
+//     round-robin let pairs drift apart: ncu showed the 20 GB corpus read
+//     17x from DRAM).
 //
 // Synchronisation (all mbarriers):
 //   full[s]   leader only; the leader's producer arms 2 x 32 KB, both CTAs'
@@ -24,6 +31,8 @@
 //             the leader's MMA commit (multicast)
 //   tempty[a] leader: 8 warp arrivals (4 local + 4 remote from the peer);
 //             peer: its 4 local warps (gates its own norm copy)
+//   ufull[i]  both CTAs: unit id published (leader producer; remote for peer)
+//   uempty[i] leader: 11 consumers read the slot (5 local + 6 remote)
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -62,6 +71,8 @@ constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int TMEM_COLS = 2 * BN;
 constexpr int NUM_THREADS = 256;
 constexpr int EPI_WARP0 = 4;
+constexpr int URING = 4;        // unit-id ring depth
+constexpr uint32_t UCONSUMERS = 11;  // leader: MMA + 4 epi; peer: producer + norm thread + 4 epi
 constexpr uint32_t IDESC = umma_idesc_bf16_f32(PM, BN);
 
 struct __align__(8) SmemTail {
@@ -69,6 +80,9 @@ struct __align__(8) SmemTail {
   uint64_t empty[STAGES];
   uint64_t tfull[2];
   uint64_t tempty[2];
+  uint64_t ufull[URING];
+  uint64_t uempty[URING];
+  int32_t uid[URING];
   uint32_t tmem_base;
 };
 
@@ -90,6 +104,7 @@ struct Params {
   int32_t qtiles, segments;
   int64_t seg_rows;
   uint64_t* part;
+  int32_t* counter;  // dynamic unit counter (zeroed before the launch)
 };
 
 __device__ __forceinline__ void unit_coords(int64_t u, const Params& p, int& qt, int& seg, int64_t& r0,
@@ -99,6 +114,21 @@ __device__ __forceinline__ void unit_coords(int64_t u, const Params& p, int& qt,
   r0 = int64_t(seg) * p.seg_rows;
   r1 = r0 + p.seg_rows;
   if (r1 > p.n) r1 = p.n;
+}
+
+// Consumer side of the unit ring: wait for slot i, read the unit id, release
+// the slot to the leader's producer.  Returns the unit (-1 = no more work).
+__device__ __forceinline__ int next_unit(SmemTail* tail, uint32_t i, bool leader, bool arrive) {
+  const int slot = int(i % URING);
+  mbar_wait_cluster(&tail->ufull[slot], (i / URING) & 1);
+  const int u = *reinterpret_cast<volatile int32_t*>(&tail->uid[slot]);
+  if (arrive) {
+    if (leader)
+      mbar_arrive(&tail->uempty[slot]);
+    else
+      mbar_arrive_cluster(mapa_shared(smem_u32(&tail->uempty[slot]), 0));
+  }
+  return u;
 }
 
 // Optional per-role cycle accounting (tuning builds: -DRS_PAIR_PROFILE=1;
@@ -132,8 +162,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
   const int64_t units = int64_t(p.qtiles) * p.segments;
-  const int64_t pair = blockIdx.x >> 1;
-  const int64_t npairs = gridDim.x >> 1;
   if ((smem_u32(smem) & 1023u) != 0) __trap();
 
   if (warp == 0 && lane == 0) {
@@ -148,6 +176,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tail->tfull[a], 2);
       mbar_init(&tail->tempty[a], leader ? 8 : 4);
+    }
+    for (int i = 0; i < URING; ++i) {
+      mbar_init(&tail->ufull[i], 1);
+      mbar_init(&tail->uempty[i], leader ? UCONSUMERS : 1);
     }
     fence_barrier_init();
   }
@@ -166,12 +198,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      // ===== TMA producer (both CTAs): own A half + own B half per k-block =====
+      // ===== TMA producer (both CTAs): own A half + own B half per k-block;
+      //       the leader's producer also schedules the units =====
       const uint64_t pol_q = policy_evict_last();
       const uint64_t pol_c = p.qtiles == 1 ? policy_evict_first() : policy_evict_normal();
       int stage = 0;
       uint32_t phase = 0;
-      for (int64_t u = pair; u < units; u += npairs) {
+      for (uint32_t i = 0;; ++i) {
+        int u;
+        if (leader) {
+          const int slot = int(i % URING);
+          mbar_wait(&tail->uempty[slot], ((i / URING) & 1) ^ 1);
+          u = atomicAdd(p.counter, 1);
+          if (u >= units) u = -1;
+          tail->uid[slot] = u;
+          st_shared_cluster_u32(mapa_shared(smem_u32(&tail->uid[slot]), 1), uint32_t(u));
+          mbar_arrive(&tail->ufull[slot]);
+          mbar_arrive_cluster(mapa_shared(smem_u32(&tail->ufull[slot]), 1));  // release: orders the remote store
+        } else {
+          u = next_unit(tail, i, false, true);
+        }
+        if (u < 0) break;
         int qt, seg;
         int64_t r0, r1;
         unit_coords(u, p, qt, seg, r0, r1);
@@ -203,7 +250,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       uint32_t tile_iter = 0;
-      for (int64_t u = pair; u < units; u += npairs) {
+      for (uint32_t i = 0;; ++i) {
+        const int u = next_unit(tail, i, leader, true);
+        if (u < 0) break;
         int qt, seg;
         int64_t r0, r1;
         unit_coords(u, p, qt, seg, r0, r1);
@@ -252,7 +301,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tail->tempty[0]), 0);
     const uint32_t tempty_leader1 = mapa_shared(smem_u32(&tail->tempty[1]), 0);
     uint32_t tile_iter = 0;
-    for (int64_t u = pair; u < units; u += npairs) {
+    for (uint32_t i = 0;; ++i) {
+      const int u = next_unit(tail, i, leader, false);
+      __syncwarp();
+      if (lane == 0) {  // one release per warp, after every lane read the slot
+        if (leader)
+          mbar_arrive(&tail->uempty[i % URING]);
+        else
+          mbar_arrive_cluster(mapa_shared(smem_u32(&tail->uempty[i % URING]), 0));
+      }
+      if (u < 0) break;
       int qt, seg;
       int64_t r0, r1;
       unit_coords(u, p, qt, seg, r0, r1);
@@ -335,7 +393,7 @@ extern "C" int rs_debug_pair_profile_reset() {
 
 int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap& tmc, const float* qn, const float* cn,
                            int64_t nq, int64_t n, int dim, int k, int64_t id_base, const SearchPlan& plan,
-                           uint64_t* part, cudaStream_t st) {
+                           uint64_t* part, int32_t* counter, cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
     RS_CHECK_CUDA(cudaFuncSetAttribute(score_topk_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -343,6 +401,7 @@ int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap& tmc, const
                   "cudaFuncSetAttribute(score_topk_pair_kernel)");
     attr_set = true;
   }
+  RS_CHECK_CUDA(cudaMemsetAsync(counter, 0, sizeof(int32_t), st), "cudaMemsetAsync(unit counter)");
   Params p{};
   p.qn = qn;
   p.cn = cn;
@@ -355,6 +414,7 @@ int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap& tmc, const
   p.segments = plan.segments;
   p.seg_rows = plan.seg_rows;
   p.part = part;
+  p.counter = counter;
   score_topk_pair_kernel<<<2 * plan.ctas, NUM_THREADS, SMEM_BYTES, st>>>(tmq, tmc, p);
   RS_CHECK_LAUNCH("score_topk_pair_kernel");
   return RS_OK;
