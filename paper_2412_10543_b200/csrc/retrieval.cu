@@ -328,6 +328,10 @@ SearchPlan plan_search(int64_t nq, int64_t n, int bq, int bn, int ctas_capacity,
   // corpus 17x from DRAM).  Budget 64 MB of the 126 MB L2 for the corpus
   // window (the query tiles are pinned evict_last next to it).
   int64_t max_tps = nt;
+  // (The CTA-pair kernel schedules units dynamically in segment-major order,
+  // so its concurrent units stay in lockstep without a segment-size cap and
+  // long segments keep the per-column top-k candidate rate low; it passes
+  // share_l2 = false.)
   if (share_l2 && qt > 1) {
     const int64_t concurrent = ceil_div(ctas_capacity, qt) + 1;
     max_tps = std::max<int64_t>(1, (int64_t(64) << 20) / (concurrent * int64_t(bn) * row_bytes));
@@ -427,7 +431,12 @@ int choose_algo(const rs_index* ix, int k) {
 rs::SearchPlan make_plan(const rs_index* ix, int algo, int64_t nq, int64_t n, int k) {
   using namespace rs;
   const int sms = sm_count(ix->device);
-  if (algo == RS_ALGO_TCGEN05) return plan_search(nq, n, 2 * kTcBM, kTcBN, sms / 2, int64_t(ix->dim) * 2, true);
+  if (algo == RS_ALGO_TCGEN05) {  // units of one cluster: kPairGroup pairs x 256 queries
+    SearchPlan p = plan_search(nq, n, 2 * kTcBM * kPairGroup, kTcBN, sms / (2 * kPairGroup), int64_t(ix->dim) * 2,
+                               /*share_l2=*/false);
+    p.lists_per_seg = kPairEpiGroups;
+    return p;
+  }
   if (algo == RS_ALGO_TCGEN05_1SM) return plan_search(nq, n, kTcBM, kTcBN, sms, int64_t(ix->dim) * 2, true);
   return plan_search(nq, n, kSimtBQ, kSimtBC, sms * simt_ctas_per_sm(ix->dtype, k),
                      int64_t(ix->dim) * esize(ix->dtype), true);
@@ -441,7 +450,7 @@ int run_partial(rs_index* ix, const void* queries, int64_t nq, int k, int64_t id
   RS_REQUIRE(!((ix->algo == RS_ALGO_TCGEN05 || ix->algo == RS_ALGO_TCGEN05_1SM) && algo == RS_ALGO_SIMT),
              "tcgen05 path needs bf16, dim %% 8 == 0 and k <= %d", kTcMaxK);
   const SearchPlan plan = make_plan(ix, algo, nq, ix->ntotal, k);
-  const size_t part_bytes = size_t(nq) * plan.segments * k * sizeof(uint64_t);
+  const size_t part_bytes = size_t(nq) * plan.lists() * k * sizeof(uint64_t);
   int rc = ensure_ws(ix, nq, part_bytes);
   if (rc) return rc;
   rc = launch_norms(queries, nq, ix->dim, ix->dtype, ix->qnorm, st);
@@ -459,7 +468,7 @@ int run_partial(rs_index* ix, const void* queries, int64_t nq, int k, int64_t id
     CUtensorMap tmq, tmc;
     rc = encode_kmajor_bf16_map(&tmq, queries, nq, ix->dim, kTcBM);
     if (rc) return rc;
-    rc = encode_kmajor_bf16_map(&tmc, ix->data, ix->ntotal, ix->dim, pair ? kTcBN / 2 : kTcBN);
+    rc = encode_kmajor_bf16_map(&tmc, ix->data, ix->ntotal, ix->dim, pair ? kTcBN / 2 / kPairGroup : kTcBN);
     if (rc) return rc;
     rc = pair ? launch_score_topk_pair(tmq, tmc, ix->qnorm, ix->norms, nq, ix->ntotal, ix->dim, k, id_base, plan,
                                        ix->part, ix->sched_counter, st)
@@ -623,7 +632,7 @@ extern "C" int rs_index_reserve(rs_index* ix, int64_t nq_max, int32_t k) {
   DeviceGuard g(ix->device);
   // worst case over the expected corpus size (capacity)
   const SearchPlan plan = make_plan(ix, choose_algo(ix, k), nq_max, std::max<int64_t>(ix->capacity, 1), k);
-  return ensure_ws(ix, nq_max, size_t(nq_max) * plan.segments * k * sizeof(uint64_t));
+  return ensure_ws(ix, nq_max, size_t(nq_max) * plan.lists() * k * sizeof(uint64_t));
 }
 
 extern "C" int rs_index_last_plan(const rs_index* ix, int32_t* segments, int32_t* qtiles, int32_t* ctas,
@@ -652,7 +661,7 @@ static int search_impl(rs_index* ix, const void* queries, int64_t nq, int32_t k,
   SearchPlan plan;
   rc = run_partial(ix, queries, nq, k, id_base, st, &plan);
   if (rc) return rc;
-  return launch_merge(ix->part, nq, plan.segments, k, /*list_stride=*/k, /*q_stride=*/int64_t(plan.segments) * k, k,
+  return launch_merge(ix->part, nq, plan.lists(), k, /*list_stride=*/k, /*q_stride=*/int64_t(plan.lists()) * k, k,
                       keep, D, I, keys, st);
 }
 

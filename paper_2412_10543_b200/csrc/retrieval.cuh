@@ -20,6 +20,8 @@ struct SearchPlan {
   int32_t segments = 0;
   int64_t seg_rows = 0;
   int32_t ctas = 0;
+  int32_t lists_per_seg = 1;  // sorted lists a unit writes per query (epilogue groups)
+  int32_t lists() const { return segments * lists_per_seg; }
 };
 
 SearchPlan plan_search(int64_t nq, int64_t n, int bq, int bn, int ctas_capacity, int64_t row_bytes,
@@ -34,6 +36,21 @@ int launch_score_topk_tc(const CUtensorMap& tmq, const CUtensorMap& tmc, const f
                          int64_t nq, int64_t n, int dim, int k, int64_t id_base, const SearchPlan& plan,
                          uint64_t* part, cudaStream_t st);
 // CTA-pair (cta_group::2) variant, 256 queries per pair tile (score_topk_sm100_pair.cu).
+// kPairGroup pairs form one cluster and share each corpus tile through TMA
+// multicast (they work on consecutive query tiles of the same segment).
+// (Measured: multicast does not pay on B200 — per-SM smem ingress, not L2
+// output, bounds the operand feed — so the default is 1, no multicast.)
+#ifndef RS_PAIR_GROUP
+#define RS_PAIR_GROUP 1
+#endif
+constexpr int kPairGroup = RS_PAIR_GROUP;
+// Epilogue warp groups per CTA: each owns a column slice of every tile and
+// keeps its own top-k per query, so a (query, segment) unit emits this many
+// sorted lists.
+#ifndef RS_PAIR_EPI_GROUPS
+#define RS_PAIR_EPI_GROUPS 1  // 2 measured no faster on B200 (and doubles the partial lists)
+#endif
+constexpr int kPairEpiGroups = RS_PAIR_EPI_GROUPS;
 int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap& tmc, const float* qn, const float* cn,
                            int64_t nq, int64_t n, int dim, int k, int64_t id_base, const SearchPlan& plan,
                            uint64_t* part, int32_t* counter, cudaStream_t st);

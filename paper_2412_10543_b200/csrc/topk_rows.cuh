@@ -331,8 +331,13 @@ template <int KREG, int ROWS, int BUF, int CHECK, bool FULL>
 __device__ __forceinline__ void epi_group8r(RegTopK<KREG, ROWS, BUF>& rt, const uint32_t* r, const float* cn,
                                             uint32_t id, int lim) {
   static_assert(BUF >= CHECK, "buffer must hold one group");
+#ifdef RS_EXP_NO_CN_LDS  // timing experiment only (wrong results): no corpus-norm smem reads
+  const float4 a = make_float4(1.0f, 1.0f, 1.0f, 1.0f), b = a;
+  (void)cn;
+#else
   const float4 a = *reinterpret_cast<const float4*>(cn);
   const float4 b = *reinterpret_cast<const float4*>(cn + 4);
+#endif
   const float2 q2 = make_float2(rt.qn, rt.qn);
   const float2 m2 = make_float2(-2.0f, -2.0f);
   const float2 e0 = __ffma2_rn(make_float2(__uint_as_float(r[0]), __uint_as_float(r[1])), m2,
@@ -344,6 +349,13 @@ __device__ __forceinline__ void epi_group8r(RegTopK<KREG, ROWS, BUF>& rt, const 
   const float2 e3 = __ffma2_rn(make_float2(__uint_as_float(r[6]), __uint_as_float(r[7])), m2,
                                __fadd2_rn(q2, make_float2(b.z, b.w)));
   const float e[8] = {e0.x, e0.y, e1.x, e1.y, e2.x, e2.y, e3.x, e3.y};
+#ifdef RS_EXP_NO_APPEND  // timing experiment only (wrong results): filter math, no candidates
+  float m = e[0];
+#pragma unroll
+  for (int j = 1; j < 8; ++j) m = fminf(m, e[j]);
+  if (m == -12345.0f) rt.append_raw(m, id);
+  return;
+#endif
 #pragma unroll
   for (int j = 0; j < 8; ++j)
     if ((FULL || j < lim) && e[j] <= rt.tau) rt.append_raw(e[j], id + j);

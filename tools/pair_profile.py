@@ -38,7 +38,7 @@ def main(n=2_000_000, nq=8192, d=1024):
              5: "epilogue finish (4 warps)", 6: "epilogue TMEM ld wait (4 warps)",
              2: "epilogue flush + mma wait full"}
     for label, rows in (("leader", a[0::2]), ("peer", a[1::2])):
-        total = rows[:, 7] / 3.0
+        total = rows[:, 7] / 3.0  # warps: producer, mma, 4 epilogue (/4)
         print(f"{label}: kernel {total.mean() / 1e6:.2f} Mcycles; flushes/warp {rows[:, 4].mean() / 4:.0f}")
         for i, nm in names.items():
             denom = total * (4 if i in (3, 5, 6) else 1)
