@@ -69,7 +69,7 @@ def sharded_retrieve_select(ops: ShardOps, queries, profiles, qlen, free_bytes, 
     rank = dist.get_rank(group)
     nq = queries.shape[0]
     keys = ops.search_keys(queries, k)                                  # [nq, k] local shard
-    gathered = torch.empty((world, nq, k), dtype=keys.dtype, device=keys.device)
+    gathered = torch.empty((world * nq, k), dtype=keys.dtype, device=keys.device)  # rank-major
     dist.all_gather_into_tensor(gathered, keys.contiguous(), group=group)
     spaces = ops.gate(profiles)                                         # full batch, in order
     q0, q1 = shard_range(nq, rank, world)
