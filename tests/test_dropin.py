@@ -1,0 +1,44 @@
+"""The drop-in rebinds exactly the reference's hot-path attributes (CPU check;
+needs the reference package, present only in the dev container)."""
+
+import os
+import sys
+
+import pytest
+
+REF = "/root/reference/pkg/src"
+
+
+@pytest.fixture()
+def ragsched():
+    if not os.path.isdir(REF):
+        pytest.skip("reference package not available here")
+    sys.path.insert(0, REF)
+    import ragsched as pkg
+
+    yield pkg
+    sys.path.remove(REF)
+
+
+def test_install_and_uninstall(ragsched):
+    import ragsched.mapping as mapping
+    import ragsched.memory as memory
+    import ragsched.profiler as profiler
+    import ragsched.scheduler as scheduler
+    import ragsched.sim as sim
+
+    from paper_2412_10543_b200 import dropin
+
+    before = (scheduler.best_fit_select, scheduler.fallback_config, profiler.gate_profile, mapping.map_profile,
+              memory.plan_bytes, sim.call_latency)
+    originals = dropin.install(ragsched)
+    after = (scheduler.best_fit_select, scheduler.fallback_config, profiler.gate_profile, mapping.map_profile,
+             memory.plan_bytes, sim.call_latency)
+    assert all(a is not b for a, b in zip(before, after))
+    # wrappers produce the reference's own classes
+    assert scheduler.best_fit_select.keywords["config_cls"] is ragsched.types.RagConfig
+    assert profiler.gate_profile.keywords["decision_cls"] is profiler.GateDecision
+    dropin.uninstall(originals)
+    restored = (scheduler.best_fit_select, scheduler.fallback_config, profiler.gate_profile, mapping.map_profile,
+                memory.plan_bytes, sim.call_latency)
+    assert all(a is b for a, b in zip(before, restored))
