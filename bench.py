@@ -237,10 +237,15 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--corpus-rows", type=int, default=None, help="override the corpus size (debug)")
+    ap.add_argument("--queries", type=int, default=None,
+                    help="override the queries per step (e.g. 128: the HBM-bound small-batch regime)")
     args = ap.parse_args()
     cfg = dict(WORKLOADS[args.workload])
     if args.corpus_rows:
         cfg["n"] = args.corpus_rows
+    if args.queries:
+        cfg["nq"] = args.queries
+        cfg["desc"] += f" [queries per step overridden: {args.queries}]"
     rank = int(os.environ.get("RANK", "0"))
     if args.impl == "reference":
         return run_reference(args, cfg, rank)
