@@ -172,6 +172,43 @@ int rs_plan_bytes(const uint8_t* method, const int32_t* num_chunks, const int32_
                   const int32_t* qlen, int64_t n, const rs_select_params* params /* host */,
                   int64_t* out, void* stream);
 
+/* ---- per-call expansion (memory.plan_calls, memory.py:89-150) --------------
+ * One LlmCall (memory.py:43-56), 24 bytes.  kind: 0 SINGLE (stuff),
+ * 1 MAPPER, 2 REDUCER, 3 RERANK (CallKind order of memory.py:29-33).  A
+ * map_reduce reducer depends on all mappers of its plan (the preceding
+ * num_chunks calls); no other call has dependencies. */
+typedef struct rs_call {
+  int64_t kv_bytes;           /* buffered_bytes(prompt + max_output, per_token) */
+  int32_t prompt_tokens;
+  int32_t max_output_tokens;
+  uint16_t index;             /* LlmCall.index */
+  uint8_t kind;
+  uint8_t reserved0;
+  uint32_t reserved1;
+} rs_call;
+
+enum rs_plan_status {
+  RS_PLAN_OK = 0,
+  RS_PLAN_NONE = 1,            /* config is MustQueue / overflow: no calls      */
+  RS_PLAN_INVALID_CHUNKS = 2,  /* InvalidChunkCount (memory.py:108-109)          */
+  RS_PLAN_CONTEXT_OVERFLOW = 3,/* ContextOverflow (memory.py:81-86)              */
+  RS_PLAN_BAD_INTERLEN = 4     /* map_reduce without positive intermediate_length */
+};
+
+/* rs_plan_calls: expand n chosen configs (rs_config from rs_select) into
+ * their calls.  Pass 1 (calls == NULL): writes offsets[0..n] (exclusive scan
+ * of the per-query call counts; offsets[n] = total calls) — size the calls
+ * buffer from it.  Pass 2: fills calls[offsets[i] .. offsets[i+1]) and, if
+ * non-NULL, total_bytes[i] (CallPlan.total_bytes) and status[i].  Queries
+ * whose plan raises in the reference get 0 calls and their RS_PLAN_* status.
+ * max_context_tokens is ModelSpec.max_context_tokens.  Workspace: device
+ * buffer of rs_plan_calls_workspace_size(n) bytes. */
+size_t rs_plan_calls_workspace_size(int64_t n);
+int rs_plan_calls(const rs_config* configs, const int32_t* qlen, int64_t n,
+                  const rs_select_params* params /* host */, int64_t max_context_tokens, int64_t* offsets,
+                  rs_call* calls, int64_t* total_bytes, uint8_t* status, void* workspace,
+                  size_t workspace_bytes, void* stream);
+
 /* ---- retrieval (FAISS IndexFlatL2 semantics) ----------------
  * An index owns one corpus shard in HBM: row-major [ntotal, dim] embeddings of
  * `dtype` plus fp32 squared norms.  Search returns, per query, the k smallest

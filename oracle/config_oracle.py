@@ -236,6 +236,46 @@ def plan_call_shapes(qlen, cfg, p: SelectParams):
     return [(q + c + t, il, True)] * n + [(q + n * il + t, o, False)]
 
 
+PLAN_OK, PLAN_NONE, PLAN_INVALID_CHUNKS, PLAN_CONTEXT_OVERFLOW, PLAN_BAD_INTERLEN = range(5)
+KIND_SINGLE, KIND_MAPPER, KIND_REDUCER, KIND_RERANK = range(4)  # CallKind order (memory.py:29-33)
+
+
+def plan_calls(qlen, cfg, p: SelectParams, max_context_tokens: int):
+    """memory.py:89-150 — (status, calls, total_bytes); calls are
+    (kind, prompt_tokens, max_output_tokens, kv_bytes, index).  The reference's
+    exceptions map to statuses, checked in its order: InvalidChunkCount
+    (:108-109), non-positive interlen (:531-532), then each call's context
+    window (:81-86)."""
+    m, n, il = cfg
+    if not 1 <= n <= p.max_chunks:
+        return PLAN_INVALID_CHUNKS, [], 0
+    q, c, t, o, pt = qlen, p.chunk_size, p.template_tokens, p.out_budget, p.per_token_bytes
+    if m == STUFF:
+        prompt = q + n * c + t
+        if prompt + o > max_context_tokens:
+            return PLAN_CONTEXT_OVERFLOW, [], 0
+        calls = [(KIND_SINGLE, prompt, o, buffered_bytes(prompt + o, pt), 0)]
+    elif m == RERANK:
+        prompt = q + c + t
+        if prompt + o > max_context_tokens:
+            return PLAN_CONTEXT_OVERFLOW, [], 0
+        kv = buffered_bytes(prompt + o, pt)
+        calls = [(KIND_RERANK, prompt, o, kv, i) for i in range(n)]
+    else:
+        if il <= 0:
+            return PLAN_BAD_INTERLEN, [], 0
+        mp = q + c + t
+        if mp + il > max_context_tokens:
+            return PLAN_CONTEXT_OVERFLOW, [], 0
+        mkv = buffered_bytes(mp + il, pt)
+        calls = [(KIND_MAPPER, mp, il, mkv, i) for i in range(n)]
+        rp = q + n * il + t
+        if rp + o > max_context_tokens:
+            return PLAN_CONTEXT_OVERFLOW, [], 0
+        calls.append((KIND_REDUCER, rp, o, buffered_bytes(rp + o, pt), 0))
+    return PLAN_OK, calls, sum(x[3] for x in calls)
+
+
 def plan_delay(qlen, cfg, p: SelectParams, cost: CostModel, running_before: int) -> float:
     """Critical-path delay of one admitted plan under the sim's dispatch rule
     (sim.py:223-229): the j-th independent call starts with

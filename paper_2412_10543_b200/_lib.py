@@ -38,6 +38,11 @@ CONFIG_DTYPE = np.dtype([("kv_bytes", "<i8"), ("method", "u1"), ("status", "u1")
                          ("num_chunks", "<u2"), ("interlen", "<u2"), ("reserved", "<u2")])
 WINDOW_DTYPE = np.dtype([("spaces", SPACE_DTYPE, (WINDOW_CAPACITY,)), ("len", "<i4"),
                          ("reserved", "<i4", (3,))])
+CALL_DTYPE = np.dtype([("kv_bytes", "<i8"), ("prompt_tokens", "<i4"), ("max_output_tokens", "<i4"),
+                       ("index", "<u2"), ("kind", "u1"), ("reserved0", "u1"), ("reserved1", "<u4")])
+CALL_KINDS = ("single", "mapper", "reducer", "rerank")  # rs_call.kind -> CallKind value (memory.py:29-33)
+RS_PLAN_OK, RS_PLAN_NONE, RS_PLAN_INVALID_CHUNKS, RS_PLAN_CONTEXT_OVERFLOW, RS_PLAN_BAD_INTERLEN = range(5)
+assert CALL_DTYPE.itemsize == 24
 assert PROFILE_DTYPE.itemsize == 16 and SPACE_DTYPE.itemsize == 16
 assert CONFIG_DTYPE.itemsize == 16 and WINDOW_DTYPE.itemsize == 176
 
@@ -99,6 +104,9 @@ SIGNATURES = {
                                           ctypes.POINTER(_I32), ctypes.POINTER(_I32)]),
     "rs_merge_topk": (ctypes.c_int, [_P, _I64, _I32, _I32, _I64, _I32, _P, _P, _P, _P]),
     "rs_row_norms": (ctypes.c_int, [_P, _I64, _I32, _I32, _P, _P]),
+    "rs_plan_calls_workspace_size": (ctypes.c_size_t, [_I64]),
+    "rs_plan_calls": (ctypes.c_int, [_P, _P, _I64, ctypes.POINTER(SelectParamsC), _I64, _P, _P, _P, _P, _P,
+                                     ctypes.c_size_t, _P]),
     "rs_launch_count": (ctypes.c_uint64, []),
     "rs_index_enable_timing": (ctypes.c_int, [_P, _I32]),
     "rs_index_kernel_times": (ctypes.c_int, [_P, _P, _I32, ctypes.POINTER(_I32)]),

@@ -248,6 +248,33 @@ def select(spaces: torch.Tensor, profiles: torch.Tensor | None, qlen: torch.Tens
     return out, (delay if cost is not None else None)
 
 
+def plan_calls(configs: torch.Tensor, qlen: torch.Tensor, params: SelectParams, max_context_tokens: int,
+               stream=None):
+    """memory.plan_calls (memory.py:89-150) for a device batch of chosen
+    rs_config records.  Returns (offsets int64 [n+1], calls uint8 [total,24]
+    of rs_call, total_bytes int64 [n], status uint8 [n]) on the device;
+    query i's calls are calls[offsets[i]:offsets[i+1]]."""
+    n = configs.shape[0]
+    lib = _lib.lib_for_device(_dev_index(configs))
+    dev = configs.device
+    offsets = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    totals = torch.empty(n, dtype=torch.int64, device=dev)
+    status = torch.empty(n, dtype=torch.uint8, device=dev)
+    ws_bytes = int(lib.rs_plan_calls_workspace_size(n))
+    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
+    pc = params.c()
+    s = _lib.stream_ptr(stream)
+    _lib.check(lib.rs_plan_calls(_lib.ptr(configs), _lib.ptr(qlen), n, ctypes.byref(pc), int(max_context_tokens),
+                                 _lib.ptr(offsets), 0, 0, _lib.ptr(status), _lib.ptr(ws), ws.numel(), s),
+               "rs_plan_calls(count)")
+    total_calls = int(offsets[n].item())  # one host read to size the CSR
+    calls = torch.empty((max(total_calls, 1), 24), dtype=torch.uint8, device=dev)
+    _lib.check(lib.rs_plan_calls(_lib.ptr(configs), _lib.ptr(qlen), n, ctypes.byref(pc), int(max_context_tokens),
+                                 _lib.ptr(offsets), _lib.ptr(calls), _lib.ptr(totals), 0, _lib.ptr(ws), ws.numel(),
+                                 s), "rs_plan_calls(fill)")
+    return offsets, calls[:total_calls], totals, status
+
+
 def call_latency_batch(prompt_tokens: torch.Tensor, max_output_tokens: torch.Tensor, concurrent: torch.Tensor,
                        cost: CostModel, stream=None) -> torch.Tensor:
     n = prompt_tokens.shape[0]

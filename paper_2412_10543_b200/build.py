@@ -20,7 +20,7 @@ CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 OBJ = os.path.join(HERE, "_obj")
 LIB = os.path.join(HERE, "libragsched_b200.so")
-SOURCES = ["abi.cu", "select.cu", "gate.cu", "retrieval.cu", "score_topk_sm100.cu", "score_topk_sm100_pair.cu"]
+SOURCES = ["abi.cu", "select.cu", "gate.cu", "plan.cu", "retrieval.cu", "score_topk_sm100.cu", "score_topk_sm100_pair.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

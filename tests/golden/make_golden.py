@@ -370,6 +370,48 @@ def gen_latency():
     print("latency:", len(rows), "calls,", len(plan_rows), "plans")
 
 
+# -- G6: per-call expansion (memory.plan_calls) --------------------------------
+
+def gen_plan_calls():
+    from ragsched.memory import CallKind
+    from ragsched.types import ContextOverflow, InvalidChunkCount
+
+    kinds = {CallKind.SINGLE: 0, CallKind.MAPPER: 1, CallKind.REDUCER: 2, CallKind.RERANK: 3}
+    rng = random.Random(31)
+    rows, calls = [], []
+    for trial in range(3000):
+        ps_i = rng.randrange(len(PARAM_SETS))
+        model0, meta, out, tmpl, mc, _ = params_kw(PARAM_SETS[ps_i])
+        max_ctx = rng.choice([131072, 32768, 16000, 8192])
+        model = ModelSpec(model0.num_layers, model0.num_kv_heads, model0.head_dim, model0.bytes_per_element,
+                          max_context_tokens=max_ctx)
+        m = rng.choice((1, 2, 4))
+        n = rng.choice([rng.randint(1, mc), rng.randint(1, mc), rng.randint(1, mc), 0, mc + 1])
+        il = rng.choice([rng.randint(1, 400), rng.randint(1, 400), 0]) if m == 4 else 0
+        q = QueryRecord(id="p", text="t", query_token_len=rng.randint(1, 12000))
+        cfg = RagConfig(FROM_BIT[m], n, il if m == 4 else None)
+        status, total = 0, 0
+        try:
+            plan = plan_calls(q, cfg, meta, model, out, template_tokens=tmpl, max_chunks=mc)
+            first = len(calls)
+            for c in plan.calls:
+                assert (not c.depends_on) or c.depends_on == frozenset(range(n))
+                calls.append((trial, kinds[c.kind], c.prompt_tokens, c.max_output_tokens, c.kv_bytes, c.index))
+            total = plan.total_bytes
+            assert len(calls) - first == len(plan.calls)
+        except InvalidChunkCount:
+            status = 2
+        except ContextOverflow:
+            status = 3
+        except ValueError:
+            status = 4
+        rows.append((trial, ps_i, max_ctx, m, n, il, q.query_token_len, status, total))
+    np.savez_compressed(os.path.join(OUT_DIR, "plan_calls.npz"), rows=np.array(rows, dtype=np.int64),
+                        calls=np.array(calls, dtype=np.int64))
+    print("plan_calls:", len(rows), "plans,", len(calls), "calls, statuses",
+          np.bincount(np.array(rows)[:, 7], minlength=5).tolist())
+
+
 # -- G5: known answers from the reference's own tests --------------------------
 
 def gen_known():
@@ -397,4 +439,5 @@ if __name__ == "__main__":
     gen_select()
     gen_gate()
     gen_latency()
+    gen_plan_calls()
     gen_known()

@@ -57,3 +57,10 @@ def latency():
 def known():
     z = _load("known.npz")
     return {k: z[k].item() for k in z.files}
+
+
+def plan_calls():
+    """rows int64 [n, 9]: trial, ps, max_ctx, m, n, il, qlen, status, total;
+    calls int64 [c, 6]: trial, kind, prompt, out, kv_bytes, index."""
+    z = _load("plan_calls.npz")
+    return z["rows"], z["calls"]

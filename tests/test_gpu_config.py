@@ -208,3 +208,39 @@ def test_gate_rejects_bad_threshold():
         batch.prune_gate(prof, batch.GateWindow(dev()), threshold=0.0)
     with pytest.raises(ValueError):
         batch.prune_gate(prof, batch.GateWindow(dev()), threshold=1.5)
+
+
+def test_plan_calls_golden_bit_exact():
+    """§8(f2): per-call expansion of chosen configs vs the reference's plan_calls."""
+    psets = gd.param_sets()
+    rows, calls = gd.plan_calls()
+    want_calls = {}
+    for c in calls:
+        want_calls.setdefault(int(c[0]), []).append(tuple(int(x) for x in c[1:]))
+    for ps in range(len(psets)):
+        for max_ctx in np.unique(rows[:, 2]):
+            sel = (rows[:, 1] == ps) & (rows[:, 2] == max_ctx)
+            if not sel.any():
+                continue
+            sub = rows[sel]
+            cfg = np.zeros(len(sub), dtype=_lib.CONFIG_DTYPE)
+            cfg["method"], cfg["num_chunks"], cfg["interlen"] = sub[:, 3], sub[:, 4], sub[:, 5]
+            cfg["status"] = 0
+            p = psets[ps]
+            params = batch.SelectParams(p["per_token_bytes"], p["chunk_size"], p["out_budget"], p["template_tokens"],
+                                        p["max_chunks"])
+            off, cl, tot, st = batch.plan_calls(batch.to_device(cfg, dev()),
+                                                torch.as_tensor(sub[:, 6].astype(np.int32), device=dev()), params,
+                                                int(max_ctx))
+            off = off.cpu().numpy()
+            cl = batch.from_device(cl, _lib.CALL_DTYPE) if off[-1] else np.zeros(0, dtype=_lib.CALL_DTYPE)
+            st, tot = st.cpu().numpy(), tot.cpu().numpy()
+            for j, r in enumerate(sub):
+                trial, status, total = int(r[0]), int(r[7]), int(r[8])
+                assert int(st[j]) == status, (trial, int(st[j]), status)
+                seg = cl[off[j]:off[j + 1]]
+                got = [(int(c["kind"]), int(c["prompt_tokens"]), int(c["max_output_tokens"]), int(c["kv_bytes"]),
+                        int(c["index"])) for c in seg]
+                assert got == want_calls.get(trial, []), trial
+                if status == 0:
+                    assert int(tot[j]) == total

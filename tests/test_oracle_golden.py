@@ -109,3 +109,16 @@ def test_c_oracle_gate_matches_reference(seq):
     out, fb, _ = c_oracle.gate_batch(seq["profiles"], seq["conf"], seq["threshold"],
                                      seq["default_space"], seq["max_chunks"], seq["prefill"])
     np.testing.assert_array_equal(np.concatenate([out, fb[:, None]], axis=1), seq["expected"])
+
+
+def test_plan_calls_matches_reference():
+    psets = [co.SelectParams(**p) for p in gd.param_sets()]
+    rows, calls = gd.plan_calls()
+    by_trial = {}
+    for c in calls:
+        by_trial.setdefault(int(c[0]), []).append(tuple(int(x) for x in c[1:]))
+    for trial, ps, max_ctx, m, n, il, qlen, status, total in (tuple(int(x) for x in r) for r in rows):
+        st, got, tot = co.plan_calls(qlen, (m, n, il), psets[ps], max_ctx)
+        assert st == status, (trial, st, status)
+        assert got == by_trial.get(trial, [])
+        assert tot == total
