@@ -346,10 +346,12 @@ def main():
     l0 = _lib.launch_count()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include timed/ lists exactly these launches
     ev0.record()
     for _ in range(args.steps):
         step()
     ev1.record()
+    torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize()
     barrier()
     launches = _lib.launch_count() - l0
@@ -410,7 +412,8 @@ def main():
         roof = {"bound": "hbm", "achieved": bytes_alg / (kernel_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s"}
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["traffic"] = None
-    roof["kernel"] = "score_topk_tc_kernel" if cfg["dtype"] == "bf16" else "score_topk_simt_kernel"
+    roof["kernel"] = {"tcgen05": "score_topk_pair_kernel", "tcgen05_1sm": "score_topk_tc_kernel"}.get(
+        index.last_plan()["algo"], "score_topk_simt_kernel")
     roof["kernel_ms"] = kernel_ms
     roof["kernel_share_of_step"] = kernel_ms / (ms_max / args.steps)
     roof["peak_source"] = f"{peak_src}, {'sustained' if roof['bound'] == 'tensor' else 'copy'}"

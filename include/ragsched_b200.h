@@ -231,6 +231,10 @@ int rs_index_ntotal(const rs_index* index, int64_t* out);
 /* Device pointers of the stored corpus / norms (read-only views). */
 int rs_index_data(const rs_index* index, const void** embeddings, const float** norms);
 int rs_index_set_algo(rs_index* index, int32_t algo);
+/* Test hook (0 in production): every CTA-pair kernel unit of query tile qt
+ * starts its corpus-segment walk bias*(qt+1) tiles past the segment frontier,
+ * so the out-of-id-order (wrap-around) top-k path runs deterministically. */
+int rs_index_set_walk_bias(rs_index* index, int32_t bias);
 /* Preallocate the search workspace for up to nq_max queries of k results. */
 int rs_index_reserve(rs_index* index, int64_t nq_max, int32_t k);
 /* Search: queries device [nq, dim] of the index dtype; D device [nq,k] fp32,

@@ -343,7 +343,7 @@ SearchPlan plan_search(int64_t nq, int64_t n, int bq, int bn, int ctas_capacity,
   double best_cost = 1e300;
   for (int64_t tps = nt; tps >= 1;) {
     const int64_t segs = ceil_div(nt, tps);
-    if (segs > 4096) break;
+    if (segs > kMaxSegments) break;
     if (tps <= max_tps && (segs * list_bytes_per_seg <= (int64_t(4) << 30) || best_cost == 1e300)) {
       const int64_t units = qt * segs;
       const int64_t rounds = ceil_div(units, ctas_capacity);
@@ -370,11 +370,12 @@ SearchPlan plan_search(int64_t nq, int64_t n, int bq, int bn, int ctas_capacity,
 // ============================ rs_index =========================================
 struct rs_index {
   int32_t dim = 0, dtype = 0, device = 0, algo = RS_ALGO_AUTO;
+  int32_t walk_bias = 0;  // test hook (rs_index_set_walk_bias)
   int64_t capacity = 0, ntotal = 0;
   void* data = nullptr;
   float* norms = nullptr;
   float* norm_max = nullptr;  // device scalar: max squared norm over the shard
-  int32_t* sched_counter = nullptr;  // device scalar: dynamic unit scheduler of the pair kernel
+  int32_t* sched_counter = nullptr;  // pair kernel: [0] unit counter, [1 + s] frontier tile of segment s
   float* qnorm = nullptr;
   int64_t qnorm_cap = 0;
   uint64_t* part = nullptr;
@@ -471,7 +472,7 @@ int run_partial(rs_index* ix, const void* queries, int64_t nq, int k, int64_t id
     rc = encode_kmajor_bf16_map(&tmc, ix->data, ix->ntotal, ix->dim, pair ? kTcBN / 2 / kPairGroup : kTcBN);
     if (rc) return rc;
     rc = pair ? launch_score_topk_pair(tmq, tmc, ix->qnorm, ix->norms, nq, ix->ntotal, ix->dim, k, id_base, plan,
-                                       ix->part, ix->sched_counter, st)
+                                       ix->part, ix->sched_counter, ix->walk_bias, st)
               : launch_score_topk_tc(tmq, tmc, ix->qnorm, ix->norms, nq, ix->ntotal, ix->dim, k, id_base, plan,
                                      ix->part, st);
   } else {
@@ -523,7 +524,7 @@ extern "C" int rs_index_create(int32_t dim, int32_t dtype, int64_t capacity, int
     // granules of norms past the last row of a partial tile
     if (e == cudaSuccess) e = cudaMalloc(&ix->norms, sizeof(float) * (capacity + rs::kTcBN));
     if (e == cudaSuccess) e = cudaMalloc(&ix->norm_max, sizeof(float));
-    if (e == cudaSuccess) e = cudaMalloc(&ix->sched_counter, sizeof(int32_t));
+    if (e == cudaSuccess) e = cudaMalloc(&ix->sched_counter, sizeof(int32_t) * (1 + rs::kMaxSegments));
     if (e == cudaSuccess) e = cudaMemset(ix->norm_max, 0, sizeof(float));
     if (e != cudaSuccess) {
       rs::set_error("cudaMalloc(corpus %lld x %d): %s", (long long)capacity, dim, cudaGetErrorString(e));
@@ -616,6 +617,13 @@ extern "C" int rs_index_data(const rs_index* ix, const void** emb, const float**
   RS_REQUIRE(ix != nullptr, "index is NULL");
   if (emb) *emb = ix->data;
   if (norms) *norms = ix->norms;
+  return RS_OK;
+}
+
+extern "C" int rs_index_set_walk_bias(rs_index* ix, int32_t bias) {
+  RS_REQUIRE(ix != nullptr, "index is NULL");
+  RS_REQUIRE(bias >= 0 && bias < (1 << 16), "walk bias out of range (%d)", bias);
+  ix->walk_bias = bias;
   return RS_OK;
 }
 

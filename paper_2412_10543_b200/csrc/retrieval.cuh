@@ -24,6 +24,9 @@ struct SearchPlan {
   int32_t lists() const { return segments * lists_per_seg; }
 };
 
+// upper bound of SearchPlan::segments (plan_search never exceeds it)
+constexpr int kMaxSegments = 4096;
+
 SearchPlan plan_search(int64_t nq, int64_t n, int bq, int bn, int ctas_capacity, int64_t row_bytes,
                        bool share_l2);
 
@@ -53,7 +56,7 @@ constexpr int kPairGroup = RS_PAIR_GROUP;
 constexpr int kPairEpiGroups = RS_PAIR_EPI_GROUPS;
 int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap& tmc, const float* qn, const float* cn,
                            int64_t nq, int64_t n, int dim, int k, int64_t id_base, const SearchPlan& plan,
-                           uint64_t* part, int32_t* counter, cudaStream_t st);
+                           uint64_t* part, int32_t* counter, int32_t walk_bias, cudaStream_t st);
 int encode_kmajor_bf16_map(CUtensorMap* map, const void* base, int64_t rows, int dim, int box_rows);
 
 // CUDA-core kernel for fp32 (and bf16 cross-checks), retrieval.cu.

@@ -110,6 +110,7 @@ struct __align__(8) SmemTail {
   uint64_t ufull[URING];
   uint64_t uempty[URING];
   int32_t uid[URING];
+  int32_t ustart[URING];  // absolute frontier tile the unit starts at
   uint32_t tmem_base;
 };
 
@@ -132,6 +133,8 @@ struct Params {
   int64_t seg_rows;
   uint64_t* part;
   int32_t* counter;  // dynamic unit counter (zeroed before the launch)
+  int32_t* seg_pos;  // per segment: absolute tile index the most advanced pair last started (zeroed)
+  int32_t walk_bias; // test hook: unit of query tile qt starts walk_bias*(qt+1) tiles past the frontier
   int64_t cunits;    // cluster units = (qtiles / G) * segments
 };
 
@@ -144,6 +147,28 @@ __device__ __forceinline__ void unit_coords(int64_t u, const Params& p, int& qt,
   if (r1 > p.n) r1 = p.n;
 }
 
+// Frontier join: a unit streams its segment's T tiles starting at the tile
+// the most advanced pair on that segment is loading (absolute index `start`)
+// and wraps around, so every pair on a segment reads the same corpus rows at
+// about the same time whenever it joined — the segment's rows are fetched
+// from HBM about once and served to the other query tiles from L2.  (In
+// plain ascending order the dynamically scheduled pairs drift apart by
+// fractions of a unit; ncu measured the 20 GB corpus read 8x from DRAM at
+// 10M x 1024, and the DRAM power cost ~10% of the SM clock under the cap.)
+struct TileWalk {
+  int64_t r0, r1, ntiles, first;  // first = start mod ntiles
+  __device__ __forceinline__ TileWalk(int64_t r0_, int64_t r1_, int32_t start) : r0(r0_), r1(r1_) {
+    ntiles = (r1 - r0 + BN - 1) / BN;
+    first = ntiles > 0 ? int64_t(start) % ntiles : 0;
+  }
+  __device__ __forceinline__ bool wrapped(int64_t j) const { return first + j >= ntiles; }
+  __device__ __forceinline__ int64_t c0(int64_t j) const {
+    int64_t t = first + j;
+    if (t >= ntiles) t -= ntiles;
+    return r0 + t * BN;
+  }
+};
+
 // Consumer side of the unit ring: wait for slot i, read the unit id, release
 // the slot to the leader's producer.  Returns the unit (-1 = no more work).
 __device__ __forceinline__ void release_unit(SmemTail* tail, uint32_t i, bool scheduler) {
@@ -152,10 +177,11 @@ __device__ __forceinline__ void release_unit(SmemTail* tail, uint32_t i, bool sc
   else
     mbar_arrive_cluster(mapa_shared(smem_u32(&tail->uempty[i % URING]), 0));
 }
-__device__ __forceinline__ int next_unit(SmemTail* tail, uint32_t i, bool scheduler, bool arrive) {
+__device__ __forceinline__ int next_unit(SmemTail* tail, uint32_t i, bool scheduler, bool arrive, int32_t& start) {
   const int slot = int(i % URING);
   mbar_wait_cluster(&tail->ufull[slot], (i / URING) & 1);
   const int u = *reinterpret_cast<volatile int32_t*>(&tail->uid[slot]);
+  start = *reinterpret_cast<volatile int32_t*>(&tail->ustart[slot]);
   if (arrive) release_unit(tail, i, scheduler);
   return u;
 }
@@ -239,24 +265,43 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       uint32_t phase = 0;
       for (uint32_t i = 0;; ++i) {
         int u;
+        int32_t start = 0;
         if (scheduler) {
           const int slot = int(i % URING);
           mbar_wait(&tail->uempty[slot], ((i / URING) & 1) ^ 1);
           u = atomicAdd(p.counter, 1);
           if (u >= p.cunits) u = -1;
+          if (u >= 0) {
+            const int64_t uu = int64_t(u) * G;
+            start = ld_relaxed_gpu_s32(p.seg_pos + uu / p.qtiles) + p.walk_bias * int32_t(uu % p.qtiles + 1);
+#ifdef RS_EXP_NO_FRONTIER  // timing experiment: ascending walk from tile 0
+            start = 0;
+#endif
+#ifdef RS_EXP_STAGGER  // timing experiment: join RS_EXP_STAGGER*(qt%8) tiles behind the frontier
+            start -= RS_EXP_STAGGER * int32_t(uu % 8);
+            if (start < 0) start = 0;
+#endif
+          }
           tail->uid[slot] = u;
-          for (uint32_t c = 1; c < CL; ++c) st_shared_cluster_u32(mapa_shared(smem_u32(&tail->uid[slot]), c), uint32_t(u));
+          tail->ustart[slot] = start;
+          for (uint32_t c = 1; c < CL; ++c) {
+            st_shared_cluster_u32(mapa_shared(smem_u32(&tail->uid[slot]), c), uint32_t(u));
+            st_shared_cluster_u32(mapa_shared(smem_u32(&tail->ustart[slot]), c), uint32_t(start));
+          }
           mbar_arrive(&tail->ufull[slot]);
           for (uint32_t c = 1; c < CL; ++c)  // release: orders the remote stores above
             mbar_arrive_cluster(mapa_shared(smem_u32(&tail->ufull[slot]), c));
         } else {
-          u = next_unit(tail, i, false, true);
+          u = next_unit(tail, i, false, true, start);
         }
         if (u < 0) break;
         int qt, seg;
         int64_t r0, r1;
         unit_coords(int64_t(u) * G + pp, p, qt, seg, r0, r1);
-        for (int64_t c0 = r0; c0 < r1; c0 += BN) {
+        const TileWalk walk(r0, r1, start);
+        for (int64_t j = 0; j < walk.ntiles; ++j) {
+          const int64_t c0 = walk.c0(j);
+          if (scheduler) red_max_relaxed_gpu_s32(p.seg_pos + seg, start + int32_t(j));
           for (int kb = 0; kb < p.kblocks; ++kb) {
             PROF(0, mbar_wait(&tail->empty[stage], phase ^ 1));
             uint8_t* sa = smem + size_t(stage) * STAGE_BYTES;
@@ -269,7 +314,12 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             if (leader) mbar_arrive_expect_tx(&tail->full[stage], 2 * STAGE_BYTES);
             tma_load_2d_pair(&tmq, full_leader, sa, kb * BK, qt * PM + int(half) * BM, pol_q);
             if (G == 1) {
+#ifdef RS_EXP_L2_CORPUS_ROWS  // timing experiment only (wrong results): corpus reads wrap in an L2-sized window
+              tma_load_2d_pair(&tmc, full_leader, sa + A_BYTES, kb * BK,
+                               int32_t(c0 % RS_EXP_L2_CORPUS_ROWS) + int(half) * HB, pol_c);
+#else
               tma_load_2d_pair(&tmc, full_leader, sa + A_BYTES, kb * BK, int32_t(c0) + int(half) * HB, pol_c);
+#endif
             } else {
               // piece pp of this half's corpus rows, written into the same smem
               // offset of every CTA holding this half in the cluster's G pairs
@@ -292,12 +342,15 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       uint32_t phase = 0;
       uint32_t tile_iter = 0;
       for (uint32_t i = 0;; ++i) {
-        const int u = next_unit(tail, i, scheduler, true);
+        int32_t start;
+        const int u = next_unit(tail, i, scheduler, true, start);
         if (u < 0) break;
         int qt, seg;
         int64_t r0, r1;
         unit_coords(int64_t(u) * G + pp, p, qt, seg, r0, r1);
-        for (int64_t c0 = r0; c0 < r1; c0 += BN, ++tile_iter) {
+        const TileWalk walk(r0, r1, start);
+        for (int64_t j = 0; j < walk.ntiles; ++j, ++tile_iter) {
+          const int64_t c0 = walk.c0(j);
           const uint32_t acc = tile_iter & 1;
           // leader: both epilogues released TMEM buffer acc; peer: own epilogue released cns[acc]
           PROF(1, mbar_wait(&tail->tempty[acc], ((tile_iter >> 1) & 1) ^ 1));
@@ -345,7 +398,8 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     const uint32_t tempty_leader1 = mapa_shared(smem_u32(&tail->tempty[1]), pair_leader);
     uint32_t tile_iter = 0;
     for (uint32_t i = 0;; ++i) {
-      const int u = next_unit(tail, i, scheduler, false);
+      int32_t start;
+      const int u = next_unit(tail, i, scheduler, false, start);
       __syncwarp();
       if (lane == 0) release_unit(tail, i, scheduler);  // one release per warp, after every lane read the slot
       if (u < 0) break;
@@ -355,7 +409,15 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       const int64_t qrow = int64_t(qt) * PM + int64_t(half) * BM + row;
       rt.qn = qrow < p.nq ? p.qn[qrow] : 0.0f;
       rt.reset();
-      for (int64_t c0 = r0; c0 < r1; c0 += BN, ++tile_iter) {
+      const TileWalk walk(r0, r1, start);
+      for (int64_t j = 0; j < walk.ntiles; ++j, ++tile_iter) {
+        const int64_t c0 = walk.c0(j);
+        // ids below every one seen so far from here on: flush the earlier
+        // phase's candidates, then tag the rest phase 0 (RegTopK ordering)
+        if (rt.phase && walk.wrapped(j)) {
+          rt.flush();
+          rt.phase = 0;
+        }
         const uint32_t acc = tile_iter & 1;
         const int valid = int(r1 - c0 < BN ? r1 - c0 : BN);
         const float* cn_t = cns + acc * BN;
@@ -431,7 +493,7 @@ extern "C" int rs_debug_pair_profile_reset() {
 
 int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap& tmc, const float* qn, const float* cn,
                            int64_t nq, int64_t n, int dim, int k, int64_t id_base, const SearchPlan& plan,
-                           uint64_t* part, int32_t* counter, cudaStream_t st) {
+                           uint64_t* part, int32_t* counter, int32_t walk_bias, cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
     RS_CHECK_CUDA(cudaFuncSetAttribute(score_topk_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -439,7 +501,9 @@ int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap& tmc, const
                   "cudaFuncSetAttribute(score_topk_pair_kernel)");
     attr_set = true;
   }
-  RS_CHECK_CUDA(cudaMemsetAsync(counter, 0, sizeof(int32_t), st), "cudaMemsetAsync(unit counter)");
+  RS_REQUIRE(plan.segments >= 1 && plan.segments <= kMaxSegments, "segments out of range (%d)", plan.segments);
+  RS_CHECK_CUDA(cudaMemsetAsync(counter, 0, sizeof(int32_t) * (1 + plan.segments), st),
+                "cudaMemsetAsync(unit counter, segment frontiers)");
   Params p{};
   p.qn = qn;
   p.cn = cn;
@@ -455,6 +519,8 @@ int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap& tmc, const
   p.seg_rows = plan.seg_rows;
   p.part = part;
   p.counter = counter;
+  p.seg_pos = counter + 1;
+  p.walk_bias = walk_bias;
   p.cunits = int64_t(plan.qtiles) * plan.segments;
   score_topk_pair_kernel<<<CL * plan.ctas, NUM_THREADS, SMEM_BYTES, st>>>(tmq, tmc, p);
   RS_CHECK_LAUNCH("score_topk_pair_kernel");

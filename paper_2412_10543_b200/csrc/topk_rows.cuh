@@ -251,26 +251,39 @@ __device__ __forceinline__ void epi_group8p(RowTopK<ROWS, BUF>& rt, const uint32
 // all KREG updates issue back to back).  Candidates still go through the smem
 // append buffer (cheap predicated stores) and are inserted in batches.
 //
-// Order: candidates of a row arrive with strictly increasing chunk ids, so a
-// new element goes after existing equal distances — a strict "<" realises
-// the (distance asc, id asc) tie rule without comparing ids.
+// Order: the list is sorted by a u32 key = (distance bits << 1) | phase
+// (distances are non-negative floats, so their bit patterns are ordered and
+// 31 bits wide), inserted with a strict "<".  Within one phase candidates
+// arrive with increasing chunk ids, so a strict "<" puts a new element after
+// equal distances of its own phase — the (distance asc, id asc) tie rule
+// without comparing ids.  A caller that streams a row range out of id order
+// (the pair kernel joins a corpus segment at its frontier tile and wraps
+// around) switches to phase 0 at the wrap: every later id is lower than every
+// id seen before it, and phase 0 sorts before phase 1 at equal distance, so
+// the rule stays exact at the same cost.
 template <int KREG, int ROWS, int BUF>
 struct RegTopK {
-  float d[KREG];
+  uint32_t key[KREG];  // (distance bits << 1) | phase
   uint32_t id[KREG];
   int k;          // <= KREG
-  float tau;      // d[k-1] (current k-th best), +inf until k candidates seen
+  float tau;      // distance of the current k-th best, +inf until k candidates seen
+  uint32_t ktau;  // key of the current k-th best
+  uint32_t phase; // 1 until the walk wraps to lower ids, then 0
   float qn;       // this row's |q|^2
   uint32_t wbase; // shared-window byte address of this row's buffer slot 0
   uint32_t wp;    // next free buffer slot
 
+  static constexpr uint32_t kEmpty = 0xff000001u;  // +inf, phase 1
+
   __device__ __forceinline__ void reset() {
 #pragma unroll
     for (int j = 0; j < KREG; ++j) {
-      d[j] = __int_as_float(0x7f800000);
+      key[j] = kEmpty;
       id[j] = 0xffffffffu;
     }
     tau = __int_as_float(0x7f800000);
+    ktau = kEmpty;
+    phase = 1;
     wp = wbase;
   }
 
@@ -280,38 +293,39 @@ struct RegTopK {
   }
   __device__ __forceinline__ int buffered() const { return int((wp - wbase) / (ROWS * 8)); }
 
-  __device__ __forceinline__ void insert(float xd, uint32_t xid) {
+  __device__ __forceinline__ void insert(uint32_t xk, uint32_t xid) {
 #pragma unroll
     for (int j = KREG - 1; j >= 1; --j) {
-      const bool lt_prev = xd < d[j - 1];
-      const bool lt_cur = xd < d[j];
+      const bool lt_prev = xk < key[j - 1];
+      const bool lt_cur = xk < key[j];
       id[j] = lt_prev ? id[j - 1] : (lt_cur ? xid : id[j]);
-      d[j] = lt_prev ? d[j - 1] : (lt_cur ? xd : d[j]);
+      key[j] = lt_prev ? key[j - 1] : (lt_cur ? xk : key[j]);
     }
-    const bool lt0 = xd < d[0];
+    const bool lt0 = xk < key[0];
     id[0] = lt0 ? xid : id[0];
-    d[0] = lt0 ? xd : d[0];
+    key[0] = lt0 ? xk : key[0];
   }
 
   __device__ __forceinline__ void refresh_tau() {
-    float t = d[0];
+    uint32_t t = key[0];
 #pragma unroll
     for (int j = 1; j < KREG; ++j)
-      if (j == k - 1) t = d[j];
-    tau = t;
+      if (j == k - 1) t = key[j];
+    ktau = t;
+    tau = __uint_as_float(t >> 1);
   }
 
   // Warp-collective: every lane inserts its buffered candidates (lockstep over
-  // the warp's largest buffer; lanes past their own count insert +inf = no-op).
+  // the warp's largest buffer; lanes past their own count insert kEmpty = no-op).
   __device__ __forceinline__ void flush() {
     const int n = buffered();
     const int nmax = __reduce_max_sync(0xffffffffu, n);
     for (int j = 0; j < nmax; ++j) {
-      uint32_t lo = 0, hi = 0x7f800000u;
+      uint32_t lo = 0, hi = 0;
       if (j < n) asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(lo), "=r"(hi) : "r"(wbase + j * ROWS * 8));
-      float xd = __uint_as_float(hi);
-      xd = xd > 0.0f ? xd : (j < n ? 0.0f : xd);  // clamp negative round-off (and -0) to +0
-      if (__any_sync(0xffffffffu, xd < tau)) insert(xd < tau ? xd : __int_as_float(0x7f800000), lo);
+      // clamp negative round-off (and -0, NaN) to +0: bit pattern 0
+      const uint32_t xk = j < n ? ((__uint_as_float(hi) > 0.0f ? hi : 0u) << 1) | phase : kEmpty;
+      if (__any_sync(0xffffffffu, xk < ktau)) insert(xk < ktau ? xk : kEmpty, lo);
     }
     wp = wbase;
     refresh_tau();
@@ -322,7 +336,7 @@ struct RegTopK {
   __device__ __forceinline__ void finish(uint64_t* __restrict__ out) const {
 #pragma unroll
     for (int j = 0; j < KREG; ++j)
-      if (j < k) out[j] = isinf(d[j]) ? ~0ull : make_key(d[j], id[j]);
+      if (j < k) out[j] = (key[j] >> 1) >= 0x7f800000u ? ~0ull : (uint64_t(key[j] >> 1) << 32) | id[j];
   }
 };
 

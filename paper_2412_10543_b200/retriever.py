@@ -81,6 +81,11 @@ class IndexFlatL2:
     def set_algo(self, algo: str) -> None:
         _lib.check(self._lib.rs_index_set_algo(self._h, ALGOS[algo]))
 
+    def set_walk_bias(self, bias: int) -> None:
+        """Test hook: start every pair-kernel unit past its segment frontier
+        (exercises the wrap-around, out-of-id-order top-k path)."""
+        _lib.check(self._lib.rs_index_set_walk_bias(self._h, int(bias)))
+
     def search(self, x, k: int, *, keep: torch.Tensor | None = None, out=None, stream=None):
         """k nearest chunks per query: (D float32 [nq,k], I int64 [nq,k]).
 

@@ -186,3 +186,35 @@ def test_plan_shapes_multi_segment(nq):
     assert plan["segments"] > 1
     sub = slice(0, 64)
     assert_parity(q[sub], c, 35, D[sub], I[sub], torch.bfloat16)
+
+
+@pytest.mark.parametrize("bias", [1, 7])
+def test_wrapped_segment_walk_keeps_lower_id_ties(bias):
+    """The pair kernel joins a corpus segment at its frontier and wraps around,
+    so ids reach a row's top-k out of order; exact-duplicate rows must still
+    resolve to the lowest ids (the walk bias forces a wrap in every unit)."""
+    nq, n, d, k, base = 1024, 300_000, 256, 35, 150_001
+    q, c = make_data(nq, n, d, torch.bfloat16, seed=bias)
+    c[base::97] = c[base]
+    q[:8] = c[base]
+    q[8:16] = c[base] + 1e-3  # near-tie neighbours of the duplicate cluster
+    ix = IndexFlatL2(d, dtype=torch.bfloat16, capacity=n)
+    ix.set_algo("tcgen05")
+    ix.set_walk_bias(bias)
+    ix.add(c.cuda())
+    D, I = ix.search(q.cuda(), k)
+    torch.cuda.synchronize()
+    plan = ix.last_plan()
+    ix.close()
+    D, I = D.cpu().numpy(), I.cpu().numpy()
+    assert plan["segments"] > 1 and plan["qtiles"] > 1
+    want = base + 97 * np.arange(k)
+    for r in range(8):
+        np.testing.assert_array_equal(I[r], want)
+        assert np.all(D[r] == D[r, 0])
+    assert_parity(q[:64], c, k, D[:64], I[:64], torch.bfloat16)
+    assert_parity(q[-64:], c, k, D[-64:], I[-64:], torch.bfloat16)
+    # the same search with the production walk agrees bit for bit
+    D0, I0, _ = run_search(q, c, k, algo="tcgen05")
+    np.testing.assert_array_equal(I0, I)
+    np.testing.assert_array_equal(D0, D)
