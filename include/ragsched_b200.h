@@ -209,6 +209,58 @@ int rs_plan_calls(const rs_config* configs, const int32_t* qlen, int64_t n,
                   rs_call* calls, int64_t* total_bytes, uint8_t* status, void* workspace,
                   size_t workspace_bytes, void* stream);
 
+/* ---- FIFO admission chain (Scheduler.step, scheduler.py:397-410) ----------
+ * The new-query loop of Scheduler.step: for the waiting queue in FIFO order,
+ * _try_admit_new (scheduler.py:335-395) — best_fit_select against the free
+ * bytes left by the admissions before it, else fallback_config (if
+ * allow_fallback), else stop — and the accounting of _start_run (:281-333):
+ * every independent call of the chosen plan is admitted, a map_reduce
+ * reducer is deferred.  With allow_fallback == 0 the fixed-config baseline
+ * path (:380-395) runs instead: the space must hold exactly one candidate,
+ * whose independent calls are admitted in index order while each fits.
+ * The backlog pass that precedes the loop (_admit_backlog, :257-270) stays
+ * with the caller, which owns the per-call state. */
+typedef struct rs_admit_params {
+  int64_t capacity_bytes;     /* Scheduler.capacity_bytes                         */
+  int64_t used_bytes;         /* Scheduler.used_bytes when the loop starts         */
+  int64_t max_context_tokens; /* ModelSpec.max_context_tokens (plan_calls checks)  */
+} rs_admit_params;
+
+typedef struct rs_admit_info { /* per admitted queue entry, 16 bytes */
+  int64_t admitted_bytes;      /* KV bytes of the calls admitted now              */
+  int32_t admitted_calls;      /* independent calls admitted now (index prefix)   */
+  int32_t fixed_path;          /* 1: the baseline path admitted it call by call
+                                  (_start_run admit_all_independent = False)     */
+} rs_admit_info;
+
+enum rs_admit_stop {
+  RS_ADMIT_DRAINED = 0,          /* every entry admitted                               */
+  RS_ADMIT_BLOCKED = 1,          /* _try_admit_new -> None: the head waits              */
+  RS_ADMIT_NO_PROFILE = 2,       /* SchedulingImpossible: fallback needs a profile (:356-359) */
+  RS_ADMIT_IMPOSSIBLE = 3,       /* SchedulingImpossible: cannot fit an empty scheduler (:374-377, :388-391) */
+  RS_ADMIT_FIXED_SPACE = 4,      /* SchedulingImpossible: baseline space not one config (:383-386) */
+  RS_ADMIT_INVALID_CHUNKS = 5,   /* InvalidChunkCount from plan_calls (memory.py:108-109) */
+  RS_ADMIT_CONTEXT_OVERFLOW = 6, /* ContextOverflow from plan_calls (memory.py:81-86)   */
+  RS_ADMIT_BAD_INTERLEN = 7,     /* ValueError: map_reduce without intermediate_length  */
+  RS_ADMIT_OVERFLOW = 8          /* inputs exceed the int64 byte range (error)          */
+};
+
+typedef struct rs_admit_result { /* device, written once per call */
+  int64_t admitted;   /* entries admitted: configs/info[0 .. admitted) are valid       */
+  int64_t used_bytes; /* Scheduler.used_bytes after them                               */
+  int32_t stop;       /* rs_admit_stop; for != DRAINED it concerns entry `admitted`     */
+  int32_t reserved;
+} rs_admit_result;
+
+/* spaces/profiles/has_profile/qlen: device arrays of the n waiting entries in
+ * queue order (has_profile may be NULL = all present; profiles may be NULL
+ * when allow_fallback == 0).  configs/info: device, n entries.  result:
+ * device.  One launch, stream-ordered. */
+int rs_admit_fifo(const rs_space* spaces, const rs_profile* profiles, const uint8_t* has_profile,
+                  const int32_t* qlen, int64_t n, const rs_select_params* params /* host */,
+                  const rs_admit_params* admit /* host */, rs_config* configs, rs_admit_info* info,
+                  rs_admit_result* result, void* stream);
+
 /* ---- retrieval (FAISS IndexFlatL2 semantics) ----------------
  * An index owns one corpus shard in HBM: row-major [ntotal, dim] embeddings of
  * `dtype` plus fp32 squared norms.  Search returns, per query, the k smallest

@@ -43,6 +43,11 @@ CALL_DTYPE = np.dtype([("kv_bytes", "<i8"), ("prompt_tokens", "<i4"), ("max_outp
 CALL_KINDS = ("single", "mapper", "reducer", "rerank")  # rs_call.kind -> CallKind value (memory.py:29-33)
 RS_PLAN_OK, RS_PLAN_NONE, RS_PLAN_INVALID_CHUNKS, RS_PLAN_CONTEXT_OVERFLOW, RS_PLAN_BAD_INTERLEN = range(5)
 assert CALL_DTYPE.itemsize == 24
+ADMIT_INFO_DTYPE = np.dtype([("admitted_bytes", "<i8"), ("admitted_calls", "<i4"), ("fixed_path", "<i4")])
+ADMIT_RESULT_DTYPE = np.dtype([("admitted", "<i8"), ("used_bytes", "<i8"), ("stop", "<i4"), ("reserved", "<i4")])
+(RS_ADMIT_DRAINED, RS_ADMIT_BLOCKED, RS_ADMIT_NO_PROFILE, RS_ADMIT_IMPOSSIBLE, RS_ADMIT_FIXED_SPACE,
+ RS_ADMIT_INVALID_CHUNKS, RS_ADMIT_CONTEXT_OVERFLOW, RS_ADMIT_BAD_INTERLEN, RS_ADMIT_OVERFLOW) = range(9)
+assert ADMIT_INFO_DTYPE.itemsize == 16 and ADMIT_RESULT_DTYPE.itemsize == 24
 assert PROFILE_DTYPE.itemsize == 16 and SPACE_DTYPE.itemsize == 16
 assert CONFIG_DTYPE.itemsize == 16 and WINDOW_DTYPE.itemsize == 176
 
@@ -71,6 +76,11 @@ class CostModelC(ctypes.Structure):
 class GateParamsC(ctypes.Structure):
     _fields_ = [("threshold", ctypes.c_double), ("default_space", SpaceC),
                 ("max_chunks", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
+class AdmitParamsC(ctypes.Structure):
+    _fields_ = [("capacity_bytes", ctypes.c_int64), ("used_bytes", ctypes.c_int64),
+                ("max_context_tokens", ctypes.c_int64)]
 
 
 assert ctypes.sizeof(SelectParamsC) == 40 and ctypes.sizeof(GateParamsC) == 32
@@ -108,6 +118,8 @@ SIGNATURES = {
     "rs_plan_calls_workspace_size": (ctypes.c_size_t, [_I64]),
     "rs_plan_calls": (ctypes.c_int, [_P, _P, _I64, ctypes.POINTER(SelectParamsC), _I64, _P, _P, _P, _P, _P,
                                      ctypes.c_size_t, _P]),
+    "rs_admit_fifo": (ctypes.c_int, [_P, _P, _P, _P, _I64, ctypes.POINTER(SelectParamsC),
+                                     ctypes.POINTER(AdmitParamsC), _P, _P, _P, _P]),
     "rs_launch_count": (ctypes.c_uint64, []),
     "rs_index_enable_timing": (ctypes.c_int, [_P, _I32]),
     "rs_index_kernel_times": (ctypes.c_int, [_P, _P, _I32, ctypes.POINTER(_I32)]),

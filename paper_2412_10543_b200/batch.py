@@ -275,6 +275,29 @@ def plan_calls(configs: torch.Tensor, qlen: torch.Tensor, params: SelectParams, 
     return offsets, calls[:total_calls], totals, status
 
 
+def admit_fifo(spaces: torch.Tensor, profiles: torch.Tensor | None, qlen: torch.Tensor, params: SelectParams, *,
+               capacity_bytes: int, used_bytes: int, max_context_tokens: int,
+               has_profile: torch.Tensor | None = None, stream=None):
+    """The FIFO new-query admission loop of Scheduler.step (scheduler.py
+    :397-410) over a device batch of waiting entries in queue order.
+    Returns device tensors (configs uint8 [n,16] rs_config, info uint8 [n,16]
+    rs_admit_info, result uint8 [24] rs_admit_result); entries
+    [0, result.admitted) were admitted, and ``result.stop`` says why the loop
+    ended (rs_admit_stop)."""
+    n = spaces.shape[0]
+    dev = spaces.device
+    lib = _lib.lib_for_device(_dev_index(spaces))
+    configs = torch.empty((max(n, 1), 16), dtype=torch.uint8, device=dev)
+    info = torch.empty((max(n, 1), 16), dtype=torch.uint8, device=dev)
+    result = torch.empty(24, dtype=torch.uint8, device=dev)
+    pc = params.c()
+    ap = _lib.AdmitParamsC(int(capacity_bytes), int(used_bytes), int(max_context_tokens))
+    _lib.check(lib.rs_admit_fifo(_lib.ptr(spaces), _lib.ptr(profiles), _lib.ptr(has_profile), _lib.ptr(qlen), n,
+                                 ctypes.byref(pc), ctypes.byref(ap), _lib.ptr(configs), _lib.ptr(info),
+                                 _lib.ptr(result), _lib.stream_ptr(stream)), "rs_admit_fifo")
+    return configs[:n], info[:n], result
+
+
 def call_latency_batch(prompt_tokens: torch.Tensor, max_output_tokens: torch.Tensor, concurrent: torch.Tensor,
                        cost: CostModel, stream=None) -> torch.Tensor:
     n = prompt_tokens.shape[0]

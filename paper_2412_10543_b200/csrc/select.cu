@@ -53,6 +53,137 @@ __device__ __forceinline__ void warp_argmax(int64_t& b, int32_t& g) {
   }
 }
 
+// Grid of one pruned space (enumerate_candidates, mapping.py:129-156, with
+// IntRange.values(step), types.py:59-60): method-major RR, ST, MR; n
+// ascending; il ascending inside MR.  Flat index g -> config without
+// materialising the list.
+struct Grid {
+  int m;
+  int64_t n_lo, n_hi, il_lo, il_hi, nn, ni, n_rr, n_st, G;
+  __device__ __forceinline__ Grid(const rs_space& sp, const SelConst& P) {
+    m = sp.methods;
+    n_lo = sp.num_chunks_lo;
+    n_hi = sp.num_chunks_hi;
+    il_lo = sp.interlen_lo;
+    il_hi = sp.interlen_hi;
+    nn = (n_hi >= n_lo) ? (n_hi - n_lo) / P.cstep + 1 : 0;
+    ni = ((m & RS_MAP_REDUCE) && il_hi >= il_lo) ? (il_hi - il_lo) / P.istep + 1 : 0;
+    n_rr = (m & RS_MAP_RERANK) ? nn : 0;
+    n_st = (m & RS_STUFF) ? nn : 0;
+    G = n_rr + n_st + nn * ni;
+  }
+  __device__ __forceinline__ void decode(int64_t g, const SelConst& P, rs_config& c) const {
+    if (g < n_rr) {
+      c.method = RS_MAP_RERANK;
+      c.num_chunks = (uint16_t)(n_lo + g * P.cstep);
+    } else if (g < n_rr + n_st) {
+      c.method = RS_STUFF;
+      c.num_chunks = (uint16_t)(n_lo + (g - n_rr) * P.cstep);
+    } else {
+      const int64_t r = g - n_rr - n_st;
+      const int64_t i_n = r / ni;
+      c.method = RS_MAP_REDUCE;
+      c.num_chunks = (uint16_t)(n_lo + i_n * P.cstep);
+      c.interlen = (uint16_t)(il_lo + (r - i_n * ni) * P.istep);
+    }
+  }
+};
+
+// int64 range guard: a conservative bound over every candidate and the
+// fallback; true = the query's byte arithmetic could overflow.
+__device__ __forceinline__ bool range_overflow(const Grid& gr, int64_t q, const SelConst& P) {
+  const int64_t nmax = gr.n_hi > P.max_chunks ? gr.n_hi : P.max_chunks;
+  const int64_t per = P.C > gr.il_hi ? P.C : gr.il_hi;
+  const int64_t tail = P.O > gr.il_hi ? P.O : gr.il_hi;
+  const int64_t tmax = q + nmax * per + P.T + tail;
+  bool bad = nmax > 65535 || per > (int64_t(1) << 30) || q > (int64_t(1) << 40) || tmax > P.tok_limit;
+  if (!bad) bad = buffered(tmax, P.pt) > (int64_t)(INT64_MAX / 2) / (nmax + 1);
+  return bad;
+}
+
+// best_fit_select (scheduler.py:127-156), warp-collective: arg-max of
+// (bytes, grid index) over the candidates with bytes <= fr.  On a fit sets
+// c.{method,num_chunks,interlen,kv_bytes} and status BEST_FIT; returns false
+// (c untouched) when nothing fits.
+__device__ __forceinline__ bool best_fit_warp(const Grid& gr, int64_t q, int64_t fr, const SelConst& P, int lane,
+                                              rs_config& c) {
+  const int64_t rr_call = buffered(q + P.C + P.T + P.O, P.pt);  // one rerank call
+  int64_t best_b = -1;
+  int32_t best_g = -1;
+  for (int64_t g = lane; g < gr.G; g += 32) {
+    int64_t bytes;
+    if (g < gr.n_rr) {
+      const int64_t nc = gr.n_lo + g * P.cstep;
+      bytes = nc * rr_call;
+    } else if (g < gr.n_rr + gr.n_st) {
+      const int64_t nc = gr.n_lo + (g - gr.n_rr) * P.cstep;
+      bytes = buffered(q + nc * P.C + P.T + P.O, P.pt);
+    } else {
+      const int64_t r = g - gr.n_rr - gr.n_st;
+      const int64_t i_n = r / gr.ni;
+      const int64_t nc = gr.n_lo + i_n * P.cstep;
+      const int64_t il = gr.il_lo + (r - i_n * gr.ni) * P.istep;
+      bytes = nc * buffered(q + P.C + P.T + il, P.pt) + buffered(q + nc * il + P.T + P.O, P.pt);
+    }
+    if (bytes <= fr && bytes >= best_b) {  // g ascends per lane: ties -> later g
+      best_b = bytes;
+      best_g = (int32_t)g;
+    }
+  }
+  warp_argmax(best_b, best_g);
+  if (best_g < 0) return false;
+  gr.decode(best_g, P, c);
+  c.kv_bytes = best_b;
+  c.status = RS_SELECT_BEST_FIT;
+  return true;
+}
+
+// fallback_config (scheduler.py:159-191), warp-collective: never map_reduce,
+// ignores the space.  Sets status FALLBACK or MUST_QUEUE.
+__device__ __forceinline__ void fallback_warp(bool joint, int64_t q, int64_t fr, const SelConst& P, int lane,
+                                              rs_config& c) {
+  const int64_t rr_call = buffered(q + P.C + P.T + P.O, P.pt);
+  if (!joint) {
+    int64_t k = fr / rr_call;  // free >= 0 in the reference; negatives give k < 1 either way
+    if (k > P.max_chunks) k = P.max_chunks;
+    if (k >= 1) {
+      c.method = RS_MAP_RERANK;
+      c.num_chunks = (uint16_t)k;
+      c.kv_bytes = k * rr_call;
+      c.status = RS_SELECT_FALLBACK;
+    } else {
+      c.status = RS_SELECT_MUST_QUEUE;
+    }
+    return;
+  }
+  // largest k in [max_chunks .. 1] whose stuff plan fits
+  int64_t kb = -1, kbytes = 0;
+  for (int64_t k = P.max_chunks - lane; k >= 1; k -= 32) {
+    const int64_t b = buffered(q + k * P.C + P.T + P.O, P.pt);
+    if (b <= fr && k > kb) {
+      kb = k;
+      kbytes = b;
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const int64_t ok = __shfl_xor_sync(0xffffffffu, kb, off);
+    const int64_t obytes = __shfl_xor_sync(0xffffffffu, kbytes, off);
+    if (ok > kb) {
+      kb = ok;
+      kbytes = obytes;
+    }
+  }
+  if (kb >= 1) {
+    c.method = RS_STUFF;
+    c.num_chunks = (uint16_t)kb;
+    c.kv_bytes = kbytes;
+    c.status = RS_SELECT_FALLBACK;
+  } else {
+    c.status = RS_SELECT_MUST_QUEUE;
+  }
+}
+
 __global__ void __launch_bounds__(256) select_kernel(const rs_space* __restrict__ spaces,
                                                      const rs_profile* __restrict__ profiles,
                                                      const int32_t* __restrict__ qlen,
@@ -67,123 +198,24 @@ __global__ void __launch_bounds__(256) select_kernel(const rs_space* __restrict_
   const rs_space sp = spaces[qi];
   const int64_t q = qlen[qi];
   const int64_t fr = free_bytes[qi];
-  const int m = sp.methods;
-  const int64_t n_lo = sp.num_chunks_lo, n_hi = sp.num_chunks_hi;
-  const int64_t il_lo = sp.interlen_lo, il_hi = sp.interlen_hi;
+  const Grid gr(sp, P);
 
-  // grid extents (IntRange.values(step), types.py:59-60)
-  const int64_t nn = (n_hi >= n_lo) ? (n_hi - n_lo) / P.cstep + 1 : 0;
-  const int64_t ni = ((m & RS_MAP_REDUCE) && il_hi >= il_lo) ? (il_hi - il_lo) / P.istep + 1 : 0;
-  const int64_t n_rr = (m & RS_MAP_RERANK) ? nn : 0;
-  const int64_t n_st = (m & RS_STUFF) ? nn : 0;
-  const int64_t G = n_rr + n_st + nn * ni;
-
-  // int64 range guard (conservative bound over every candidate + fallback)
-  {
-    const int64_t nmax = n_hi > P.max_chunks ? n_hi : P.max_chunks;
-    const int64_t per = P.C > il_hi ? P.C : il_hi;
-    const int64_t tail = P.O > il_hi ? P.O : il_hi;
-    const int64_t tmax = q + nmax * per + P.T + tail;
-    bool bad = nmax > 65535 || per > (int64_t(1) << 30) || q > (int64_t(1) << 40) ||
-               tmax > P.tok_limit;
-    if (!bad) bad = buffered(tmax, P.pt) > (int64_t)(INT64_MAX / 2) / (nmax + 1);
-    if (bad) {
-      if (lane == 0) {
-        rs_config c{};
-        c.status = RS_SELECT_OVERFLOW;
-        out[qi] = c;
-        if (delay) delay[qi] = 0.0;
-      }
-      return;
+  if (range_overflow(gr, q, P)) {
+    if (lane == 0) {
+      rs_config c{};
+      c.status = RS_SELECT_OVERFLOW;
+      out[qi] = c;
+      if (delay) delay[qi] = 0.0;
     }
+    return;
   }
-
-  const int64_t rr_call = buffered(q + P.C + P.T + P.O, P.pt);  // one rerank call
-  int64_t best_b = -1;
-  int32_t best_g = -1;
-  for (int64_t g = lane; g < G; g += 32) {
-    int64_t bytes;
-    if (g < n_rr) {
-      const int64_t nc = n_lo + g * P.cstep;
-      bytes = nc * rr_call;
-    } else if (g < n_rr + n_st) {
-      const int64_t nc = n_lo + (g - n_rr) * P.cstep;
-      bytes = buffered(q + nc * P.C + P.T + P.O, P.pt);
-    } else {
-      const int64_t r = g - n_rr - n_st;
-      const int64_t i_n = r / ni;
-      const int64_t nc = n_lo + i_n * P.cstep;
-      const int64_t il = il_lo + (r - i_n * ni) * P.istep;
-      bytes = nc * buffered(q + P.C + P.T + il, P.pt) + buffered(q + nc * il + P.T + P.O, P.pt);
-    }
-    if (bytes <= fr && bytes >= best_b) {  // g ascends per lane: ties -> later g
-      best_b = bytes;
-      best_g = (int32_t)g;
-    }
-  }
-  warp_argmax(best_b, best_g);
 
   rs_config c{};
-  if (best_g >= 0) {
-    const int64_t g = best_g;
-    if (g < n_rr) {
-      c.method = RS_MAP_RERANK;
-      c.num_chunks = (uint16_t)(n_lo + g * P.cstep);
-    } else if (g < n_rr + n_st) {
-      c.method = RS_STUFF;
-      c.num_chunks = (uint16_t)(n_lo + (g - n_rr) * P.cstep);
-    } else {
-      const int64_t r = g - n_rr - n_st;
-      const int64_t i_n = r / ni;
-      c.method = RS_MAP_REDUCE;
-      c.num_chunks = (uint16_t)(n_lo + i_n * P.cstep);
-      c.interlen = (uint16_t)(il_lo + (r - i_n * ni) * P.istep);
-    }
-    c.kv_bytes = best_b;
-    c.status = RS_SELECT_BEST_FIT;
-  } else if (P.allow_fallback) {
-    // fallback_config (scheduler.py:159-191): never map_reduce, ignores the space
-    if (!profiles[qi].needs_joint_reasoning) {
-      int64_t k = fr / rr_call;  // free >= 0 in the reference; negatives give k < 1 either way
-      if (k > P.max_chunks) k = P.max_chunks;
-      if (k >= 1) {
-        c.method = RS_MAP_RERANK;
-        c.num_chunks = (uint16_t)k;
-        c.kv_bytes = k * rr_call;
-        c.status = RS_SELECT_FALLBACK;
-      } else {
-        c.status = RS_SELECT_MUST_QUEUE;
-      }
-    } else {
-      // largest k in [max_chunks .. 1] whose stuff plan fits
-      int64_t kb = -1, kbytes = 0;
-      for (int64_t k = P.max_chunks - lane; k >= 1; k -= 32) {
-        const int64_t b = buffered(q + k * P.C + P.T + P.O, P.pt);
-        if (b <= fr && k > kb) {
-          kb = k;
-          kbytes = b;
-        }
-      }
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-        const int64_t ok = __shfl_xor_sync(0xffffffffu, kb, off);
-        const int64_t obytes = __shfl_xor_sync(0xffffffffu, kbytes, off);
-        if (ok > kb) {
-          kb = ok;
-          kbytes = obytes;
-        }
-      }
-      if (kb >= 1) {
-        c.method = RS_STUFF;
-        c.num_chunks = (uint16_t)kb;
-        c.kv_bytes = kbytes;
-        c.status = RS_SELECT_FALLBACK;
-      } else {
-        c.status = RS_SELECT_MUST_QUEUE;
-      }
-    }
-  } else {
-    c.status = RS_SELECT_MUST_QUEUE;
+  if (!best_fit_warp(gr, q, fr, P, lane, c)) {
+    if (P.allow_fallback)
+      fallback_warp(profiles[qi].needs_joint_reasoning != 0, q, fr, P, lane, c);
+    else
+      c.status = RS_SELECT_MUST_QUEUE;
   }
 
   if (lane == 0) out[qi] = c;
@@ -210,6 +242,165 @@ __global__ void __launch_bounds__(256) select_kernel(const rs_space* __restrict_
       }
     }
     delay[qi] = d;
+  }
+}
+
+// plan_calls' raising checks for a chosen config (memory.py:106-145, in the
+// reference's order): chunk count, then per call kind the context window
+// (memory.py:81-86), map_reduce's intermediate length before its mappers.
+// Also returns the independent calls (CallPlan.independent_calls, memory.py
+// :66-67): every call but a map_reduce reducer, all of one size per plan.
+__device__ __forceinline__ int plan_check(const rs_config& c, int64_t q, const SelConst& P, int64_t ctx,
+                                          int64_t& n_indep, int64_t& indep_bytes) {
+  const int64_t n = c.num_chunks;
+  if (n < 1 || n > P.max_chunks) return RS_ADMIT_INVALID_CHUNKS;
+  if (c.method == RS_STUFF) {
+    if (q + n * P.C + P.T + P.O > ctx) return RS_ADMIT_CONTEXT_OVERFLOW;
+    n_indep = 1;
+    indep_bytes = buffered(q + n * P.C + P.T + P.O, P.pt);
+  } else if (c.method == RS_MAP_RERANK) {
+    if (q + P.C + P.T + P.O > ctx) return RS_ADMIT_CONTEXT_OVERFLOW;
+    n_indep = n;
+    indep_bytes = buffered(q + P.C + P.T + P.O, P.pt);
+  } else {
+    const int64_t il = c.interlen;
+    if (il <= 0) return RS_ADMIT_BAD_INTERLEN;
+    if (q + P.C + P.T + il > ctx) return RS_ADMIT_CONTEXT_OVERFLOW;
+    if (q + n * il + P.T + P.O > ctx) return RS_ADMIT_CONTEXT_OVERFLOW;
+    n_indep = n;
+    indep_bytes = buffered(q + P.C + P.T + il, P.pt);
+  }
+  return RS_ADMIT_DRAINED;  // ok
+}
+
+// FIFO admission chain: the new-query loop of Scheduler.step
+// (scheduler.py:397-410) over _try_admit_new (:335-395) and the memory
+// accounting of _start_run (:281-333).  The chain is serial through the free
+// bytes (each admission lowers them by its admitted independent calls; a
+// map_reduce reducer is deferred), so one warp walks the queue in order and
+// evaluates each query's candidates lane-parallel; queue records are
+// prefetched 32 at a time (lane j loads entry base + j) and broadcast with
+// shuffles, keeping global-load latency off the serial path.
+__global__ void __launch_bounds__(32) admit_fifo_kernel(const rs_space* __restrict__ spaces,
+                                                        const rs_profile* __restrict__ profiles,
+                                                        const uint8_t* __restrict__ has_profile,
+                                                        const int32_t* __restrict__ qlen, int64_t n, SelConst P,
+                                                        int64_t capacity, int64_t used0, int64_t ctx,
+                                                        rs_config* __restrict__ configs,
+                                                        rs_admit_info* __restrict__ info,
+                                                        rs_admit_result* __restrict__ result) {
+  const int lane = threadIdx.x;
+  int64_t used = used0;
+  int64_t i = 0;
+  int32_t stop = RS_ADMIT_DRAINED;
+  for (int64_t base = 0; base < n && stop == RS_ADMIT_DRAINED; base += 32) {
+    // prefetch 32 queue entries: lane j holds entry base + j
+    uint2 sp_lo = make_uint2(0, 0), sp_hi = make_uint2(0, 0);
+    int32_t ql = 0;
+    uint32_t joint = 0, hasp = 1;
+    if (base + lane < n) {
+      const uint4 v = reinterpret_cast<const uint4*>(spaces)[base + lane];
+      sp_lo = make_uint2(v.x, v.y);
+      sp_hi = make_uint2(v.z, v.w);
+      ql = qlen[base + lane];
+      if (profiles) joint = profiles[base + lane].needs_joint_reasoning;
+      if (has_profile) hasp = has_profile[base + lane];
+    }
+    const int cnt = int(n - base < 32 ? n - base : 32);
+    for (int t = 0; t < cnt; ++t) {
+      i = base + t;
+      uint4 v;
+      v.x = __shfl_sync(0xffffffffu, sp_lo.x, t);
+      v.y = __shfl_sync(0xffffffffu, sp_lo.y, t);
+      v.z = __shfl_sync(0xffffffffu, sp_hi.x, t);
+      v.w = __shfl_sync(0xffffffffu, sp_hi.y, t);
+      rs_space sp;
+      memcpy(&sp, &v, sizeof(sp));
+      const int64_t q = __shfl_sync(0xffffffffu, ql, t);
+      const bool jt = __shfl_sync(0xffffffffu, joint, t) != 0;
+      const bool hp = __shfl_sync(0xffffffffu, hasp, t) != 0;
+      const int64_t fr = capacity - used;
+      const Grid gr(sp, P);
+
+      rs_config c{};
+      int64_t n_adm = 0, adm_bytes = 0;
+      bool fixed = false;
+      if (range_overflow(gr, q, P)) {
+        stop = RS_ADMIT_OVERFLOW;
+      } else {
+        // best fit first, whatever the mode (scheduler.py:339-351)
+        bool ok = best_fit_warp(gr, q, fr, P, lane, c);
+        if (!ok && P.allow_fallback) {
+          if (!hp) {
+            stop = RS_ADMIT_NO_PROFILE;  // scheduler.py:356-359
+          } else {
+            fallback_warp(jt, q, fr, P, lane, c);
+            ok = c.status == RS_SELECT_FALLBACK;
+            if (!ok) stop = used == 0 ? RS_ADMIT_IMPOSSIBLE : RS_ADMIT_BLOCKED;  // :374-378
+          }
+        } else if (!ok) {
+          // fixed-config baseline (scheduler.py:380-395): exactly one
+          // candidate, admitted call by call in index order while each fits
+          fixed = true;
+          if (gr.G != 1) {
+            stop = RS_ADMIT_FIXED_SPACE;
+          } else {
+            gr.decode(0, P, c);
+            int64_t n_ind = 0, per = 0;
+            const int rc = plan_check(c, q, P, ctx, n_ind, per);
+            if (rc != RS_ADMIT_DRAINED) {
+              stop = rc;
+            } else if (per > capacity) {
+              stop = RS_ADMIT_IMPOSSIBLE;
+            } else if (per > fr) {
+              stop = RS_ADMIT_BLOCKED;
+            } else {
+              const int64_t nc = c.num_chunks;
+              c.kv_bytes = c.method == RS_STUFF        ? per
+                           : c.method == RS_MAP_RERANK ? nc * per
+                                                       : nc * per + buffered(q + nc * c.interlen + P.T + P.O, P.pt);
+              c.status = RS_SELECT_BEST_FIT;
+              n_adm = fr / per < n_ind ? fr / per : n_ind;
+              adm_bytes = n_adm * per;
+            }
+          }
+        }
+        if (ok && !fixed) {
+          int64_t n_ind = 0, per = 0;
+          const int rc = plan_check(c, q, P, ctx, n_ind, per);
+          if (rc != RS_ADMIT_DRAINED) {
+            stop = rc;
+          } else {
+            // admit_all_independent: every independent call fits by construction
+            // (their sum is at most plan_bytes <= free); the host re-checks
+            n_adm = n_ind;
+            adm_bytes = n_ind * per;
+          }
+        }
+      }
+      if (stop != RS_ADMIT_DRAINED) {
+        // the chosen (or fixed) config of the entry that raised, for the
+        // caller's error message
+        if (lane == 0) configs[i] = c;
+        break;
+      }
+      used += adm_bytes;
+      if (lane == 0) {
+        configs[i] = c;
+        rs_admit_info a{};
+        a.admitted_bytes = adm_bytes;
+        a.admitted_calls = int32_t(n_adm);
+        a.fixed_path = fixed ? 1 : 0;
+        info[i] = a;
+      }
+    }
+  }
+  if (lane == 0) {
+    rs_admit_result r{};
+    r.admitted = stop == RS_ADMIT_DRAINED ? n : i;
+    r.used_bytes = used;
+    r.stop = stop;
+    *result = r;
   }
 }
 
@@ -318,5 +509,27 @@ extern "C" int rs_plan_bytes(const uint8_t* method, const int32_t* num_chunks, c
   plan_bytes_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(method, num_chunks, interlen, qlen, n,
                                                                      c, out);
   RS_CHECK_LAUNCH("plan_bytes_kernel");
+  return RS_OK;
+}
+
+extern "C" int rs_admit_fifo(const rs_space* spaces, const rs_profile* profiles, const uint8_t* has_profile,
+                             const int32_t* qlen, int64_t n, const rs_select_params* params,
+                             const rs_admit_params* admit, rs_config* configs, rs_admit_info* info,
+                             rs_admit_result* result, void* stream) {
+  using namespace rs;
+  RS_REQUIRE(n >= 0, "n must be non-negative");
+  RS_REQUIRE(admit != nullptr && result != nullptr, "NULL argument");
+  RS_REQUIRE(n == 0 || (spaces && qlen && configs && info), "NULL device pointer");
+  RS_REQUIRE(n == 0 || profiles || (params && !params->allow_fallback), "profiles required by the fallback");
+  RS_REQUIRE(admit->capacity_bytes > 0, "capacity_bytes must be positive");
+  RS_REQUIRE(admit->used_bytes >= 0 && admit->used_bytes <= admit->capacity_bytes, "used_bytes outside [0, capacity]");
+  RS_REQUIRE(admit->max_context_tokens > 0, "max_context_tokens must be positive");
+  SelConst c;
+  int rc = make_const(params, nullptr, &c);
+  if (rc) return rc;
+  admit_fifo_kernel<<<1, 32, 0, as_stream(stream)>>>(spaces, profiles, has_profile, qlen, n, c,
+                                                     admit->capacity_bytes, admit->used_bytes,
+                                                     admit->max_context_tokens, configs, info, result);
+  RS_CHECK_LAUNCH("admit_fifo_kernel");
   return RS_OK;
 }

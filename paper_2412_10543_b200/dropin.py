@@ -13,12 +13,32 @@ of the reference pipeline are unchanged.
 from __future__ import annotations
 
 import functools
+from types import SimpleNamespace
 
 from . import mapping as _mapping
 from . import memory as _memory
 from . import profiler as _profiler
 from . import scheduler as _scheduler
 from . import sim as _sim
+
+
+def scheduler_class(ragsched_pkg):
+    """This package's GPU-backed Scheduler (FIFO admission chain on the
+    device, scheduler.py:194-469) building the reference's own Admission /
+    AdmittedCall / CompletionInfo / QueryRun / CallPlan objects and raising
+    its own exceptions."""
+    import importlib
+
+    sched = importlib.import_module(ragsched_pkg.__name__ + ".scheduler")
+    memory = importlib.import_module(ragsched_pkg.__name__ + ".memory")
+    types = importlib.import_module(ragsched_pkg.__name__ + ".types")
+    ns = SimpleNamespace(
+        Admission=sched.Admission, AdmittedCall=sched.AdmittedCall, CompletionInfo=sched.CompletionInfo,
+        QueryRun=sched.QueryRun, UnknownCall=sched.UnknownCall, MemorySafetyViolation=sched.MemorySafetyViolation,
+        SchedulingImpossible=sched.SchedulingImpossible, InvalidChunkCount=types.InvalidChunkCount,
+        ContextOverflow=types.ContextOverflow, RagConfig=types.RagConfig, SynthesisMethod=types.SynthesisMethod,
+        LlmCall=memory.LlmCall, CallPlan=memory.CallPlan, CallKind=memory.CallKind)
+    return type("Scheduler", (_scheduler.Scheduler,), {"classes": ns, "__module__": __name__})
 
 
 def install(ragsched_pkg) -> dict:
@@ -44,6 +64,10 @@ def install(ragsched_pkg) -> dict:
         (mapping, "map_profile"): mapping.map_profile,
         (memory, "plan_bytes"): memory.plan_bytes,
         (sim, "call_latency"): sim.call_latency,
+        (sched, "Scheduler"): sched.Scheduler,
+        (sim, "Scheduler"): sim.Scheduler,
+        (memory, "plan_calls"): memory.plan_calls,
+        (sched, "plan_calls"): sched.plan_calls,
     }
 
     sched.best_fit_select = functools.partial(_scheduler.best_fit_select, **kw_cfg)
@@ -55,6 +79,13 @@ def install(ragsched_pkg) -> dict:
     mapping.map_profile = mp
     memory.plan_bytes = _memory.plan_bytes
     sim.call_latency = _sim.call_latency
+    gpu_sched = scheduler_class(ragsched_pkg)
+    sched.Scheduler = gpu_sched
+    sim.Scheduler = gpu_sched
+    pc = functools.partial(_memory.plan_calls, call_cls=memory.LlmCall, plan_cls=memory.CallPlan,
+                           kind_enum=memory.CallKind)
+    memory.plan_calls = pc
+    sched.plan_calls = pc
     return originals
 
 

@@ -37,3 +37,128 @@ def plan_bytes(query_token_len: int, cfg, chunk_size: int, per_token_bytes: int,
     out = _b.plan_bytes_batch(t(m, torch.uint8), t(int(cfg.num_chunks), torch.int32), t(int(il or 0), torch.int32),
                               t(int(query_token_len), torch.int32), params)
     return int(out.item())
+
+
+# -- per-call expansion (memory.py:29-67, :89-150) -----------------------------
+
+from dataclasses import dataclass, field  # noqa: E402
+from enum import Enum  # noqa: E402
+
+import numpy as np  # noqa: E402
+
+from . import _lib  # noqa: E402
+from .types import DEFAULT_MAX_CHUNKS, ContextOverflow, InvalidChunkCount  # noqa: E402
+
+
+class CallKind(str, Enum):
+    """memory.py:29-33."""
+
+    SINGLE = "single"
+    MAPPER = "mapper"
+    REDUCER = "reducer"
+    RERANK = "rerank"
+
+
+class AdmissionMode(str, Enum):
+    """memory.py:36-40."""
+
+    WHOLE = "whole"
+    PER_CALL = "per_call"
+
+
+@dataclass(frozen=True)
+class LlmCall:
+    """memory.py:43-56."""
+
+    kind: CallKind
+    prompt_tokens: int
+    max_output_tokens: int
+    kv_bytes: int
+    index: int = 0
+    depends_on: frozenset = field(default_factory=frozenset)
+
+
+@dataclass(frozen=True)
+class CallPlan:
+    """memory.py:59-67."""
+
+    calls: tuple
+    total_bytes: int
+
+    def independent_calls(self) -> list[int]:
+        return [i for i, c in enumerate(self.calls) if not c.depends_on]
+
+
+def memory_requirement(plan, admission=AdmissionMode.WHOLE) -> int:
+    """memory.py:153-161."""
+    if getattr(admission, "value", admission) == AdmissionMode.WHOLE.value:
+        return plan.total_bytes
+    return max(c.kv_bytes for c in plan.calls)
+
+
+PLAN_ERRORS = {
+    _lib.RS_PLAN_INVALID_CHUNKS: (InvalidChunkCount, "num_chunks {n} outside [1, {mc}]"),
+    _lib.RS_PLAN_CONTEXT_OVERFLOW: (ContextOverflow, "a call of {cfg} exceeds the context window of {ctx} tokens"),
+    _lib.RS_PLAN_BAD_INTERLEN: (ValueError, "map_reduce config requires a positive intermediate_length"),
+}
+
+
+def plans_from_device(offsets, calls, totals, status, *, call_cls=LlmCall, plan_cls=CallPlan,
+                      kind_enum=CallKind) -> list:
+    """Host objects of an ``rs_plan_calls`` result: one CallPlan per query, or
+    the RS_PLAN_* status (int) where the reference raises."""
+    off = offsets.cpu().numpy()
+    rec = _b.from_device(calls, _lib.CALL_DTYPE) if calls.numel() else np.zeros(0, _lib.CALL_DTYPE)
+    tot = totals.cpu().numpy()
+    st = status.cpu().numpy()
+    kinds = [kind_enum(v) for v in _lib.CALL_KINDS]
+    out = []
+    for i in range(len(st)):
+        if st[i] != _lib.RS_PLAN_OK:
+            out.append(int(st[i]))
+            continue
+        cs = []
+        mappers = frozenset()
+        for r in rec[off[i]:off[i + 1]]:
+            kind = kinds[int(r["kind"])]
+            if kind.value == "reducer":
+                deps = mappers
+            else:
+                deps = frozenset()
+            if kind.value == "mapper":
+                mappers = mappers | {int(r["index"])}
+            cs.append(call_cls(kind, int(r["prompt_tokens"]), int(r["max_output_tokens"]), int(r["kv_bytes"]),
+                               index=int(r["index"]), depends_on=deps))
+        out.append(plan_cls(calls=tuple(cs), total_bytes=int(tot[i])))
+    return out
+
+
+def raise_plan_error(code: int, cfg, *, max_chunks: int, max_context_tokens: int):
+    exc, fmt = PLAN_ERRORS[code]
+    desc = cfg.describe() if hasattr(cfg, "describe") else str(cfg)
+    raise exc(fmt.format(n=getattr(cfg, "num_chunks", "?"), mc=max_chunks, cfg=desc, ctx=max_context_tokens))
+
+
+def plan_calls(q, cfg, meta, model, out_budget: int, *, template_tokens: int = DEFAULT_TEMPLATE_TOKENS,
+               max_chunks: int = DEFAULT_MAX_CHUNKS, call_cls=LlmCall, plan_cls=CallPlan, kind_enum=CallKind):
+    """memory.py:89-150 on the GPU (``rs_plan_calls``): the config's LLM calls
+    with their KV bytes.  Raises InvalidChunkCount / ContextOverflow /
+    ValueError exactly where the reference does."""
+    if out_budget <= 0:
+        raise ValueError("out_budget must be positive")
+    dev = _b.default_device()
+    rec = np.zeros(1, dtype=_lib.CONFIG_DTYPE)
+    rec["method"] = method_bit(cfg.synthesis_method)
+    rec["num_chunks"] = min(max(int(cfg.num_chunks), 0), 0xFFFF)
+    il = cfg.intermediate_length
+    rec["interlen"] = 0 if il is None or il <= 0 else min(int(il), 0xFFFF)
+    params = _b.SelectParams(_b.bytes_per_kv_token(model), int(meta.chunk_size), int(out_budget),
+                             int(template_tokens), int(max_chunks))
+    qlen = torch.tensor([int(q.query_token_len)], dtype=torch.int32, device=dev)
+    res = _b.plan_calls(_b.to_device(rec, dev), qlen, params, int(model.max_context_tokens))
+    plan = plans_from_device(*res, call_cls=call_cls, plan_cls=plan_cls, kind_enum=kind_enum)[0]
+    if isinstance(plan, int):
+        if int(cfg.num_chunks) < 1 or int(cfg.num_chunks) > max_chunks:
+            plan = _lib.RS_PLAN_INVALID_CHUNKS
+        raise_plan_error(plan, cfg, max_chunks=max_chunks, max_context_tokens=model.max_context_tokens)
+    return plan

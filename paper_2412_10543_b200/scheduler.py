@@ -48,3 +48,370 @@ def fallback_config(profile, q, free_bytes: int, *, model, meta, out_budget: int
                                         allow_fallback=True)
     empty = np.zeros(1, dtype=SPACE_DTYPE)  # no candidates: the kernel goes straight to the fallback
     return _run_select(empty, profile, q, free_bytes, params, config_cls, method_enum)
+
+
+# -- the stateful scheduler (scheduler.py:33-469) -------------------------------
+#
+# Scheduler mirrors the reference class (same attributes, methods, trace
+# events and exceptions).  Its new-query admission loop — the serial FIFO
+# chain of best-fit / fallback / memory accounting that Scheduler.step runs
+# over the waiting queue — is ONE kernel launch (rs_admit_fifo) over the
+# packed queue, followed by one rs_plan_calls launch that expands the
+# admitted configs into their calls.  The host applies those decisions to the
+# per-call state (active runs, backlog, trace), which the reference keeps in
+# Python objects too; completions and the backlog pass are pure bookkeeping.
+
+import itertools  # noqa: E402
+from collections import deque  # noqa: E402
+from dataclasses import dataclass, field  # noqa: E402
+from types import SimpleNamespace  # noqa: E402
+
+from . import _lib  # noqa: E402
+from . import memory as _mem  # noqa: E402
+from .types import ContextOverflow, InvalidChunkCount  # noqa: E402
+
+
+class UnknownCall(KeyError):
+    """scheduler.py:33-34."""
+
+
+class MemorySafetyViolation(RuntimeError):
+    """scheduler.py:37-38."""
+
+
+@dataclass(frozen=True)
+class SchedulerParams:
+    """scheduler.py:45-56."""
+
+    model: object
+    meta: object
+    out_budget: int
+    template_tokens: int = DEFAULT_TEMPLATE_TOKENS
+    max_chunks: int = DEFAULT_MAX_CHUNKS
+    granularity: EnumGranularity = EnumGranularity()
+    allow_fallback: bool = True
+
+
+@dataclass
+class PendingQuery:
+    """scheduler.py:59-71."""
+
+    query: object
+    space: object
+    arrival_time: float
+    profile: object = None
+    truth: object = None
+    gate_fallback: bool = False
+    confidence: float = 1.0
+    profiler_latency: float = 0.0
+
+
+@dataclass(frozen=True)
+class Admission:
+    """scheduler.py:74-82."""
+
+    query_id: str
+    chosen_config: RagConfig
+    admitted_calls: tuple
+    deferred_calls: tuple
+    is_fallback: bool
+
+
+@dataclass(frozen=True)
+class AdmittedCall:
+    """scheduler.py:85-93."""
+
+    query_id: str
+    call_index: int
+    prompt_tokens: int
+    max_output_tokens: int
+    kv_bytes: int
+
+
+@dataclass(frozen=True)
+class CompletionInfo:
+    """scheduler.py:96-102."""
+
+    query_done: bool
+    config: RagConfig
+    is_fallback: bool
+    newly_ready: tuple
+    winning_rerank: int | None = None
+
+
+@dataclass
+class QueryRun:
+    """scheduler.py:105-124."""
+
+    pending: PendingQuery
+    config: RagConfig
+    plan: object
+    is_fallback: bool
+    admission_time: float
+    admitted: set = field(default_factory=set)
+    completed: set = field(default_factory=set)
+    rerank_confidences: dict = field(default_factory=dict)
+
+    def deferred(self) -> list[int]:
+        return [i for i in range(len(self.plan.calls)) if i not in self.admitted]
+
+    def ready(self, idx: int) -> bool:
+        return self.plan.calls[idx].depends_on <= self.completed
+
+    def fully_admitted(self) -> bool:
+        return len(self.admitted) == len(self.plan.calls)
+
+    def done(self) -> bool:
+        return len(self.completed) == len(self.plan.calls)
+
+
+def own_classes() -> SimpleNamespace:
+    """The value/exception classes a Scheduler builds (this package's
+    mirrors; ``dropin`` substitutes the reference's own)."""
+    return SimpleNamespace(
+        Admission=Admission, AdmittedCall=AdmittedCall, CompletionInfo=CompletionInfo, QueryRun=QueryRun,
+        UnknownCall=UnknownCall, MemorySafetyViolation=MemorySafetyViolation,
+        SchedulingImpossible=SchedulingImpossible, InvalidChunkCount=InvalidChunkCount,
+        ContextOverflow=ContextOverflow, RagConfig=RagConfig, SynthesisMethod=SynthesisMethod,
+        LlmCall=_mem.LlmCall, CallPlan=_mem.CallPlan, CallKind=_mem.CallKind)
+
+
+class Scheduler:
+    """scheduler.py:194-469: the FIFO waiting queue, the running batch and the
+    KV memory accounting, with the admission chain on the GPU."""
+
+    classes = None  # SimpleNamespace of the classes to build (own_classes() when None)
+    FIRST_CHUNK = 32  # queue entries packed for the first admission launch of a step (doubles)
+
+    def __init__(self, capacity_bytes: int, params) -> None:
+        if capacity_bytes <= 0:
+            raise ValueError("capacity_bytes must be positive")
+        self.capacity_bytes = capacity_bytes
+        self.params = params
+        self.used_bytes = 0
+        self.waiting: deque = deque()
+        self.active: dict = {}
+        self.backlog_order: list[str] = []
+        self.trace: list[dict] = []
+        self._k = self.classes or own_classes()
+        self._packed: dict[int, tuple] = {}
+        g = params.granularity
+        self._sel = _b.SelectParams.from_model(params.model, params.meta, params.out_budget, params.template_tokens,
+                                               params.max_chunks, g, allow_fallback=params.allow_fallback)
+        self._dev = None
+
+    @property
+    def free_bytes(self) -> int:
+        return self.capacity_bytes - self.used_bytes
+
+    def submit(self, pending) -> None:
+        self.waiting.append(pending)
+
+    # -- admission ---------------------------------------------------------
+
+    def _check_accounting(self) -> None:
+        if not 0 <= self.used_bytes <= self.capacity_bytes:
+            raise self._k.MemorySafetyViolation(f"used {self.used_bytes} outside [0, {self.capacity_bytes}]")
+
+    def _admit_call(self, run, idx: int, now: float, admitted: list, deferred: bool) -> None:
+        call = run.plan.calls[idx]
+        self.used_bytes += call.kv_bytes
+        self._check_accounting()
+        run.admitted.add(idx)
+        admitted.append(self._k.AdmittedCall(query_id=run.pending.query.id, call_index=idx,
+                                             prompt_tokens=call.prompt_tokens,
+                                             max_output_tokens=call.max_output_tokens, kv_bytes=call.kv_bytes))
+        if deferred:
+            self.trace.append({"event": "admit_deferred", "t": now, "query": run.pending.query.id, "call": idx,
+                               "kv_bytes": call.kv_bytes})
+
+    def _admit_backlog(self, now: float, admitted: list) -> bool:
+        """scheduler.py:257-270: deferred work of admitted queries, FIFO; True
+        when a ready call does not fit (blocks new admissions)."""
+        for qid in list(self.backlog_order):
+            run = self.active[qid]
+            for idx in run.deferred():
+                call = run.plan.calls[idx]
+                if not run.ready(idx):
+                    continue
+                if call.kv_bytes > self.free_bytes:
+                    return True
+                self._admit_call(run, idx, now, admitted, deferred=True)
+            if run.fully_admitted():
+                self.backlog_order.remove(qid)
+        return False
+
+    def _start_run(self, pending, cfg, plan, is_fallback: bool, now: float, admitted: list, *,
+                   admit_all_independent: bool):
+        """scheduler.py:281-333 (the plan comes from rs_plan_calls)."""
+        run = self._k.QueryRun(pending=pending, config=cfg, plan=plan, is_fallback=is_fallback, admission_time=now)
+        self.active[pending.query.id] = run
+        for idx in plan.independent_calls():
+            call = plan.calls[idx]
+            if call.kv_bytes <= self.free_bytes:
+                self._admit_call(run, idx, now, admitted, deferred=False)
+            elif admit_all_independent:
+                raise self._k.MemorySafetyViolation(
+                    f"call {idx} of {pending.query.id} should fit after best-fit selection")
+        deferred = tuple(run.deferred())
+        if deferred:
+            self.backlog_order.append(pending.query.id)
+        admission = self._k.Admission(query_id=pending.query.id, chosen_config=cfg,
+                                      admitted_calls=tuple(sorted(run.admitted)), deferred_calls=deferred,
+                                      is_fallback=is_fallback)
+        self.trace.append({"event": "admission", "t": now, "query": pending.query.id, "config": cfg.describe(),
+                           "admitted": list(admission.admitted_calls), "deferred": list(admission.deferred_calls),
+                           "fallback": is_fallback})
+        return admission
+
+    def _pack(self, pending) -> tuple:
+        key = id(pending)
+        rec = self._packed.get(key)
+        if rec is None or rec[0] is not pending:
+            sp = np.zeros(1, dtype=SPACE_DTYPE)
+            sp[0] = (*_b.space_record(pending.space), 0, 0)
+            prof = pending.profile
+            pr = _b.pack_profiles([prof]) if prof is not None else np.zeros(1, dtype=_lib.PROFILE_DTYPE)
+            rec = (pending, sp.tobytes(), pr.tobytes(), prof is not None, int(pending.query.query_token_len))
+            self._packed[key] = rec
+        return rec
+
+    def _device(self):
+        if self._dev is None:
+            self._dev = _b.default_device()
+        return self._dev
+
+    def _admit_new(self, now: float, admissions: list, admitted: list) -> None:
+        """The loop of scheduler.py:404-409 over _try_admit_new (:335-395),
+        as rs_admit_fifo launches over chunks of the waiting queue."""
+        k, p = self._k, self.params
+        dev = self._device()
+        chunk = self.FIRST_CHUNK
+        while self.waiting:
+            entries = [self._pack(pq) for pq in itertools.islice(self.waiting, 0, chunk)]
+            n = len(entries)
+            sp = torch.frombuffer(bytearray(b"".join(e[1] for e in entries)), dtype=torch.uint8).view(n, 16)
+            pr = torch.frombuffer(bytearray(b"".join(e[2] for e in entries)), dtype=torch.uint8).view(n, 16)
+            hp = torch.tensor([e[3] for e in entries], dtype=torch.uint8)
+            ql = torch.tensor([e[4] for e in entries], dtype=torch.int32)
+            sp, pr, hp, ql = (t.to(dev, non_blocking=True) for t in (sp, pr, hp, ql))
+            configs, info, result = _b.admit_fifo(sp, pr, ql, self._sel, capacity_bytes=self.capacity_bytes,
+                                                  used_bytes=self.used_bytes,
+                                                  max_context_tokens=p.model.max_context_tokens, has_profile=hp)
+            m_dev = None
+            res = _b.from_device(result.view(1, 24), _lib.ADMIT_RESULT_DTYPE)[0]
+            m, stop = int(res["admitted"]), int(res["stop"])
+            cfg_all = _b.from_device(configs[: min(m + 1, n)], _lib.CONFIG_DTYPE)
+            if m:
+                m_dev = configs[:m]
+                plans = _mem.plans_from_device(*_b.plan_calls(m_dev, ql[:m], self._sel, p.model.max_context_tokens),
+                                               call_cls=k.LlmCall, plan_cls=k.CallPlan, kind_enum=k.CallKind)
+                infos = _b.from_device(info[:m], _lib.ADMIT_INFO_DTYPE)
+            for j in range(m):
+                pending = self.waiting[0]
+                rec = cfg_all[j]
+                cfg = _b.unpack_config(rec, config_cls=k.RagConfig, method_enum=k.SynthesisMethod)
+                plan = plans[j]
+                if isinstance(plan, int):  # the kernel checked the plan; a mismatch is a bug
+                    raise _lib.RagschedError(f"rs_plan_calls rejected an admitted config (status {plan})")
+                used0 = self.used_bytes
+                adm = self._start_run(pending, cfg, plan, int(rec["status"]) == _lib.RS_SELECT_FALLBACK, now,
+                                      admitted, admit_all_independent=not int(infos[j]["fixed_path"]))
+                if self.used_bytes - used0 != int(infos[j]["admitted_bytes"]):
+                    raise _lib.RagschedError("admission accounting diverged from rs_admit_fifo")
+                self.waiting.popleft()
+                self._packed.pop(id(pending), None)
+                admissions.append(adm)
+            if stop == _lib.RS_ADMIT_DRAINED:
+                chunk *= 2
+                continue
+            if stop == _lib.RS_ADMIT_BLOCKED:
+                return
+            self._raise_stop(stop, self.waiting[0], cfg_all[m] if m < len(cfg_all) else None)
+
+    def _raise_stop(self, stop: int, pending, rec) -> None:
+        k, p = self._k, self.params
+        q = pending.query
+        cfg = None
+        if rec is not None and int(rec["method"]) in (1, 2, 4):
+            m = int(rec["method"])
+            cfg = k.RagConfig(k.SynthesisMethod({1: "map_rerank", 2: "stuff", 4: "map_reduce"}[m]),
+                              int(rec["num_chunks"]), int(rec["interlen"]) if m == 4 else None)
+        if stop == _lib.RS_ADMIT_NO_PROFILE:
+            raise k.SchedulingImpossible(f"query {q.id} needs the fallback path but carries no profile")
+        if stop == _lib.RS_ADMIT_IMPOSSIBLE:
+            if p.allow_fallback:
+                raise k.SchedulingImpossible(f"query {q.id} cannot fit even with all memory free")
+            raise k.SchedulingImpossible(f"fixed config {cfg.describe()} can never fit capacity for query {q.id}")
+        if stop == _lib.RS_ADMIT_FIXED_SPACE:
+            raise k.SchedulingImpossible("fallback is disabled but the space is not a single fixed config")
+        if stop == _lib.RS_ADMIT_INVALID_CHUNKS:
+            raise k.InvalidChunkCount(f"num_chunks {cfg.num_chunks} outside [1, {p.max_chunks}]")
+        if stop == _lib.RS_ADMIT_BAD_INTERLEN:
+            raise ValueError("map_reduce config requires a positive intermediate_length")
+        if stop == _lib.RS_ADMIT_CONTEXT_OVERFLOW:
+            raise k.ContextOverflow(self._overflow_message(q.query_token_len, cfg))
+        raise OverflowError(f"KV byte arithmetic exceeds int64 for query {q.id}")
+
+    def _overflow_message(self, qlen: int, cfg) -> str:
+        """The message of the first failing _check_context (memory.py:81-86,
+        :117-145) for this config."""
+        p = self.params
+        C, T, O, ctx = p.meta.chunk_size, p.template_tokens, p.out_budget, p.model.max_context_tokens
+        n, m = cfg.num_chunks, cfg.synthesis_method.value
+        if m == "stuff":
+            checks = [("stuff call", qlen + n * C + T, O)]
+        elif m == "map_rerank":
+            checks = [("rerank call", qlen + C + T, O)]
+        else:
+            il = cfg.intermediate_length
+            checks = [("mapper call", qlen + C + T, il), ("reducer call", qlen + n * il + T, O)]
+        for label, prompt, out in checks:
+            if prompt + out > ctx:
+                return f"{label} needs {prompt + out} tokens, context window is {ctx}"
+        return "context window exceeded"
+
+    def step(self, now: float):
+        """scheduler.py:397-410: deferred work first, then new queries in FIFO
+        order until the head cannot make progress."""
+        admissions: list = []
+        admitted: list = []
+        blocked = self._admit_backlog(now, admitted)
+        if not blocked and self.waiting:
+            self._admit_new(now, admissions, admitted)
+        return admissions, admitted
+
+    # -- completion --------------------------------------------------------
+
+    def complete(self, query_id: str, call_index: int, now: float, rerank_confidence: float | None = None):
+        """scheduler.py:414-466."""
+        k = self._k
+        run = self.active.get(query_id)
+        if run is None:
+            raise k.UnknownCall(f"no active query {query_id}")
+        if call_index not in run.admitted or call_index in run.completed:
+            raise k.UnknownCall(f"call {call_index} of {query_id} is not running")
+        call = run.plan.calls[call_index]
+        self.used_bytes -= call.kv_bytes
+        self._check_accounting()
+        run.completed.add(call_index)
+        if rerank_confidence is not None:
+            run.rerank_confidences[call_index] = rerank_confidence
+        self.trace.append({"event": "completion", "t": now, "query": query_id, "call": call_index})
+        newly_ready = tuple(i for i in run.deferred()
+                            if run.ready(i) and not (run.plan.calls[i].depends_on <= (run.completed - {call_index})))
+        if not run.done():
+            return k.CompletionInfo(query_done=False, config=run.config, is_fallback=run.is_fallback,
+                                    newly_ready=newly_ready)
+        winning = None
+        if run.config.synthesis_method.value == "map_rerank" and run.rerank_confidences:
+            winning = max(sorted(run.rerank_confidences), key=lambda i: run.rerank_confidences[i])
+        del self.active[query_id]
+        if query_id in self.backlog_order:
+            self.backlog_order.remove(query_id)
+        self.trace.append({"event": "query_done", "t": now, "query": query_id, "winning_rerank": winning})
+        return k.CompletionInfo(query_done=True, config=run.config, is_fallback=run.is_fallback,
+                                newly_ready=newly_ready, winning_rerank=winning)
+
+    def idle(self) -> bool:
+        return not self.waiting and not self.active

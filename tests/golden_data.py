@@ -64,3 +64,25 @@ def plan_calls():
     calls int64 [c, 6]: trial, kind, prompt, out, kv_bytes, index."""
     z = _load("plan_calls.npz")
     return z["rows"], z["calls"]
+
+
+# PARAM_SETS of make_golden.py (layers, heads, head_dim, width, chunk, out, template, max_chunks, cstep, istep)
+PARAM_SETS = [
+    (32, 8, 128, 2, 1000, 10, 64, 35, 1, 10),
+    (32, 8, 128, 2, 1000, 40, 64, 35, 1, 10),
+    (32, 8, 128, 2, 1024, 40, 64, 35, 1, 10),
+    (32, 8, 128, 2, 1024, 60, 64, 35, 1, 10),
+    (32, 8, 128, 2, 1000, 20, 64, 35, 1, 10),
+    (80, 8, 128, 1, 512, 10, 0, 20, 2, 5),
+    (28, 4, 128, 0.5, 1000, 60, 100, 50, 1, 1),
+    (16, 16, 64, 4, 700, 7, 33, 35, 3, 7),
+]
+
+
+def scheduler_traces():
+    """Reference Scheduler runs (tests/golden/make_sched_golden.py)."""
+    import gzip
+    import json
+
+    with gzip.open(os.path.join(GOLDEN, "scheduler_traces.json.gz"), "rt") as f:
+        return json.load(f)

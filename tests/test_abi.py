@@ -51,9 +51,10 @@ def test_struct_sizes_match_header():
 #include <stddef.h>
 #include "ragsched_b200.h"
 int main(void) {
-  printf("%zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(rs_profile), sizeof(rs_space), sizeof(rs_config),
-         sizeof(rs_select_params), sizeof(rs_cost_model), sizeof(rs_gate_params), sizeof(rs_window),
-         offsetof(rs_profile, confidence));
+  printf("%zu %zu %zu %zu %zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(rs_profile), sizeof(rs_space),
+         sizeof(rs_config), sizeof(rs_select_params), sizeof(rs_cost_model), sizeof(rs_gate_params),
+         sizeof(rs_window), offsetof(rs_profile, confidence), sizeof(rs_call), sizeof(rs_admit_params),
+         sizeof(rs_admit_info), sizeof(rs_admit_result));
   return 0;
 }
 """
@@ -67,7 +68,9 @@ int main(void) {
     assert sizes == [_lib.PROFILE_DTYPE.itemsize, _lib.SPACE_DTYPE.itemsize, _lib.CONFIG_DTYPE.itemsize,
                      ctypes.sizeof(_lib.SelectParamsC), ctypes.sizeof(_lib.CostModelC),
                      ctypes.sizeof(_lib.GateParamsC), _lib.WINDOW_DTYPE.itemsize,
-                     _lib.PROFILE_DTYPE.fields["confidence"][1]]
+                     _lib.PROFILE_DTYPE.fields["confidence"][1], _lib.CALL_DTYPE.itemsize,
+                     ctypes.sizeof(_lib.AdmitParamsC), _lib.ADMIT_INFO_DTYPE.itemsize,
+                     _lib.ADMIT_RESULT_DTYPE.itemsize]
 
 
 def test_sass_contains_tcgen05_and_tma():

@@ -29,16 +29,20 @@ def test_install_and_uninstall(ragsched):
 
     from paper_2412_10543_b200 import dropin
 
-    before = (scheduler.best_fit_select, scheduler.fallback_config, profiler.gate_profile, mapping.map_profile,
-              memory.plan_bytes, sim.call_latency)
+    names = lambda: (scheduler.best_fit_select, scheduler.fallback_config, profiler.gate_profile,  # noqa: E731
+                     mapping.map_profile, memory.plan_bytes, sim.call_latency, scheduler.Scheduler, sim.Scheduler,
+                     memory.plan_calls, scheduler.plan_calls)
+    before = names()
     originals = dropin.install(ragsched)
-    after = (scheduler.best_fit_select, scheduler.fallback_config, profiler.gate_profile, mapping.map_profile,
-             memory.plan_bytes, sim.call_latency)
+    after = names()
     assert all(a is not b for a, b in zip(before, after))
     # wrappers produce the reference's own classes
     assert scheduler.best_fit_select.keywords["config_cls"] is ragsched.types.RagConfig
     assert profiler.gate_profile.keywords["decision_cls"] is profiler.GateDecision
+    # the GPU Scheduler builds the reference's own value classes
+    assert scheduler.Scheduler.classes.Admission is ragsched.scheduler.Admission
+    assert scheduler.Scheduler.classes.CallKind is ragsched.memory.CallKind
+    assert sim.Scheduler is scheduler.Scheduler
     dropin.uninstall(originals)
-    restored = (scheduler.best_fit_select, scheduler.fallback_config, profiler.gate_profile, mapping.map_profile,
-                memory.plan_bytes, sim.call_latency)
+    restored = names()
     assert all(a is b for a, b in zip(before, restored))
