@@ -250,6 +250,86 @@ int launch_merge(const uint64_t* keys, int64_t nq, int nlists, int k_in, int64_t
   return RS_OK;
 }
 
+// Exact fp32 re-rank of the 3xTF32 candidates.  The tensor core accumulates
+// each MMA's products into the fp32 TMEM accumulator with truncation, so at
+// d = 768 a near neighbour's dot (~0.9) drifts by ~1.4e-5 relative — above the
+// north star's 1e-5 fp32 tolerance.  The fused kernel therefore keeps
+// kc = k + kRefineExtra candidates per query, and this kernel recomputes
+// their distances with fp32 FMAs on CUDA cores (lanes over the dimension,
+// float4 loads, warp reduction; error ~1e-7), ranks them by (distance, id)
+// and emits the top k — the FAISS semantics the oracle checks, at a cost of
+// nq * kc * d FMAs (negligible next to the GEMM).
+__global__ void __launch_bounds__(256) refine_fp32_kernel(const uint64_t* __restrict__ cand, int kc,
+                                                          const float* __restrict__ Q, const float* __restrict__ qn,
+                                                          const float* __restrict__ C, const float* __restrict__ cn,
+                                                          int64_t nq, int dim, int64_t id_base, int k,
+                                                          const rs_config* __restrict__ keep, float* __restrict__ D,
+                                                          int64_t* __restrict__ I, uint64_t* __restrict__ keys_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t q = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (q >= nq) return;
+  const float4* qv = reinterpret_cast<const float4*>(Q + q * dim);
+  const int d4 = dim / 4;
+  const float qq = qn[q];
+  // lane j owns candidates j and j + 32 (kc <= 40 < 64)
+  uint64_t mine[2] = {kEmptyKey, kEmptyKey};
+  for (int j = 0; j < kc; ++j) {
+    const uint64_t key = cand[q * kc + j];
+    if (key == kEmptyKey) break;  // sorted: the rest is padding
+    const int64_t row = int64_t(uint32_t(key)) - id_base;
+    const float4* cv = reinterpret_cast<const float4*>(C + row * dim);
+    float acc = 0.0f;
+    for (int i = lane; i < d4; i += 32) {
+      const float4 a = qv[i], b = cv[i];
+      acc = fmaf(a.x, b.x, acc);
+      acc = fmaf(a.y, b.y, acc);
+      acc = fmaf(a.z, b.z, acc);
+      acc = fmaf(a.w, b.w, acc);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    float dist = fmaf(-2.0f, acc, qq + cn[row]);
+    dist = dist > 0.0f ? dist : 0.0f;  // FAISS clamps round-off at 0 (and NaN -> 0)
+    const uint64_t ek = (uint64_t(__float_as_uint(dist)) << 32) | uint32_t(key);
+    if (j == lane) mine[0] = ek;
+    if (j == lane + 32) mine[1] = ek;
+  }
+  int limit = k;
+  if (keep) {
+    const rs_config c = keep[q];
+    limit = (c.status == RS_SELECT_BEST_FIT || c.status == RS_SELECT_FALLBACK) ? c.num_chunks : 0;
+    if (limit > k) limit = k;
+  }
+  // rank of each owned key among all candidates (keys are unique except padding)
+  int rank[2] = {0, 0};
+  for (int j = 0; j < 64; ++j) {
+    const uint64_t o = shfl_u64(mine[j >> 5], j & 31);
+#pragma unroll
+    for (int t = 0; t < 2; ++t) rank[t] += (o < mine[t] || (o == mine[t] && j < lane + 32 * t)) ? 1 : 0;
+  }
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    const int r = rank[t];
+    if (r < k) {
+      const bool real = mine[t] != kEmptyKey && r < limit;
+      if (keys_out) keys_out[q * k + r] = real ? mine[t] : kEmptyKey;
+      if (D) D[q * k + r] = real ? key_dist(mine[t]) : __int_as_float(0x7f800000);
+      if (I) I[q * k + r] = real ? int64_t(uint32_t(mine[t])) : int64_t(-1);
+    }
+  }
+}
+
+int launch_refine_fp32(const uint64_t* cand, int kc, const float* Q, const float* qn, const float* C,
+                       const float* cn, int64_t nq, int dim, int64_t id_base, int k, const rs_config* keep, float* D,
+                       int64_t* I, uint64_t* keys_out, cudaStream_t st) {
+  RS_REQUIRE(kc >= k && kc <= 64 && dim % 4 == 0, "refine: bad shape");
+  const int64_t blocks = ceil_div(nq * 32, 256);
+  refine_fp32_kernel<<<(unsigned)blocks, 256, 0, st>>>(cand, kc, Q, qn, C, cn, nq, dim, id_base, k, keep, D, I,
+                                                       keys_out);
+  RS_CHECK_LAUNCH("refine_fp32_kernel");
+  return RS_OK;
+}
+
 int launch_norms(const void* x, int64_t n, int dim, int dtype, float* out, cudaStream_t st,
                  float* max_out = nullptr) {
   if (n <= 0) return RS_OK;
@@ -317,6 +397,30 @@ int launch_simt(int dtype, const void* Q, const float* qn, int64_t nq, const voi
 
 }  // namespace
 
+// ---- 3xTF32 operand split ------------------------------------------------------
+__global__ void tf32_lo_kernel(const float4* __restrict__ x, int64_t n4, float4* __restrict__ lo) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += int64_t(gridDim.x) * blockDim.x) {
+    float4 v = x[i], r;
+    // the tensor core reads fp32 operands as tf32 by dropping the low 13
+    // mantissa bits; the residual below is exact in fp32
+    r.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xffffe000u);
+    r.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xffffe000u);
+    r.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xffffe000u);
+    r.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xffffe000u);
+    lo[i] = r;
+  }
+}
+
+int launch_tf32_lo(const float* x, int64_t count, float* lo, cudaStream_t st) {
+  if (count == 0) return RS_OK;
+  RS_REQUIRE(count % 4 == 0, "tf32 split needs a multiple of 4 elements");
+  const int64_t n4 = count / 4;
+  const unsigned blocks = unsigned(std::min<int64_t>(ceil_div(n4, 256), 148 * 16));
+  tf32_lo_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const float4*>(x), n4, reinterpret_cast<float4*>(lo));
+  RS_CHECK_LAUNCH("tf32_lo_kernel");
+  return RS_OK;
+}
+
 // ---- planner -----------------------------------------------------------------
 SearchPlan plan_search(int64_t nq, int64_t n, int bq, int bn, int ctas_capacity, int64_t row_bytes, bool share_l2) {
   SearchPlan best;
@@ -376,6 +480,11 @@ struct rs_index {
   float* norms = nullptr;
   float* norm_max = nullptr;  // device scalar: max squared norm over the shard
   int32_t* sched_counter = nullptr;  // pair kernel: [0] unit counter, [1 + s] frontier tile of segment s
+  float* lo = nullptr;        // fp32 index: [capacity, dim] tf32 residuals x - trunc_tf32(x) (3xTF32 path)
+  float* qlo = nullptr;       // per-search query residuals [qlo_cap, dim]
+  int64_t qlo_cap = 0;
+  uint64_t* cand = nullptr;   // fp32 path: merged 3xTF32 candidates [nq, kc] before the exact re-rank
+  size_t cand_cap = 0;        // bytes
   float* qnorm = nullptr;
   int64_t qnorm_cap = 0;
   uint64_t* part = nullptr;
@@ -393,6 +502,12 @@ namespace {
 size_t esize(int dtype) { return dtype == RS_BF16 ? 2 : 4; }
 
 int ensure_ws(rs_index* ix, int64_t nq, size_t part_bytes) {
+  if (ix->dtype == RS_F32 && nq > ix->qlo_cap) {
+    if (ix->qlo) cudaFree(ix->qlo);
+    ix->qlo = nullptr;
+    RS_CHECK_CUDA(cudaMalloc(&ix->qlo, sizeof(float) * size_t(nq) * ix->dim), "cudaMalloc(query tf32 residuals)");
+    ix->qlo_cap = nq;
+  }
   if (nq > ix->qnorm_cap) {
     if (ix->qnorm) cudaFree(ix->qnorm);
     ix->qnorm = nullptr;
@@ -421,19 +536,23 @@ struct DeviceGuard {
   }
 };
 
-// Concrete kernel for a search: the CTA-pair tcgen05 kernel for bf16 (default),
-// the single-CTA tcgen05 kernel on request, else the CUDA-core kernel.
+// Concrete kernel for a search: the CTA-pair tcgen05 kernel (default; bf16,
+// or 3xTF32 for an fp32 corpus), the single-CTA tcgen05 kernel on request
+// (bf16), else the CUDA-core kernel (k > 40, odd dims, or on request).
 int choose_algo(const rs_index* ix, int k) {
-  const bool tc_ok = ix->dtype == RS_BF16 && ix->dim % 8 == 0 && k <= rs::kTcMaxK;
+  const bool tc_ok = k <= rs::kTcMaxK && (ix->dtype == RS_BF16 ? ix->dim % 8 == 0 : ix->dim % 4 == 0);
   if (ix->algo == RS_ALGO_SIMT || !tc_ok) return RS_ALGO_SIMT;
-  return ix->algo == RS_ALGO_TCGEN05_1SM ? RS_ALGO_TCGEN05_1SM : RS_ALGO_TCGEN05;
+  if (ix->algo == RS_ALGO_TCGEN05_1SM && ix->dtype == RS_BF16) return RS_ALGO_TCGEN05_1SM;
+  return RS_ALGO_TCGEN05;
 }
 
 rs::SearchPlan make_plan(const rs_index* ix, int algo, int64_t nq, int64_t n, int k) {
   using namespace rs;
   const int sms = sm_count(ix->device);
   if (algo == RS_ALGO_TCGEN05) {  // units of one cluster: kPairGroup pairs x 256 queries
-    SearchPlan p = plan_search(nq, n, 2 * kTcBM * kPairGroup, kTcBN, sms / (2 * kPairGroup), int64_t(ix->dim) * 2,
+    // tile cost in bf16-equivalent K: 3 tf32 passes at half the bf16 rate
+    const int64_t eq_row_bytes = int64_t(ix->dim) * 2 * (ix->dtype == RS_BF16 ? 1 : 6);
+    SearchPlan p = plan_search(nq, n, 2 * kTcBM * kPairGroup, kTcBN, sms / (2 * kPairGroup), eq_row_bytes,
                                /*share_l2=*/false);
     p.lists_per_seg = kPairEpiGroups;
     return p;
@@ -449,7 +568,8 @@ int run_partial(rs_index* ix, const void* queries, int64_t nq, int k, int64_t id
   using namespace rs;
   const int algo = choose_algo(ix, k);
   RS_REQUIRE(!((ix->algo == RS_ALGO_TCGEN05 || ix->algo == RS_ALGO_TCGEN05_1SM) && algo == RS_ALGO_SIMT),
-             "tcgen05 path needs bf16, dim %% 8 == 0 and k <= %d", kTcMaxK);
+             "tcgen05 path needs 16-byte rows (bf16 dim %% 8, fp32 dim %% 4) and k <= %d", kTcMaxK);
+  RS_REQUIRE(!(ix->algo == RS_ALGO_TCGEN05_1SM && ix->dtype != RS_BF16), "the single-CTA tcgen05 kernel is bf16-only");
   const SearchPlan plan = make_plan(ix, algo, nq, ix->ntotal, k);
   const size_t part_bytes = size_t(nq) * plan.lists() * k * sizeof(uint64_t);
   int rc = ensure_ws(ix, nq, part_bytes);
@@ -466,13 +586,24 @@ int run_partial(rs_index* ix, const void* queries, int64_t nq, int k, int64_t id
   }
   if (algo != RS_ALGO_SIMT) {
     const bool pair = algo == RS_ALGO_TCGEN05;
-    CUtensorMap tmq, tmc;
-    rc = encode_kmajor_bf16_map(&tmq, queries, nq, ix->dim, kTcBM);
+    const bool tf = ix->dtype == RS_F32;
+    CUtensorMap tmq, tmc, tmql, tmcl;
+    const int crows = pair ? kTcBN / 2 / kPairGroup : kTcBN;
+    rc = encode_kmajor_map(&tmq, queries, nq, ix->dim, kTcBM, ix->dtype);
     if (rc) return rc;
-    rc = encode_kmajor_bf16_map(&tmc, ix->data, ix->ntotal, ix->dim, pair ? kTcBN / 2 / kPairGroup : kTcBN);
+    rc = encode_kmajor_map(&tmc, ix->data, ix->ntotal, ix->dim, crows, ix->dtype);
     if (rc) return rc;
-    rc = pair ? launch_score_topk_pair(tmq, tmc, ix->qnorm, ix->norms, nq, ix->ntotal, ix->dim, k, id_base, plan,
-                                       ix->part, ix->sched_counter, ix->walk_bias, st)
+    if (tf) {  // 3xTF32: the queries' residuals (the corpus's were made at add)
+      rc = launch_tf32_lo(static_cast<const float*>(queries), nq * ix->dim, ix->qlo, st);
+      if (rc) return rc;
+      rc = encode_kmajor_map(&tmql, ix->qlo, nq, ix->dim, kTcBM, RS_F32);
+      if (rc) return rc;
+      rc = encode_kmajor_map(&tmcl, ix->lo, ix->ntotal, ix->dim, crows, RS_F32);
+      if (rc) return rc;
+    }
+    rc = pair ? launch_score_topk_pair(tmq, tf ? &tmql : nullptr, tmc, tf ? &tmcl : nullptr, ix->qnorm, ix->norms,
+                                       nq, ix->ntotal, ix->dim, k, id_base, plan, ix->part, ix->sched_counter,
+                                       ix->walk_bias, st)
               : launch_score_topk_tc(tmq, tmc, ix->qnorm, ix->norms, nq, ix->ntotal, ix->dim, k, id_base, plan,
                                      ix->part, st);
   } else {
@@ -525,6 +656,7 @@ extern "C" int rs_index_create(int32_t dim, int32_t dtype, int64_t capacity, int
     if (e == cudaSuccess) e = cudaMalloc(&ix->norms, sizeof(float) * (capacity + rs::kTcBN));
     if (e == cudaSuccess) e = cudaMalloc(&ix->norm_max, sizeof(float));
     if (e == cudaSuccess) e = cudaMalloc(&ix->sched_counter, sizeof(int32_t) * (1 + rs::kMaxSegments));
+    if (e == cudaSuccess && dtype == RS_F32) e = cudaMalloc(&ix->lo, size_t(capacity) * dim * sizeof(float));
     if (e == cudaSuccess) e = cudaMemset(ix->norm_max, 0, sizeof(float));
     if (e != cudaSuccess) {
       rs::set_error("cudaMalloc(corpus %lld x %d): %s", (long long)capacity, dim, cudaGetErrorString(e));
@@ -571,6 +703,9 @@ extern "C" int rs_index_destroy(rs_index* ix) {
   cudaFree(ix->norms);
   cudaFree(ix->norm_max);
   cudaFree(ix->sched_counter);
+  cudaFree(ix->lo);
+  cudaFree(ix->qlo);
+  cudaFree(ix->cand);
   cudaFree(ix->qnorm);
   cudaFree(ix->part);
   delete ix;
@@ -593,6 +728,11 @@ extern "C" int rs_index_add(rs_index* ix, const void* emb, int64_t n, void* stre
   int rc = rs::launch_norms((char*)ix->data + size_t(ix->ntotal) * row, n, ix->dim, ix->dtype,
                             ix->norms + ix->ntotal, st, ix->norm_max);
   if (rc) return rc;
+  if (ix->dtype == RS_F32) {  // 3xTF32 residuals of the new rows
+    const size_t off = size_t(ix->ntotal) * ix->dim;
+    rc = rs::launch_tf32_lo(static_cast<const float*>(ix->data) + off, n * ix->dim, ix->lo + off, st);
+    if (rc) return rc;
+  }
   ix->ntotal += n;
   return RS_OK;
 }
@@ -667,6 +807,25 @@ static int search_impl(rs_index* ix, const void* queries, int64_t nq, int32_t k,
     return RS_OK;
   }
   SearchPlan plan;
+  if (ix->dtype == RS_F32 && choose_algo(ix, k) == RS_ALGO_TCGEN05) {
+    // 3xTF32 candidates (kc per query) -> exact fp32 re-rank to k
+    const int kc = std::min(k + kRefineExtra, kTcMaxK);
+    rc = run_partial(ix, queries, nq, kc, id_base, st, &plan);
+    if (rc) return rc;
+    const size_t cb = size_t(nq) * kc * sizeof(uint64_t);
+    if (cb > ix->cand_cap) {
+      if (ix->cand) cudaFree(ix->cand);
+      ix->cand = nullptr;
+      RS_CHECK_CUDA(cudaMalloc(&ix->cand, cb), "cudaMalloc(refine candidates)");
+      ix->cand_cap = cb;
+    }
+    rc = launch_merge(ix->part, nq, plan.lists(), kc, kc, int64_t(plan.lists()) * kc, kc, nullptr, nullptr, nullptr,
+                      ix->cand, st);
+    if (rc) return rc;
+    return launch_refine_fp32(ix->cand, kc, static_cast<const float*>(queries), ix->qnorm,
+                              static_cast<const float*>(ix->data), ix->norms, nq, ix->dim, id_base, k, keep, D, I,
+                              keys, st);
+  }
   rc = run_partial(ix, queries, nq, k, id_base, st, &plan);
   if (rc) return rc;
   return launch_merge(ix->part, nq, plan.lists(), k, /*list_stride=*/k, /*q_stride=*/int64_t(plan.lists()) * k, k,

@@ -32,6 +32,8 @@ SearchPlan plan_search(int64_t nq, int64_t n, int bq, int bn, int ctas_capacity,
 
 // tcgen05/TMA/TMEM bf16 kernel (score_topk_sm100.cu).
 constexpr int kTcMaxK = 40;
+// fp32 (3xTF32) path: extra candidates kept for the exact fp32 re-rank
+constexpr int kRefineExtra = 8;
 constexpr int kTcBM = 128;
 constexpr int kTcBN = 256;
 size_t tc_smem_bytes();
@@ -54,10 +56,16 @@ constexpr int kPairGroup = RS_PAIR_GROUP;
 #define RS_PAIR_EPI_GROUPS 1  // 2 measured no faster on B200 (and doubles the partial lists)
 #endif
 constexpr int kPairEpiGroups = RS_PAIR_EPI_GROUPS;
-int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap& tmc, const float* qn, const float* cn,
-                           int64_t nq, int64_t n, int dim, int k, int64_t id_base, const SearchPlan& plan,
-                           uint64_t* part, int32_t* counter, int32_t walk_bias, cudaStream_t st);
+// tmql / tmcl: the fp32 path's lo maps (3xTF32), NULL for bf16.
+int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap* tmql, const CUtensorMap& tmc,
+                           const CUtensorMap* tmcl, const float* qn, const float* cn, int64_t nq, int64_t n, int dim,
+                           int k, int64_t id_base, const SearchPlan& plan, uint64_t* part, int32_t* counter,
+                           int32_t walk_bias, cudaStream_t st);
 int encode_kmajor_bf16_map(CUtensorMap* map, const void* base, int64_t rows, int dim, int box_rows);
+// dtype RS_BF16 or RS_F32: 128-byte boxes (64 bf16 / 32 fp32) x box_rows, SWIZZLE_128B.
+int encode_kmajor_map(CUtensorMap* map, const void* base, int64_t rows, int dim, int box_rows, int dtype);
+// 3xTF32 operand split: lo[i] = x[i] - trunc_tf32(x[i]) (exact in fp32).
+int launch_tf32_lo(const float* x, int64_t count, float* lo, cudaStream_t st);
 
 // CUDA-core kernel for fp32 (and bf16 cross-checks), retrieval.cu.
 constexpr int kSimtBQ = 64;

@@ -272,26 +272,33 @@ EncodeTiledFn get_encode_fn() {
 
 size_t tc_smem_bytes() { return SMEM_BYTES; }
 
-int encode_kmajor_bf16_map(CUtensorMap* map, const void* base, int64_t rows, int dim, int box_rows) {
+int encode_kmajor_map(CUtensorMap* map, const void* base, int64_t rows, int dim, int box_rows, int dtype) {
   EncodeTiledFn fn = get_encode_fn();
   if (!fn) {
     set_error("cuTensorMapEncodeTiled unavailable");
     return RS_ERR_UNSUPPORTED;
   }
-  RS_REQUIRE(dim % 8 == 0, "bf16 TMA path needs dim %% 8 == 0 (16-byte rows), got %d", dim);
+  const int es = dtype == RS_BF16 ? 2 : 4;
+  RS_REQUIRE((int64_t(dim) * es) % 16 == 0, "TMA path needs 16-byte rows (dim %d)", dim);
   RS_REQUIRE((reinterpret_cast<uintptr_t>(base) & 15) == 0, "embedding base must be 16-byte aligned");
   const cuuint64_t dims[2] = {cuuint64_t(dim), cuuint64_t(rows > 0 ? rows : 1)};
-  const cuuint64_t strides[1] = {cuuint64_t(dim) * 2};
-  const cuuint32_t box[2] = {BK, cuuint32_t(box_rows)};
+  const cuuint64_t strides[1] = {cuuint64_t(dim) * es};
+  // one 128-byte (SWIZZLE_128B) row per k-block: 64 bf16 or 32 fp32 elements
+  const cuuint32_t box[2] = {cuuint32_t(128 / es), cuuint32_t(box_rows)};
   const cuuint32_t estr[2] = {1, 1};
-  const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  const CUresult r = fn(map, dtype == RS_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                        const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled failed (%d)", int(r));
     return RS_ERR_CUDA;
   }
   return RS_OK;
+}
+
+int encode_kmajor_bf16_map(CUtensorMap* map, const void* base, int64_t rows, int dim, int box_rows) {
+  return encode_kmajor_map(map, base, rows, dim, box_rows, RS_BF16);
 }
 
 int launch_score_topk_tc(const CUtensorMap& tmq, const CUtensorMap& tmc, const float* qn, const float* cn,

@@ -57,17 +57,18 @@ constexpr int BM = 128;         // query rows per CTA (TMEM lanes)
 constexpr int PM = 2 * BM;      // query rows per pair tile
 constexpr int BN = kTcBN;       // corpus columns per tile (both CTAs)
 constexpr int HB = BN / 2;      // corpus rows staged per CTA
-constexpr int BK = 64;
-constexpr int STAGES = RS_PAIR_STAGES;
+#ifndef RS_PAIR_STAGES_TF32
+#define RS_PAIR_STAGES_TF32 3
+#endif
 constexpr int KREG = kTcMaxK;   // register top-k capacity (k <= 40)
 // candidate buffer per row; a warp flushes when one of its lanes holds more
 // than BUF - CHECK entries, so every flush batches many candidates per lane
 constexpr int BUF = RS_PAIR_BUF;
 constexpr int CHECK = 8;
 constexpr int EPI_COLS = 32;    // TMEM columns per tcgen05.ld / wait
-constexpr int A_BYTES = BM * BK * 2;
-constexpr int B_BYTES = HB * BK * 2;
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int ROW_BYTES = 128;  // one SWIZZLE_128B row of a k-block (64 bf16 / 32 fp32)
+constexpr int A_BYTES = BM * ROW_BYTES;
+constexpr int B_BYTES = HB * ROW_BYTES;
 constexpr int TMEM_COLS = 2 * BN;
 constexpr int EG = kPairEpiGroups;       // epilogue warp groups (column slices)
 constexpr int CPG = BN / EG;             // tile columns per epilogue group
@@ -100,11 +101,11 @@ constexpr int URING = 4;        // unit-id ring depth
 // and every producer except the scheduling one (cluster rank 0)
 constexpr uint32_t UCONSUMERS = (2 + 4 * EG) * CL - 1;
 static_assert(HB % G == 0 && BPIECE % 8 == 0, "corpus piece must be whole swizzle atoms");
-constexpr uint32_t IDESC = umma_idesc_bf16_f32(PM, BN);
 
-struct __align__(8) SmemTail {
-  uint64_t full[STAGES];
-  uint64_t empty[STAGES];
+template <int S>
+struct __align__(8) SmemTailT {
+  uint64_t full[S];
+  uint64_t empty[S];
   uint64_t tfull[2];
   uint64_t tempty[2];
   uint64_t ufull[URING];
@@ -114,11 +115,30 @@ struct __align__(8) SmemTail {
   uint32_t tmem_base;
 };
 
-constexpr size_t OFF_BUF = size_t(STAGES) * STAGE_BYTES;
-constexpr size_t OFF_CN = OFF_BUF + size_t(BUF) * EPI_THREADS * 8;
-constexpr size_t OFF_TAIL = OFF_CN + 2 * BN * sizeof(float);
-constexpr size_t SMEM_BYTES = OFF_TAIL + sizeof(SmemTail);
-static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
+// Operand precision.  bf16: one kind::f16 MMA per 16-element k-step.  fp32
+// (TF = true, "3xTF32"): each operand x is fed as hi = x (the tensor core
+// reads the top 19 bits, i.e. tf32 truncation) and lo = x - trunc_tf32(x)
+// (exact in fp32, precomputed: the corpus at add(), the queries per search),
+// and every 8-element k-step issues lo*hi + hi*lo + hi*hi into the same fp32
+// TMEM accumulator.  The accumulator's truncating adds leave ~1e-5 relative
+// error on large dots at d = 768, so the fp32 search keeps k + 8 candidates
+// and re-ranks them exactly (refine_fp32_kernel, retrieval.cu).
+template <bool TF>
+struct Cfg {
+  static constexpr int BK = TF ? 32 : 64;  // elements per k-block (one 128-byte row)
+  static constexpr int NT = TF ? 2 : 1;    // tiles per operand per stage (hi, lo)
+  static constexpr int STAGES = TF ? RS_PAIR_STAGES_TF32 : RS_PAIR_STAGES;
+  static constexpr int STAGE_BYTES = NT * (A_BYTES + B_BYTES);
+  static constexpr int OFF_B = NT * A_BYTES;  // stage layout: A hi | [A lo] | B hi | [B lo]
+  static constexpr uint32_t IDESC = TF ? umma_idesc_tf32_f32(PM, BN) : umma_idesc_bf16_f32(PM, BN);
+  using Tail = SmemTailT<STAGES>;
+  static constexpr size_t OFF_BUF = size_t(STAGES) * STAGE_BYTES;
+  static constexpr size_t OFF_CN = OFF_BUF + size_t(BUF) * EPI_THREADS * 8;
+  static constexpr size_t OFF_TAIL = OFF_CN + 2 * BN * sizeof(float);
+  static constexpr size_t SMEM_BYTES = OFF_TAIL + sizeof(Tail);
+  static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
+  static_assert(!TF || G == 1, "tf32 path has no multicast variant");
+};
 
 using TopK = RegTopK<KREG, EPI_THREADS, BUF>;
 
@@ -171,12 +191,14 @@ struct TileWalk {
 
 // Consumer side of the unit ring: wait for slot i, read the unit id, release
 // the slot to the leader's producer.  Returns the unit (-1 = no more work).
+template <class SmemTail>
 __device__ __forceinline__ void release_unit(SmemTail* tail, uint32_t i, bool scheduler) {
   if (scheduler)
     mbar_arrive(&tail->uempty[i % URING]);
   else
     mbar_arrive_cluster(mapa_shared(smem_u32(&tail->uempty[i % URING]), 0));
 }
+template <class SmemTail>
 __device__ __forceinline__ int next_unit(SmemTail* tail, uint32_t i, bool scheduler, bool arrive, int32_t& start) {
   const int slot = int(i % URING);
   mbar_wait_cluster(&tail->ufull[slot], (i / URING) & 1);
@@ -203,14 +225,19 @@ __device__ unsigned long long g_pair_prof[1024][8];
 #define PROF(slot, stmt) stmt
 #endif
 
+template <bool TF>
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
-    score_topk_pair_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmc,
+    score_topk_pair_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmql,
+                           const __grid_constant__ CUtensorMap tmc, const __grid_constant__ CUtensorMap tmcl,
                            const Params p) {
+  using C = Cfg<TF>;
+  using SmemTail = typename C::Tail;
+  constexpr int STAGES = C::STAGES;
   // no static shared memory: the dynamic window starts at the CTA's shared
   // base, 1024-aligned as SWIZZLE_128B requires
   extern __shared__ __align__(1024) uint8_t smem[];
-  SmemTail* tail = reinterpret_cast<SmemTail*>(smem + OFF_TAIL);
-  float* cns = reinterpret_cast<float*>(smem + OFF_CN);
+  SmemTail* tail = reinterpret_cast<SmemTail*>(smem + C::OFF_TAIL);
+  float* cns = reinterpret_cast<float*>(smem + C::OFF_CN);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -226,6 +253,10 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   if (warp == WARP_PROD && lane == 0) {
     tma_prefetch_desc(&tmq);
     tma_prefetch_desc(&tmc);
+    if (TF) {
+      tma_prefetch_desc(&tmql);
+      tma_prefetch_desc(&tmcl);
+    }
   }
   if (warp == WARP_MMA && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -304,26 +335,30 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           if (scheduler) red_max_relaxed_gpu_s32(p.seg_pos + seg, start + int32_t(j));
           for (int kb = 0; kb < p.kblocks; ++kb) {
             PROF(0, mbar_wait(&tail->empty[stage], phase ^ 1));
-            uint8_t* sa = smem + size_t(stage) * STAGE_BYTES;
+            uint8_t* sa = smem + size_t(stage) * C::STAGE_BYTES;
             const uint32_t full_leader = mapa_shared(smem_u32(&tail->full[stage]), pair_leader);
 #ifdef RS_PAIR_NO_TMA  // timing experiment only: MMA pipeline with no operand traffic
             (void)sa;
             (void)full_leader;
             if (leader) mbar_arrive(&tail->full[stage]);
 #else
-            if (leader) mbar_arrive_expect_tx(&tail->full[stage], 2 * STAGE_BYTES);
-            tma_load_2d_pair(&tmq, full_leader, sa, kb * BK, qt * PM + int(half) * BM, pol_q);
+            if (leader) mbar_arrive_expect_tx(&tail->full[stage], 2 * C::STAGE_BYTES);
+            const int32_t kx = kb * C::BK;
+            const int32_t qrow0 = qt * PM + int(half) * BM;
+            tma_load_2d_pair(&tmq, full_leader, sa, kx, qrow0, pol_q);
+            if (TF) tma_load_2d_pair(&tmql, full_leader, sa + A_BYTES, kx, qrow0, pol_q);
             if (G == 1) {
 #ifdef RS_EXP_L2_CORPUS_ROWS  // timing experiment only (wrong results): corpus reads wrap in an L2-sized window
-              tma_load_2d_pair(&tmc, full_leader, sa + A_BYTES, kb * BK,
-                               int32_t(c0 % RS_EXP_L2_CORPUS_ROWS) + int(half) * HB, pol_c);
+              const int32_t crow0 = int32_t(c0 % RS_EXP_L2_CORPUS_ROWS) + int(half) * HB;
 #else
-              tma_load_2d_pair(&tmc, full_leader, sa + A_BYTES, kb * BK, int32_t(c0) + int(half) * HB, pol_c);
+              const int32_t crow0 = int32_t(c0) + int(half) * HB;
 #endif
+              tma_load_2d_pair(&tmc, full_leader, sa + C::OFF_B, kx, crow0, pol_c);
+              if (TF) tma_load_2d_pair(&tmcl, full_leader, sa + C::OFF_B + B_BYTES, kx, crow0, pol_c);
             } else {
               // piece pp of this half's corpus rows, written into the same smem
               // offset of every CTA holding this half in the cluster's G pairs
-              tma_load_2d_pair_mc(&tmc, full_leader, sa + A_BYTES + pp * BPIECE * BK * 2, kb * BK,
+              tma_load_2d_pair_mc(&tmc, full_leader, sa + C::OFF_B + pp * BPIECE * ROW_BYTES, kx,
                                   int32_t(c0) + int(half) * HB + pp * BPIECE, mc_half, pol_c);
             }
 #endif
@@ -368,12 +403,20 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           for (int kb = 0; kb < p.kblocks; ++kb) {
             PROF(2, mbar_wait(&tail->full[stage], phase));
             tc_fence_after();
-            const uint32_t a_addr = smem_u32(smem + size_t(stage) * STAGE_BYTES);
-            const uint32_t b_addr = a_addr + A_BYTES;
+            const uint32_t a_addr = smem_u32(smem + size_t(stage) * C::STAGE_BYTES);
+            const uint32_t b_addr = a_addr + C::OFF_B;
 #pragma unroll
-            for (int kk = 0; kk < BK / 16; ++kk) {
-              umma_bf16_ss_pair(d_tmem, umma_desc_sw128(a_addr + kk * 32), umma_desc_sw128(b_addr + kk * 32),
-                                IDESC, (kb | kk) != 0);
+            for (int kk = 0; kk < 4; ++kk) {  // 4 MMA k-steps of 32 bytes per 128-byte k-block
+              if constexpr (!TF) {
+                umma_bf16_ss_pair(d_tmem, umma_desc_sw128(a_addr + kk * 32), umma_desc_sw128(b_addr + kk * 32),
+                                  C::IDESC, (kb | kk) != 0);
+              } else {
+                const uint64_t ahi = umma_desc_sw128(a_addr + kk * 32), alo = umma_desc_sw128(a_addr + A_BYTES + kk * 32);
+                const uint64_t bhi = umma_desc_sw128(b_addr + kk * 32), blo = umma_desc_sw128(b_addr + B_BYTES + kk * 32);
+                umma_tf32_ss_pair(d_tmem, alo, bhi, C::IDESC, (kb | kk) != 0);  // small terms first
+                umma_tf32_ss_pair(d_tmem, ahi, blo, C::IDESC, 1);
+                umma_tf32_ss_pair(d_tmem, ahi, bhi, C::IDESC, 1);
+              }
             }
             umma_commit_pair_mc(&tail->empty[stage], uint16_t((1u << CL) - 1u));  // every CTA of the cluster
             if (++stage == STAGES) {
@@ -393,7 +436,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     const int et = (warp - EPI_WARP0) * 32 + lane;
     TopK rt;
     rt.k = p.k;
-    rt.wbase = smem_u32(smem + OFF_BUF) + uint32_t(et) * 8u;
+    rt.wbase = smem_u32(smem + C::OFF_BUF) + uint32_t(et) * 8u;
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tail->tempty[0]), pair_leader);
     const uint32_t tempty_leader1 = mapa_shared(smem_u32(&tail->tempty[1]), pair_leader);
     uint32_t tile_iter = 0;
@@ -491,15 +534,23 @@ extern "C" int rs_debug_pair_profile_reset() {
 }
 #endif
 
-int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap& tmc, const float* qn, const float* cn,
-                           int64_t nq, int64_t n, int dim, int k, int64_t id_base, const SearchPlan& plan,
-                           uint64_t* part, int32_t* counter, int32_t walk_bias, cudaStream_t st) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    RS_CHECK_CUDA(cudaFuncSetAttribute(score_topk_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       int(SMEM_BYTES)),
-                  "cudaFuncSetAttribute(score_topk_pair_kernel)");
-    attr_set = true;
+int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap* tmql, const CUtensorMap& tmc,
+                           const CUtensorMap* tmcl, const float* qn, const float* cn, int64_t nq, int64_t n, int dim,
+                           int k, int64_t id_base, const SearchPlan& plan, uint64_t* part, int32_t* counter,
+                           int32_t walk_bias, cudaStream_t st) {
+  const bool tf = tmql != nullptr;
+  RS_REQUIRE(tf == (tmcl != nullptr), "tf32 path needs both lo maps");
+  static bool attr_set[2] = {false, false};
+  if (!attr_set[tf]) {
+    if (tf)
+      RS_CHECK_CUDA(cudaFuncSetAttribute(score_topk_pair_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(Cfg<true>::SMEM_BYTES)),
+                    "cudaFuncSetAttribute(score_topk_pair_kernel<tf32>)");
+    else
+      RS_CHECK_CUDA(cudaFuncSetAttribute(score_topk_pair_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(Cfg<false>::SMEM_BYTES)),
+                    "cudaFuncSetAttribute(score_topk_pair_kernel<bf16>)");
+    attr_set[tf] = true;
   }
   RS_REQUIRE(plan.segments >= 1 && plan.segments <= kMaxSegments, "segments out of range (%d)", plan.segments);
   RS_CHECK_CUDA(cudaMemsetAsync(counter, 0, sizeof(int32_t) * (1 + plan.segments), st),
@@ -509,7 +560,8 @@ int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap& tmc, const
   p.cn = cn;
   p.nq = nq;
   p.n = n;
-  p.kblocks = (dim + BK - 1) / BK;
+  const int bk = tf ? Cfg<true>::BK : Cfg<false>::BK;
+  p.kblocks = (dim + bk - 1) / bk;
   p.k = k;
   p.id_base = id_base;
   // the plan counts cluster units (256*G query rows); the kernel works in
@@ -522,7 +574,10 @@ int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap& tmc, const
   p.seg_pos = counter + 1;
   p.walk_bias = walk_bias;
   p.cunits = int64_t(plan.qtiles) * plan.segments;
-  score_topk_pair_kernel<<<CL * plan.ctas, NUM_THREADS, SMEM_BYTES, st>>>(tmq, tmc, p);
+  if (tf)
+    score_topk_pair_kernel<true><<<CL * plan.ctas, NUM_THREADS, Cfg<true>::SMEM_BYTES, st>>>(tmq, *tmql, tmc, *tmcl, p);
+  else
+    score_topk_pair_kernel<false><<<CL * plan.ctas, NUM_THREADS, Cfg<false>::SMEM_BYTES, st>>>(tmq, tmq, tmc, tmc, p);
   RS_CHECK_LAUNCH("score_topk_pair_kernel");
   return RS_OK;
 }

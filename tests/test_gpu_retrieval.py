@@ -85,9 +85,36 @@ def test_pair_and_single_cta_kernels_agree():
 @pytest.mark.parametrize("nq,n,d,k", SHAPES[:6])
 def test_simt_fp32_matches_oracle(nq, n, d, k):
     q, c = make_data(nq, n, d, torch.float32, seed=7 + nq)
-    D, I, plan = run_search(q, c, k)
+    D, I, plan = run_search(q, c, k, algo="simt")
     assert plan["algo"] == "simt"
     assert_parity(q, c, k, D, I, torch.float32)
+
+
+@pytest.mark.parametrize("nq,n,d,k", SHAPES + [(1000, 100_000, 768, 35)])
+def test_tf32x3_fp32_matches_oracle(nq, n, d, k):
+    """fp32 corpus on the tensor cores (3xTF32 split, CTA-pair kernel) within
+    the north star's fp32 tolerance (1e-5 relative)."""
+    q, c = make_data(nq, n, d, torch.float32, seed=9 + nq)
+    D, I, plan = run_search(q, c, k)
+    assert plan["algo"] == "tcgen05"
+    assert_parity(q, c, k, D, I, torch.float32)
+
+
+def test_tf32x3_ties_and_wrapped_walk():
+    nq, n, d, k, base = 600, 120_000, 128, 35, 60_001
+    q, c = make_data(nq, n, d, torch.float32, seed=4)
+    c[base::97] = c[base]
+    q[:8] = c[base]
+    ix = IndexFlatL2(d, dtype=torch.float32, capacity=n)
+    ix.set_walk_bias(3)
+    ix.add(c.cuda())
+    D, I = ix.search(q.cuda(), k)
+    torch.cuda.synchronize()
+    ix.close()
+    D, I = D.cpu().numpy(), I.cpu().numpy()
+    for r in range(8):
+        np.testing.assert_array_equal(I[r], base + 97 * np.arange(k))
+    assert_parity(q[:100], c, k, D[:100], I[:100], torch.float32)
 
 
 def test_simt_bf16_and_large_k():

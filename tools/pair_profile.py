@@ -34,17 +34,18 @@ def main(n=2_000_000, nq=8192, d=1024):
     a = a[:ctas]
     # slot 7 = kernel cycles from warps 0, 1 and the 4 epilogue warps (each /4);
     # warps 2, 3 finish immediately and add ~0
-    names = {0: "producer wait empty", 1: "mma wait tempty", 3: "epilogue wait tfull (4 warps)",
-             5: "epilogue finish (4 warps)", 6: "epilogue TMEM ld wait (4 warps)",
-             2: "epilogue flush + mma wait full"}
+    names = {0: "producer wait empty (ring full)", 1: "mma wait tempty (epilogue-bound)",
+             2: "mma wait full (operand-bound)", 3: "epilogue wait tfull (4 warps)",
+             5: "epilogue final flush (4 warps)"}
     for label, rows in (("leader", a[0::2]), ("peer", a[1::2])):
         total = rows[:, 7] / 3.0  # warps: producer, mma, 4 epilogue (/4)
-        print(f"{label}: kernel {total.mean() / 1e6:.2f} Mcycles; flushes/warp {rows[:, 4].mean() / 4:.0f}")
+        print(f"{label}: kernel {total.mean() / 1e6:.2f} Mcycles")
         for i, nm in names.items():
-            denom = total * (4 if i in (3, 5, 6) else 1)
-            print(f"   {nm:32s} {100 * (rows[:, i] / denom).mean():5.1f}%")
+            denom = total * (4 if i in (3, 5) else 1)
+            print(f"   {nm:34s} {100 * (rows[:, i] / denom).mean():5.1f}%")
     print(plan)
 
 
 if __name__ == "__main__":
-    main()
+    args = [int(x) for x in sys.argv[1:4]]
+    main(*args)
