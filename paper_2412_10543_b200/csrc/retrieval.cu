@@ -421,6 +421,29 @@ int launch_tf32_lo(const float* x, int64_t count, float* lo, cudaStream_t st) {
   return RS_OK;
 }
 
+// ---- per-chunk norm minima (the pair kernel's dot bound) ------------------------
+__global__ void chunk_min_kernel(const float* __restrict__ norms, int64_t c_lo, int64_t c_hi, int64_t r1,
+                                 float* __restrict__ cmin) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t c = c_lo + ((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5); c < c_hi;
+       c += (int64_t(gridDim.x) * blockDim.x) >> 5) {
+    const int64_t r = c * 32 + lane;
+    float v = r < r1 ? norms[r] : __int_as_float(0x7f800000);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, off));
+    if (lane == 0) cmin[c] = v;
+  }
+}
+
+int launch_chunk_min(const float* norms, int64_t r0, int64_t r1, float* cmin, cudaStream_t st) {
+  if (r1 <= r0) return RS_OK;
+  const int64_t c_lo = r0 / 32, c_hi = ceil_div(r1, 32);
+  const int64_t blocks = std::min<int64_t>(ceil_div((c_hi - c_lo) * 32, 256), 148 * 16);
+  chunk_min_kernel<<<(unsigned)blocks, 256, 0, st>>>(norms, c_lo, c_hi, r1, cmin);
+  RS_CHECK_LAUNCH("chunk_min_kernel");
+  return RS_OK;
+}
+
 // ---- planner -----------------------------------------------------------------
 SearchPlan plan_search(int64_t nq, int64_t n, int bq, int bn, int ctas_capacity, int64_t row_bytes, bool share_l2) {
   SearchPlan best;
@@ -480,6 +503,7 @@ struct rs_index {
   float* norms = nullptr;
   float* norm_max = nullptr;  // device scalar: max squared norm over the shard
   int32_t* sched_counter = nullptr;  // pair kernel: [0] unit counter, [1 + s] frontier tile of segment s
+  float* cmin = nullptr;      // [ceil(capacity/256)*8 + 8]: min squared norm per 32-row chunk
   float* lo = nullptr;        // fp32 index: [capacity, dim] tf32 residuals x - trunc_tf32(x) (3xTF32 path)
   float* qlo = nullptr;       // per-search query residuals [qlo_cap, dim]
   int64_t qlo_cap = 0;
@@ -602,8 +626,8 @@ int run_partial(rs_index* ix, const void* queries, int64_t nq, int k, int64_t id
       if (rc) return rc;
     }
     rc = pair ? launch_score_topk_pair(tmq, tf ? &tmql : nullptr, tmc, tf ? &tmcl : nullptr, ix->qnorm, ix->norms,
-                                       nq, ix->ntotal, ix->dim, k, id_base, plan, ix->part, ix->sched_counter,
-                                       ix->walk_bias, st)
+                                       ix->cmin, nq, ix->ntotal, ix->dim, k, id_base, plan, ix->part,
+                                       ix->sched_counter, ix->walk_bias, st)
               : launch_score_topk_tc(tmq, tmc, ix->qnorm, ix->norms, nq, ix->ntotal, ix->dim, k, id_base, plan,
                                      ix->part, st);
   } else {
@@ -657,6 +681,7 @@ extern "C" int rs_index_create(int32_t dim, int32_t dtype, int64_t capacity, int
     if (e == cudaSuccess) e = cudaMalloc(&ix->norm_max, sizeof(float));
     if (e == cudaSuccess) e = cudaMalloc(&ix->sched_counter, sizeof(int32_t) * (1 + rs::kMaxSegments));
     if (e == cudaSuccess && dtype == RS_F32) e = cudaMalloc(&ix->lo, size_t(capacity) * dim * sizeof(float));
+    if (e == cudaSuccess) e = cudaMalloc(&ix->cmin, sizeof(float) * (rs::ceil_div(capacity, 256) * 8 + 8));
     if (e == cudaSuccess) e = cudaMemset(ix->norm_max, 0, sizeof(float));
     if (e != cudaSuccess) {
       rs::set_error("cudaMalloc(corpus %lld x %d): %s", (long long)capacity, dim, cudaGetErrorString(e));
@@ -704,6 +729,7 @@ extern "C" int rs_index_destroy(rs_index* ix) {
   cudaFree(ix->norm_max);
   cudaFree(ix->sched_counter);
   cudaFree(ix->lo);
+  cudaFree(ix->cmin);
   cudaFree(ix->qlo);
   cudaFree(ix->cand);
   cudaFree(ix->qnorm);
@@ -727,6 +753,8 @@ extern "C" int rs_index_add(rs_index* ix, const void* emb, int64_t n, void* stre
                 "cudaMemcpyAsync(add)");
   int rc = rs::launch_norms((char*)ix->data + size_t(ix->ntotal) * row, n, ix->dim, ix->dtype,
                             ix->norms + ix->ntotal, st, ix->norm_max);
+  if (rc) return rc;
+  rc = rs::launch_chunk_min(ix->norms, ix->ntotal, ix->ntotal + n, ix->cmin, st);
   if (rc) return rc;
   if (ix->dtype == RS_F32) {  // 3xTF32 residuals of the new rows
     const size_t off = size_t(ix->ntotal) * ix->dim;

@@ -58,9 +58,12 @@ constexpr int kPairGroup = RS_PAIR_GROUP;
 constexpr int kPairEpiGroups = RS_PAIR_EPI_GROUPS;
 // tmql / tmcl: the fp32 path's lo maps (3xTF32), NULL for bf16.
 int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap* tmql, const CUtensorMap& tmc,
-                           const CUtensorMap* tmcl, const float* qn, const float* cn, int64_t nq, int64_t n, int dim,
-                           int k, int64_t id_base, const SearchPlan& plan, uint64_t* part, int32_t* counter,
-                           int32_t walk_bias, cudaStream_t st);
+                           const CUtensorMap* tmcl, const float* qn, const float* cn, const float* cmin, int64_t nq,
+                           int64_t n, int dim, int k, int64_t id_base, const SearchPlan& plan, uint64_t* part,
+                           int32_t* counter, int32_t walk_bias, cudaStream_t st);
+// per 32-row chunk minimum of the squared norms over rows [r0, r1) of a shard
+// (recomputes every chunk the range touches)
+int launch_chunk_min(const float* norms, int64_t r0, int64_t r1, float* cmin, cudaStream_t st);
 int encode_kmajor_bf16_map(CUtensorMap* map, const void* base, int64_t rows, int dim, int box_rows);
 // dtype RS_BF16 or RS_F32: 128-byte boxes (64 bf16 / 32 fp32) x box_rows, SWIZZLE_128B.
 int encode_kmajor_map(CUtensorMap* map, const void* base, int64_t rows, int dim, int box_rows, int dtype);

@@ -145,6 +145,7 @@ using TopK = RegTopK<KREG, EPI_THREADS, BUF>;
 struct Params {
   const float* qn;
   const float* cn;
+  const float* cmin;  // per 32-row chunk of the shard: min squared norm (the epilogue's dot bound)
   int64_t nq, n;
   int32_t kblocks;
   int32_t k;
@@ -464,6 +465,9 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         const uint32_t acc = tile_iter & 1;
         const int valid = int(r1 - c0 < BN ? r1 - c0 : BN);
         const float* cn_t = cns + acc * BN;
+        // the tile's eight 32-column norm minima, loaded before the wait
+        const float4 cm0 = __ldg(reinterpret_cast<const float4*>(p.cmin + (c0 >> 5)));
+        const float4 cm1 = __ldg(reinterpret_cast<const float4*>(p.cmin + (c0 >> 5)) + 1);
         PROF(3, mbar_wait(&tail->tfull[acc], (tile_iter >> 1) & 1));
         tc_fence_after();
         const uint32_t t_row = tmem_base + (uint32_t(ew * 32) << 16) + acc * BN;
@@ -474,6 +478,12 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           uint32_t r[EPI_COLS];
           __syncwarp();
           tmem_ld_32x32b_x32(t_row + base, r);
+          // this chunk's dot bound (epi_group8b), selected while the load is in flight
+          const int ci = base >> 5;
+          const float4 ch = ci < 4 ? cm0 : cm1;
+          const int cj = ci & 3;
+          const float cmin = cj < 2 ? (cj == 0 ? ch.x : ch.y) : (cj == 2 ? ch.z : ch.w);
+          const float thr = chunk_threshold(rt.qn, cmin, rt.tau);
           tmem_wait_ld();
 #ifdef RS_PAIR_EPI_NOP  // timing experiment only: the MMA pipeline without the top-k work
           if (__uint_as_float(r[0]) == 12345.0f) rt.append_raw(0.0f, id0);
@@ -482,12 +492,12 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           if (base + EPI_COLS <= valid) {
 #pragma unroll
             for (int g = 0; g < EPI_COLS; g += 8)
-              epi_group8r<KREG, EPI_THREADS, BUF, CHECK, true>(rt, r + g, cn_t + base + g, id0 + base + g, 8);
+              epi_group8b<KREG, EPI_THREADS, BUF, CHECK, true>(rt, r + g, cn_t + base + g, id0 + base + g, 8, thr);
           } else {
 #pragma unroll
             for (int g = 0; g < EPI_COLS; g += 8)
-              epi_group8r<KREG, EPI_THREADS, BUF, CHECK, false>(rt, r + g, cn_t + base + g, id0 + base + g,
-                                                       valid - base - g);
+              epi_group8b<KREG, EPI_THREADS, BUF, CHECK, false>(rt, r + g, cn_t + base + g, id0 + base + g,
+                                                       valid - base - g, thr);
           }
         }
         tc_fence_before();
@@ -535,9 +545,9 @@ extern "C" int rs_debug_pair_profile_reset() {
 #endif
 
 int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap* tmql, const CUtensorMap& tmc,
-                           const CUtensorMap* tmcl, const float* qn, const float* cn, int64_t nq, int64_t n, int dim,
-                           int k, int64_t id_base, const SearchPlan& plan, uint64_t* part, int32_t* counter,
-                           int32_t walk_bias, cudaStream_t st) {
+                           const CUtensorMap* tmcl, const float* qn, const float* cn, const float* cmin, int64_t nq,
+                           int64_t n, int dim, int k, int64_t id_base, const SearchPlan& plan, uint64_t* part,
+                           int32_t* counter, int32_t walk_bias, cudaStream_t st) {
   const bool tf = tmql != nullptr;
   RS_REQUIRE(tf == (tmcl != nullptr), "tf32 path needs both lo maps");
   static bool attr_set[2] = {false, false};
@@ -558,6 +568,7 @@ int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap* tmql, cons
   Params p{};
   p.qn = qn;
   p.cn = cn;
+  p.cmin = cmin;
   p.nq = nq;
   p.n = n;
   const int bk = tf ? Cfg<true>::BK : Cfg<false>::BK;

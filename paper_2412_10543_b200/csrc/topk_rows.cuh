@@ -376,6 +376,34 @@ __device__ __forceinline__ void epi_group8r(RegTopK<KREG, ROWS, BUF>& rt, const 
   if (__any_sync(0xffffffffu, rt.buffered() > BUF - CHECK)) rt.flush();
 }
 
+// Bound-filtered variant.  For the columns of a 32-column chunk,
+//   e_j = |q|^2 + |c_j|^2 - 2<q,c_j>  >=  |q|^2 + min_chunk|c|^2 - 2<q,c_j>,
+// so e_j <= tau needs <q,c_j> >= thr = (|q|^2 + min|c|^2 - tau) / 2 (minus a
+// rounding margin, chunk_threshold).  The fast path is therefore the raw TMEM
+// dots alone — an 8-way max, one compare, one warp vote — and only groups
+// where some lane of the warp passes compute the exact distances (the same
+// FADD2/FFMA2 rounding as epi_group8r) and append.  With normalised corpora
+// the bound is tight; otherwise it is looser but never drops a candidate.
+template <int KREG, int ROWS, int BUF, int CHECK, bool FULL>
+__device__ __forceinline__ void epi_group8b(RegTopK<KREG, ROWS, BUF>& rt, const uint32_t* r, const float* cn,
+                                            uint32_t id, int lim, float thr) {
+  static_assert(BUF >= CHECK, "buffer must hold one group");
+  float m = __uint_as_float(r[0]);
+#pragma unroll
+  for (int j = 1; j < 8; ++j)
+    if (FULL || j < lim) m = fmaxf(m, __uint_as_float(r[j]));
+  if (!__any_sync(0xffffffffu, m >= thr)) return;
+  epi_group8r<KREG, ROWS, BUF, CHECK, FULL>(rt, r, cn, id, lim);
+}
+
+// Dot threshold of a chunk whose smallest corpus norm is cmin (see
+// epi_group8b); +inf tau (list not full) gives -inf: everything passes.  The
+// margin covers the fp32 rounding of both this bound and the exact distance.
+__device__ __forceinline__ float chunk_threshold(float qn, float cmin, float tau) {
+  const float t = 0.5f * (qn + cmin - tau);
+  return t - 1e-6f * (fabsf(qn) + fabsf(cmin) + fabsf(tau)) - 1e-30f;
+}
+
 // Distance from the fused epilogue: ||q||^2 + ||c||^2 - 2<q,c>, negative
 // round-off clamped to 0 (FAISS exhaustive_L2sqr_blas); NaN maps to 0 too.
 __device__ __forceinline__ float l2_from_dot(float qn_plus_cn, float dot) {
