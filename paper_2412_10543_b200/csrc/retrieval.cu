@@ -510,6 +510,7 @@ struct rs_index {
   uint64_t* cand = nullptr;   // fp32 path: merged 3xTF32 candidates [nq, kc] before the exact re-rank
   size_t cand_cap = 0;        // bytes
   float* qnorm = nullptr;
+  uint32_t* qtau = nullptr;   // pair kernel: per-query shared k-th distance (threshold sharing)
   int64_t qnorm_cap = 0;
   uint64_t* part = nullptr;
   size_t part_cap = 0;  // bytes
@@ -536,6 +537,9 @@ int ensure_ws(rs_index* ix, int64_t nq, size_t part_bytes) {
     if (ix->qnorm) cudaFree(ix->qnorm);
     ix->qnorm = nullptr;
     RS_CHECK_CUDA(cudaMalloc(&ix->qnorm, sizeof(float) * nq), "cudaMalloc(qnorm)");
+    if (ix->qtau) cudaFree(ix->qtau);
+    ix->qtau = nullptr;
+    RS_CHECK_CUDA(cudaMalloc(&ix->qtau, sizeof(uint32_t) * nq), "cudaMalloc(qtau)");
     ix->qnorm_cap = nq;
   }
   if (part_bytes > ix->part_cap) {
@@ -627,7 +631,7 @@ int run_partial(rs_index* ix, const void* queries, int64_t nq, int k, int64_t id
     }
     rc = pair ? launch_score_topk_pair(tmq, tf ? &tmql : nullptr, tmc, tf ? &tmcl : nullptr, ix->qnorm, ix->norms,
                                        ix->cmin, nq, ix->ntotal, ix->dim, k, id_base, plan, ix->part,
-                                       ix->sched_counter, ix->walk_bias, st)
+                                       ix->sched_counter, ix->walk_bias, ix->qtau, st)
               : launch_score_topk_tc(tmq, tmc, ix->qnorm, ix->norms, nq, ix->ntotal, ix->dim, k, id_base, plan,
                                      ix->part, st);
   } else {
@@ -733,6 +737,7 @@ extern "C" int rs_index_destroy(rs_index* ix) {
   cudaFree(ix->qlo);
   cudaFree(ix->cand);
   cudaFree(ix->qnorm);
+  cudaFree(ix->qtau);
   cudaFree(ix->part);
   delete ix;
   return RS_OK;

@@ -60,7 +60,7 @@ constexpr int kPairEpiGroups = RS_PAIR_EPI_GROUPS;
 int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap* tmql, const CUtensorMap& tmc,
                            const CUtensorMap* tmcl, const float* qn, const float* cn, const float* cmin, int64_t nq,
                            int64_t n, int dim, int k, int64_t id_base, const SearchPlan& plan, uint64_t* part,
-                           int32_t* counter, int32_t walk_bias, cudaStream_t st);
+                           int32_t* counter, int32_t walk_bias, uint32_t* qtau, cudaStream_t st);
 // per 32-row chunk minimum of the squared norms over rows [r0, r1) of a shard
 // (recomputes every chunk the range touches)
 int launch_chunk_min(const float* norms, int64_t r0, int64_t r1, float* cmin, cudaStream_t st);

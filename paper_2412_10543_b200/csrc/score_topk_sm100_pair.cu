@@ -156,6 +156,7 @@ struct Params {
   int32_t* counter;  // dynamic unit counter (zeroed before the launch)
   int32_t* seg_pos;  // per segment: absolute tile index the most advanced pair last started (zeroed)
   int32_t walk_bias; // test hook: unit of query tile qt starts walk_bias*(qt+1) tiles past the frontier
+  uint32_t* qtau;    // per query: best k-th distance bits published by any unit (memset 0xff per search)
   int64_t cunits;    // cluster units = (qtiles / G) * segments
 };
 
@@ -451,8 +452,15 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       int64_t r0, r1;
       unit_coords(int64_t(u) * G + pp, p, qt, seg, r0, r1);
       const int64_t qrow = int64_t(qt) * PM + int64_t(half) * BM + row;
-      rt.qn = qrow < p.nq ? p.qn[qrow] : 0.0f;
+      const bool real_row = qrow < p.nq;
+      rt.qn = real_row ? p.qn[qrow] : 0.0f;
       rt.reset();
+#ifndef RS_PAIR_NO_SHARED_TAU
+      // threshold sharing: start from the best k-th distance any unit of this
+      // query has published (units of other segments, finished or running)
+      if (real_row) rt.seed(ld_relaxed_gpu_u32(p.qtau + qrow));
+      uint32_t tau_pending = 0xffffffffu;
+#endif
       const TileWalk walk(r0, r1, start);
       for (int64_t j = 0; j < walk.ntiles; ++j, ++tile_iter) {
         const int64_t c0 = walk.c0(j);
@@ -465,6 +473,10 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         const uint32_t acc = tile_iter & 1;
         const int valid = int(r1 - c0 < BN ? r1 - c0 : BN);
         const float* cn_t = cns + acc * BN;
+#ifndef RS_PAIR_NO_SHARED_TAU
+        // every 4th tile: fetch the shared threshold (consumed after the tile)
+        if ((j & 3) == 0 && real_row) tau_pending = ld_relaxed_gpu_u32(p.qtau + qrow);
+#endif
         // the tile's eight 32-column norm minima, loaded before the wait
         const float4 cm0 = __ldg(reinterpret_cast<const float4*>(p.cmin + (c0 >> 5)));
         const float4 cm1 = __ldg(reinterpret_cast<const float4*>(p.cmin + (c0 >> 5)) + 1);
@@ -483,12 +495,18 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           const float4 ch = ci < 4 ? cm0 : cm1;
           const int cj = ci & 3;
           const float cmin = cj < 2 ? (cj == 0 ? ch.x : ch.y) : (cj == 2 ? ch.z : ch.w);
+#ifdef RS_EXP_NO_SLOW  // timing experiment only (wrong results): no candidate ever passes the bound
+          const float thr = __int_as_float(0x7f800000);
+          (void)cmin;
+#else
           const float thr = chunk_threshold(rt.qn, cmin, rt.tau);
+#endif
           tmem_wait_ld();
 #ifdef RS_PAIR_EPI_NOP  // timing experiment only: the MMA pipeline without the top-k work
           if (__uint_as_float(r[0]) == 12345.0f) rt.append_raw(0.0f, id0);
           continue;
 #endif
+#ifdef RS_PAIR_EPI_GROUP_VOTE  // variant: one vote + branch per 8-column group
           if (base + EPI_COLS <= valid) {
 #pragma unroll
             for (int g = 0; g < EPI_COLS; g += 8)
@@ -499,7 +517,22 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
               epi_group8b<KREG, EPI_THREADS, BUF, CHECK, false>(rt, r + g, cn_t + base + g, id0 + base + g,
                                                        valid - base - g, thr);
           }
+#else
+          if (base + EPI_COLS <= valid)
+            epi_chunk32b<KREG, EPI_THREADS, BUF, CHECK, true>(rt, r, cn_t + base, id0 + base, EPI_COLS, thr);
+          else
+            epi_chunk32b<KREG, EPI_THREADS, BUF, CHECK, false>(rt, r, cn_t + base, id0 + base, valid - base, thr);
+#endif
         }
+#ifndef RS_PAIR_NO_SHARED_TAU
+        if ((j & 3) == 0 && real_row) {
+          // publish this list's k-th best (a bound for every other unit of
+          // the query), then adopt the fetched one
+          const uint32_t kb = rt.kth_bits();
+          if (kb < 0x7f800000u && kb < tau_pending) red_min_relaxed_gpu_u32(p.qtau + qrow, kb);
+          rt.seed(tau_pending);
+        }
+#endif
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
@@ -511,6 +544,9 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       }
       // every lane flushes (warp-collective), then writes its row if it is a real query
       PROF(5, rt.flush());
+#ifndef RS_PAIR_NO_SHARED_TAU
+      if (real_row && rt.kth_bits() < 0x7f800000u) red_min_relaxed_gpu_u32(p.qtau + qrow, rt.kth_bits());
+#endif
       if (qrow < p.nq) rt.finish(p.part + ((qrow * p.segments + seg) * EG + eg) * p.k);
     }
   }
@@ -547,7 +583,7 @@ extern "C" int rs_debug_pair_profile_reset() {
 int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap* tmql, const CUtensorMap& tmc,
                            const CUtensorMap* tmcl, const float* qn, const float* cn, const float* cmin, int64_t nq,
                            int64_t n, int dim, int k, int64_t id_base, const SearchPlan& plan, uint64_t* part,
-                           int32_t* counter, int32_t walk_bias, cudaStream_t st) {
+                           int32_t* counter, int32_t walk_bias, uint32_t* qtau, cudaStream_t st) {
   const bool tf = tmql != nullptr;
   RS_REQUIRE(tf == (tmcl != nullptr), "tf32 path needs both lo maps");
   static bool attr_set[2] = {false, false};
@@ -565,6 +601,7 @@ int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap* tmql, cons
   RS_REQUIRE(plan.segments >= 1 && plan.segments <= kMaxSegments, "segments out of range (%d)", plan.segments);
   RS_CHECK_CUDA(cudaMemsetAsync(counter, 0, sizeof(int32_t) * (1 + plan.segments), st),
                 "cudaMemsetAsync(unit counter, segment frontiers)");
+  RS_CHECK_CUDA(cudaMemsetAsync(qtau, 0xff, sizeof(uint32_t) * size_t(nq), st), "cudaMemsetAsync(shared tau)");
   Params p{};
   p.qn = qn;
   p.cn = cn;
@@ -584,6 +621,7 @@ int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap* tmql, cons
   p.counter = counter;
   p.seg_pos = counter + 1;
   p.walk_bias = walk_bias;
+  p.qtau = qtau;
   p.cunits = int64_t(plan.qtiles) * plan.segments;
   if (tf)
     score_topk_pair_kernel<true><<<CL * plan.ctas, NUM_THREADS, Cfg<true>::SMEM_BYTES, st>>>(tmq, *tmql, tmc, *tmcl, p);

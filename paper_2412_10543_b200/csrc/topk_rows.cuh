@@ -267,7 +267,9 @@ struct RegTopK {
   uint32_t id[KREG];
   int k;          // <= KREG
   float tau;      // distance of the current k-th best, +inf until k candidates seen
-  uint32_t ktau;  // key of the current k-th best
+  uint32_t ktau;  // admission key: min(key of the current k-th best, seedk)
+  uint32_t seedk; // shared-threshold seed (see seed()), kEmpty when none
+  uint32_t kthk;  // key of the current k-th best (kEmpty until k entries)
   uint32_t phase; // 1 until the walk wraps to lower ids, then 0
   float qn;       // this row's |q|^2
   uint32_t wbase; // shared-window byte address of this row's buffer slot 0
@@ -283,6 +285,8 @@ struct RegTopK {
     }
     tau = __int_as_float(0x7f800000);
     ktau = kEmpty;
+    seedk = kEmpty;
+    kthk = kEmpty;
     phase = 1;
     wp = wbase;
   }
@@ -311,9 +315,31 @@ struct RegTopK {
 #pragma unroll
     for (int j = 1; j < KREG; ++j)
       if (j == k - 1) t = key[j];
-    ktau = t;
-    tau = __uint_as_float(t >> 1);
+    kthk = t;
+    ktau = t < seedk ? t : seedk;
+    tau = __uint_as_float(ktau >> 1);
   }
+
+  // Shared threshold: dist_bits is the k-th best distance of SOME k real rows
+  // of this query (another unit's list), hence >= the final k-th distance;
+  // only candidates at or below it can reach the final top-k.  The seed key
+  // (bits + 1) << 1 admits every candidate with distance <= that value, in
+  // either phase (exact ties are kept; the merge orders them by id), so the
+  // unit's list may end with fewer than k real entries — it never loses one
+  // the global top-k needs.
+  __device__ __forceinline__ void seed(uint32_t dist_bits) {
+    if (dist_bits >= 0x7f800000u) return;  // +inf / no bound yet
+    const uint32_t s = (dist_bits + 1u) << 1;
+    if (s < seedk) {
+      seedk = s;
+      if (s < ktau) {
+        ktau = s;
+        tau = __uint_as_float(s >> 1);
+      }
+    }
+  }
+  // distance bits of the current k-th best (0x7f800000 = +inf until k entries)
+  __device__ __forceinline__ uint32_t kth_bits() const { return kthk >> 1; }
 
   // Warp-collective: every lane inserts its buffered candidates (lockstep over
   // the warp's largest buffer; lanes past their own count insert kEmpty = no-op).
@@ -394,6 +420,37 @@ __device__ __forceinline__ void epi_group8b(RegTopK<KREG, ROWS, BUF>& rt, const 
     if (FULL || j < lim) m = fmaxf(m, __uint_as_float(r[j]));
   if (!__any_sync(0xffffffffu, m >= thr)) return;
   epi_group8r<KREG, ROWS, BUF, CHECK, FULL>(rt, r, cn, id, lim);
+}
+
+// A whole 32-column TMEM chunk through the dot bound: four independent 8-way
+// max trees, four votes, and a single branch in the common case that no lane
+// of the warp has a candidate anywhere in the chunk (a one-warp-per-SMSP
+// epilogue is latency-bound, so the short dependency chains and the single
+// branch matter more than the instruction count).
+template <int KREG, int ROWS, int BUF, int CHECK, bool FULL>
+__device__ __forceinline__ void epi_chunk32b(RegTopK<KREG, ROWS, BUF>& rt, const uint32_t* r, const float* cn,
+                                             uint32_t id, int lim, float thr) {
+  float m[4];
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    float v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      v[j] = (FULL || g * 8 + j < lim) ? __uint_as_float(r[g * 8 + j]) : -__int_as_float(0x7f800000);
+    m[g] = fmaxf(fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3])), fmaxf(fmaxf(v[4], v[5]), fmaxf(v[6], v[7])));
+  }
+  uint32_t hit = 0;
+#pragma unroll
+  for (int g = 0; g < 4; ++g) hit |= __any_sync(0xffffffffu, m[g] >= thr) ? (1u << g) : 0u;
+  if (hit == 0) return;
+#pragma unroll
+  for (int g = 0; g < 4; ++g)
+    if (hit & (1u << g)) {
+      if (FULL)
+        epi_group8r<KREG, ROWS, BUF, CHECK, true>(rt, r + g * 8, cn + g * 8, id + g * 8, 8);
+      else
+        epi_group8r<KREG, ROWS, BUF, CHECK, false>(rt, r + g * 8, cn + g * 8, id + g * 8, lim - g * 8);
+    }
 }
 
 // Dot threshold of a chunk whose smallest corpus norm is cmin (see
