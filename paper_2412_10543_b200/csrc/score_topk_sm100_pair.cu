@@ -137,7 +137,6 @@ struct Cfg {
   static constexpr size_t OFF_TAIL = OFF_CN + 2 * BN * sizeof(float);
   static constexpr size_t SMEM_BYTES = OFF_TAIL + sizeof(Tail);
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
-  static_assert(!TF || G == 1, "tf32 path has no multicast variant");
 };
 
 using TopK = RegTopK<KREG, EPI_THREADS, BUF>;
@@ -586,6 +585,7 @@ int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap* tmql, cons
                            int32_t* counter, int32_t walk_bias, uint32_t* qtau, cudaStream_t st) {
   const bool tf = tmql != nullptr;
   RS_REQUIRE(tf == (tmcl != nullptr), "tf32 path needs both lo maps");
+  RS_REQUIRE(!tf || G == 1, "the tf32 path has no multicast (RS_PAIR_GROUP) variant");
   static bool attr_set[2] = {false, false};
   if (!attr_set[tf]) {
     if (tf)
