@@ -444,7 +444,10 @@ def main():
     prof_path = os.path.join(ROOT, "profiles", f"ncu_{args.workload}_n{world}.json")
     if os.path.exists(prof_path):
         try:
-            roof["traffic"] = json.load(open(prof_path)).get("dram_bytes_per_launch")
+            pj = json.load(open(prof_path))
+            roof["traffic"] = pj.get("dram_bytes_per_launch")
+            if pj.get("tensor_pipe_pct") is not None:  # same kernel's tensor pipe activity in that capture
+                roof["tensor_pipe_active_ncu"] = round(pj["tensor_pipe_pct"] / 100.0, 4)
         except Exception:
             pass
 
