@@ -209,6 +209,19 @@ int rs_plan_calls(const rs_config* configs, const int32_t* qlen, int64_t n,
                   rs_call* calls, int64_t* total_bytes, uint8_t* status, void* workspace,
                   size_t workspace_bytes, void* stream);
 
+/* ---- profile ingestion (parse_profile_text, profiler.py:203-254) -----------
+ * Host routine (the answers are strings on the host): parse n estimator
+ * answers — UTF-8, answer i = text[offsets[i] .. offsets[i+1]) — into
+ * rs_profile records with confidence[i] (NULL = 1.0), the clamped-field bits
+ * and, if line_numbers is non-NULL, the line of each field (n x 4: complexity,
+ * joint_reasoning, pieces, summary_range; -1 = absent).  status[i] is
+ * RS_PARSE_UNPARSEABLE where the reference raises UnparseableAnswer.
+ * nthreads <= 0 uses every hardware thread.  All pointers are host memory. */
+enum rs_parse_status { RS_PARSE_OK = 0, RS_PARSE_UNPARSEABLE = 1 };
+enum rs_clamped_bits { RS_CLAMPED_PIECES = 1, RS_CLAMPED_SUMMARY = 2 };
+int rs_parse_profiles(const char* text, const int64_t* offsets, int64_t n, const double* confidence,
+                      rs_profile* out, uint8_t* clamped, int32_t* line_numbers, uint8_t* status, int32_t nthreads);
+
 /* ---- FIFO admission chain (Scheduler.step, scheduler.py:397-410) ----------
  * The new-query loop of Scheduler.step: for the waiting queue in FIFO order,
  * _try_admit_new (scheduler.py:335-395) — best_fit_select against the free

@@ -118,6 +118,7 @@ SIGNATURES = {
     "rs_plan_calls_workspace_size": (ctypes.c_size_t, [_I64]),
     "rs_plan_calls": (ctypes.c_int, [_P, _P, _I64, ctypes.POINTER(SelectParamsC), _I64, _P, _P, _P, _P, _P,
                                      ctypes.c_size_t, _P]),
+    "rs_parse_profiles": (ctypes.c_int, [ctypes.c_char_p, _P, _I64, _P, _P, _P, _P, _P, _I32]),
     "rs_admit_fifo": (ctypes.c_int, [_P, _P, _P, _P, _I64, ctypes.POINTER(SelectParamsC),
                                      ctypes.POINTER(AdmitParamsC), _P, _P, _P, _P]),
     "rs_launch_count": (ctypes.c_uint64, []),

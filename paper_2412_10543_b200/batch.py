@@ -164,6 +164,50 @@ def unpack_config(rec, *, config_cls=RagConfig, method_enum=SynthesisMethod):
     return config_cls(me, int(rec["num_chunks"]), il)
 
 
+RS_PARSE_OK, RS_PARSE_UNPARSEABLE = 0, 1
+RS_CLAMPED_PIECES, RS_CLAMPED_SUMMARY = 1, 2
+
+
+def parse_profiles(texts, confidences=None, *, nthreads: int = 0):
+    """parse_profile_text (profiler.py:203-254) for a batch of estimator
+    answers, on the host (``rs_parse_profiles``, multi-threaded native code).
+    Returns (rs_profile structured array, clamped bits u8 [n], status u8 [n],
+    field line numbers int32 [n, 4])."""
+    n = len(texts)
+    enc = [t.encode("utf-8", "surrogatepass") for t in texts]
+    offsets = np.zeros(n + 1, dtype=np.int64)
+    if n:
+        offsets[1:] = np.cumsum([len(b) for b in enc])
+    buf = b"".join(enc) + b"\0"
+    conf = np.ones(n, dtype=np.float64) if confidences is None else np.asarray(confidences, dtype=np.float64)
+    out = np.zeros(n, dtype=PROFILE_DTYPE)
+    clamped = np.zeros(n, dtype=np.uint8)
+    status = np.zeros(n, dtype=np.uint8)
+    lines = np.zeros((n, 4), dtype=np.int32)
+    lib = _lib.load()
+    _lib.check(lib.rs_parse_profiles(buf, offsets.ctypes.data, n, conf.ctypes.data, out.ctypes.data,
+                                     clamped.ctypes.data, lines.ctypes.data, status.ctypes.data, int(nthreads)),
+               "rs_parse_profiles")
+    return out, clamped, status, lines
+
+
+def clamped_names(bits) -> frozenset:
+    bits = int(bits)
+    return frozenset(n for b, n in ((RS_CLAMPED_PIECES, "pieces"), (RS_CLAMPED_SUMMARY, "summary_range"))
+                     if bits & b)
+
+
+def unpack_profile(rec, *, profile_cls=None, range_cls=IntRange):
+    """rs_profile record -> QueryProfile (this package's or the reference's)."""
+    from .mapping import QueryProfile
+
+    cls = profile_cls or QueryProfile
+    return cls(complexity_high=bool(rec["complexity_high"]), needs_joint_reasoning=bool(rec["needs_joint_reasoning"]),
+               pieces_required=int(rec["pieces_required"]),
+               summary_len_range=range_cls(int(rec["summary_lo"]), int(rec["summary_hi"])),
+               confidence=float(rec["confidence"]))
+
+
 def to_device(arr: np.ndarray, device) -> torch.Tensor:
     """Structured numpy array -> device uint8 tensor [n, itemsize]."""
     raw = np.ascontiguousarray(arr).view(np.uint8).reshape(len(arr), arr.dtype.itemsize)

@@ -20,7 +20,8 @@ CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 OBJ = os.path.join(HERE, "_obj")
 LIB = os.path.join(HERE, "libragsched_b200.so")
-SOURCES = ["abi.cu", "select.cu", "gate.cu", "plan.cu", "retrieval.cu", "score_topk_sm100.cu", "score_topk_sm100_pair.cu"]
+SOURCES = ["abi.cu", "select.cu", "gate.cu", "plan.cu", "retrieval.cu", "score_topk_sm100.cu", "score_topk_sm100_pair.cu",
+           "parse.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -52,7 +53,7 @@ def _stale(target, deps):
 
 def _compile(src, verbose, objdir=None, defines=()):
     objdir = objdir or OBJ
-    obj = os.path.join(objdir, src.replace(".cu", ".o"))
+    obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")
     if not _stale(obj, _deps(src)):
         return obj, ""
     cmd = [nvcc(), *_flags(), *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, src), "-o", obj]

@@ -67,6 +67,7 @@ def install(ragsched_pkg) -> dict:
         (sched, "Scheduler"): sched.Scheduler,
         (sim, "Scheduler"): sim.Scheduler,
         (memory, "plan_calls"): memory.plan_calls,
+        (prof, "parse_profile_text"): prof.parse_profile_text,
         (sched, "plan_calls"): sched.plan_calls,
     }
 
@@ -86,6 +87,8 @@ def install(ragsched_pkg) -> dict:
                            kind_enum=memory.CallKind)
     memory.plan_calls = pc
     sched.plan_calls = pc
+    prof.parse_profile_text = functools.partial(_profiler.parse_profile_text, profile_cls=mapping.QueryProfile,
+                                                range_cls=types.IntRange, exc_cls=prof.UnparseableAnswer)
     return originals
 
 

@@ -104,3 +104,25 @@ def gate_profile(out, window, threshold: float = GATE_THRESHOLD, *, default_spac
 
 def window_records(window) -> np.ndarray:
     return _b.pack_spaces(_window_spaces(window))
+
+
+# -- answer ingestion (profiler.py:191-254) -------------------------------------
+
+PROFILE_FIELDS = ("complexity", "joint_reasoning", "pieces", "summary_range")  # profiler.py:51
+
+
+class UnparseableAnswer(ValueError):
+    """profiler.py:84-85."""
+
+
+def parse_profile_text(text: str, confidence: float = 1.0, *, profile_cls=None, range_cls=IntRange,
+                       exc_cls=UnparseableAnswer):
+    """profiler.py:203-254 through the native batch parser (``rs_parse_profiles``):
+    (profile, clamped field names, field line numbers); raises
+    UnparseableAnswer when a field is missing."""
+    recs, clamped, status, lines = _b.parse_profiles([text], [confidence], nthreads=1)
+    if status[0] != _b.RS_PARSE_OK:
+        raise exc_cls(f"missing fields {[PROFILE_FIELDS[i] for i in range(4) if lines[0, i] < 0]} "
+                      f"in estimator answer: {text!r}")
+    return (_b.unpack_profile(recs[0], profile_cls=profile_cls, range_cls=range_cls),
+            _b.clamped_names(clamped[0]), {f: int(lines[0, i]) for i, f in enumerate(PROFILE_FIELDS)})

@@ -434,6 +434,102 @@ def gen_known():
     print("known:", known)
 
 
+# -- G7: estimator answer parsing (profiler.parse_profile_text) -----------------
+
+def gen_parse():
+    """Random answers around the four-line grammar (profiler.py:191-200):
+    case, spacing (incl. Unicode spaces), line separators, out-of-domain and
+    huge numbers, reversed ranges, duplicate / missing / garbled fields,
+    word-boundary and folding edge cases.  ASCII digits only."""
+    import gzip
+    import json
+
+    from ragsched.profiler import UnparseableAnswer, parse_profile_text
+
+    rng = random.Random(7)
+    spaces = [" ", "  ", "\t", "", "\u00a0", "\u3000", " \t ", "\x1f"]
+    seps = ["\n", "\r\n", "\r", "\n\n", "\x0b", "\x0c", "\u2028", "\x1c", "\x85"]
+
+    def case(w):
+        r = rng.random()
+        if r < 0.5:
+            return w
+        if r < 0.7:
+            return w.upper()
+        if r < 0.85:
+            return w.lower()
+        return "".join(c.upper() if rng.random() < 0.5 else c.lower() for c in w)
+
+    def sp():
+        return rng.choice(spaces) if rng.random() < 0.4 else rng.choice([" ", ""])
+
+    def num():
+        r = rng.random()
+        if r < 0.6:
+            return str(rng.randint(-5, 260))
+        if r < 0.7:
+            return "0" + str(rng.randint(0, 99))
+        if r < 0.8:
+            return str(rng.randint(10 ** 18, 10 ** 30)) * rng.choice([1, 2])
+        if r < 0.9:
+            return "-" + str(rng.randint(10 ** 18, 10 ** 25))
+        return str(rng.randint(1, 12))
+
+    def tail():
+        if rng.random() < 0.8:
+            return ""
+        return rng.choice([".", " ", "x", "_", "1", "é", "—", "!", " extra", "\u00a0"])
+
+    def field(kind):
+        if kind == 0:
+            word = rng.choice(["High", "Low"]) if rng.random() < 0.9 else rng.choice(["Hıgh", "Medium", "Lo"])
+            return f"{sp()}{case('Complexity')}{sp()}:{sp()}{case(word) if word.isascii() else word}{tail()}"
+        if kind == 1:
+            word = rng.choice(["Yes", "No"]) if rng.random() < 0.9 else rng.choice(["Maybe", "Yeſ", "Ye"])
+            key = "Joint Reasoning needed" if rng.random() < 0.9 else rng.choice(
+                ["Joint  Reasoning needed", "Joint reaſoning needed", "Joint Reasoning"])
+            return f"{sp()}{case(key) if key.isascii() else key}{sp()}:{sp()}{word}{tail()}"
+        if kind == 2:
+            key = "Pieces" if rng.random() < 0.93 else rng.choice(["Piece", "Pİeces"])
+            return f"{sp()}{case(key) if key.isascii() else key}{sp()}:{sp()}{num()}{tail()}"
+        a, b = num(), num()
+        dash = rng.choice(["-", " - ", "--"]) if rng.random() < 0.93 else rng.choice(["–", "to"])
+        key = "Summary range" if rng.random() < 0.93 else rng.choice(["summary  range", "Summary"])
+        return f"{sp()}{case(key)}{sp()}:{sp()}{a}{sp()}{dash}{sp()}{b}{tail()}"
+
+    rows = []
+    for i in range(4000):
+        kinds = [0, 1, 2, 3]
+        rng.shuffle(kinds) if rng.random() < 0.3 else None
+        lines = []
+        for k in kinds:
+            if rng.random() < 0.03:
+                continue  # missing field
+            lines.append(field(k))
+            if rng.random() < 0.15:
+                lines.append(field(k))  # duplicate: the first match wins
+            if rng.random() < 0.1:
+                lines.append(rng.choice(["", "Note: none", "Answer:", "   ", "Complexity", "Pieces:"]))
+        if rng.random() < 0.2:
+            lines.insert(0, rng.choice(["Here is the profile:", "", "Profile"]))
+        text = ""
+        for j, ln in enumerate(lines):
+            text += ln + (rng.choice(seps) if j + 1 < len(lines) or rng.random() < 0.3 else "")
+        conf = rng.random()
+        try:
+            prof, clamped, lnums = parse_profile_text(text, confidence=conf)
+            res = [int(prof.complexity_high), int(prof.needs_joint_reasoning), prof.pieces_required,
+                   prof.summary_len_range.low, prof.summary_len_range.high, sorted(clamped),
+                   [lnums.get(f, -1) for f in ("complexity", "joint_reasoning", "pieces", "summary_range")]]
+        except UnparseableAnswer:
+            res = None
+        rows.append([text, conf, res])
+    with gzip.open(os.path.join(OUT_DIR, "parse.json.gz"), "wt", encoding="utf-8") as f:
+        json.dump(rows, f, ensure_ascii=False)
+    print("parse:", len(rows), "answers,", sum(r[2] is None for r in rows), "unparseable,",
+          sum(bool(r[2] and r[2][5]) for r in rows), "clamped")
+
+
 if __name__ == "__main__":
     gen_mapping()
     gen_select()
@@ -441,3 +537,4 @@ if __name__ == "__main__":
     gen_latency()
     gen_plan_calls()
     gen_known()
+    gen_parse()

@@ -86,3 +86,13 @@ def scheduler_traces():
 
     with gzip.open(os.path.join(GOLDEN, "scheduler_traces.json.gz"), "rt") as f:
         return json.load(f)
+
+
+def parse_answers():
+    """[text, confidence, result | None] from the reference's parse_profile_text
+    (tests/golden/make_golden.py gen_parse)."""
+    import gzip
+    import json
+
+    with gzip.open(os.path.join(GOLDEN, "parse.json.gz"), "rt", encoding="utf-8") as f:
+        return json.load(f)

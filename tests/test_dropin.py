@@ -31,7 +31,7 @@ def test_install_and_uninstall(ragsched):
 
     names = lambda: (scheduler.best_fit_select, scheduler.fallback_config, profiler.gate_profile,  # noqa: E731
                      mapping.map_profile, memory.plan_bytes, sim.call_latency, scheduler.Scheduler, sim.Scheduler,
-                     memory.plan_calls, scheduler.plan_calls)
+                     memory.plan_calls, scheduler.plan_calls, profiler.parse_profile_text)
     before = names()
     originals = dropin.install(ragsched)
     after = names()
@@ -43,6 +43,10 @@ def test_install_and_uninstall(ragsched):
     assert scheduler.Scheduler.classes.Admission is ragsched.scheduler.Admission
     assert scheduler.Scheduler.classes.CallKind is ragsched.memory.CallKind
     assert sim.Scheduler is scheduler.Scheduler
+    # the native parser returns the reference's own QueryProfile (host code: runs without a GPU)
+    p, clamped, lines = profiler.parse_profile_text("Complexity: High\nJoint Reasoning needed: Yes\nPieces: 4\n"
+                                                    "Summary range: 50-120", 0.97)
+    assert isinstance(p, ragsched.mapping.QueryProfile) and p.summary_len_range == ragsched.types.IntRange(50, 120)
     dropin.uninstall(originals)
     restored = names()
     assert all(a is b for a, b in zip(before, restored))
