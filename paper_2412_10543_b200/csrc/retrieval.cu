@@ -574,15 +574,19 @@ int choose_algo(const rs_index* ix, int k) {
   return RS_ALGO_TCGEN05;
 }
 
+// small batches take the CTA pair's M = 128 tile: one tile, no padding rows
+bool pair_small(int64_t nq) { return nq <= rs::kSmallBatchMax && rs::kPairGroup == 1; }
+
 rs::SearchPlan make_plan(const rs_index* ix, int algo, int64_t nq, int64_t n, int k) {
   using namespace rs;
   const int sms = sm_count(ix->device);
-  if (algo == RS_ALGO_TCGEN05) {  // units of one cluster: kPairGroup pairs x 256 queries
+  if (algo == RS_ALGO_TCGEN05) {  // units of one cluster: kPairGroup pair tiles
     // tile cost in bf16-equivalent K: 3 tf32 passes at half the bf16 rate
     const int64_t eq_row_bytes = int64_t(ix->dim) * 2 * (ix->dtype == RS_BF16 ? 1 : 6);
-    SearchPlan p = plan_search(nq, n, 2 * kTcBM * kPairGroup, kTcBN, sms / (2 * kPairGroup), eq_row_bytes,
-                               /*share_l2=*/false);
-    p.lists_per_seg = kPairEpiGroups;
+    const bool small = pair_small(nq);
+    SearchPlan p = plan_search(nq, n, pair_tile_rows(small) * kPairGroup, kTcBN, sms / (2 * kPairGroup),
+                               eq_row_bytes, /*share_l2=*/false);
+    p.lists_per_seg = small ? 2 : kPairEpiGroups;
     return p;
   }
   if (algo == RS_ALGO_TCGEN05_1SM) return plan_search(nq, n, kTcBM, kTcBN, sms, int64_t(ix->dim) * 2, true);
@@ -617,20 +621,22 @@ int run_partial(rs_index* ix, const void* queries, int64_t nq, int k, int64_t id
     const bool tf = ix->dtype == RS_F32;
     CUtensorMap tmq, tmc, tmql, tmcl;
     const int crows = pair ? kTcBN / 2 / kPairGroup : kTcBN;
-    rc = encode_kmajor_map(&tmq, queries, nq, ix->dim, kTcBM, ix->dtype);
+    const bool small = pair && pair_small(nq);
+    const int qrows = pair ? pair_tile_rows(small) / 2 : kTcBM;  // query rows per CTA
+    rc = encode_kmajor_map(&tmq, queries, nq, ix->dim, qrows, ix->dtype);
     if (rc) return rc;
     rc = encode_kmajor_map(&tmc, ix->data, ix->ntotal, ix->dim, crows, ix->dtype);
     if (rc) return rc;
     if (tf) {  // 3xTF32: the queries' residuals (the corpus's were made at add)
       rc = launch_tf32_lo(static_cast<const float*>(queries), nq * ix->dim, ix->qlo, st);
       if (rc) return rc;
-      rc = encode_kmajor_map(&tmql, ix->qlo, nq, ix->dim, kTcBM, RS_F32);
+      rc = encode_kmajor_map(&tmql, ix->qlo, nq, ix->dim, qrows, RS_F32);
       if (rc) return rc;
       rc = encode_kmajor_map(&tmcl, ix->lo, ix->ntotal, ix->dim, crows, RS_F32);
       if (rc) return rc;
     }
     rc = pair ? launch_score_topk_pair(tmq, tf ? &tmql : nullptr, tmc, tf ? &tmcl : nullptr, ix->qnorm, ix->norms,
-                                       ix->cmin, nq, ix->ntotal, ix->dim, k, id_base, plan, ix->part,
+                                       ix->cmin, nq, ix->ntotal, ix->dim, k, id_base, plan, small, ix->part,
                                        ix->sched_counter, ix->walk_bias, ix->qtau, st)
               : launch_score_topk_tc(tmq, tmc, ix->qnorm, ix->norms, nq, ix->ntotal, ix->dim, k, id_base, plan,
                                      ix->part, st);

@@ -59,8 +59,12 @@ constexpr int kPairEpiGroups = RS_PAIR_EPI_GROUPS;
 // tmql / tmcl: the fp32 path's lo maps (3xTF32), NULL for bf16.
 int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap* tmql, const CUtensorMap& tmc,
                            const CUtensorMap* tmcl, const float* qn, const float* cn, const float* cmin, int64_t nq,
-                           int64_t n, int dim, int k, int64_t id_base, const SearchPlan& plan, uint64_t* part,
-                           int32_t* counter, int32_t walk_bias, uint32_t* qtau, cudaStream_t st);
+                           int64_t n, int dim, int k, int64_t id_base, const SearchPlan& plan, bool small,
+                           uint64_t* part, int32_t* counter, int32_t walk_bias, uint32_t* qtau, cudaStream_t st);
+// query rows per pair tile: 256, or 128 for the small-batch (M = 128) variant
+int pair_tile_rows(bool small);
+// queries up to which a search uses the M = 128 pair tile (one tile, no padding rows)
+constexpr int64_t kSmallBatchMax = 128;
 // per 32-row chunk minimum of the squared norms over rows [r0, r1) of a shard
 // (recomputes every chunk the range touches)
 int launch_chunk_min(const float* norms, int64_t r0, int64_t r1, float* cmin, cudaStream_t st);

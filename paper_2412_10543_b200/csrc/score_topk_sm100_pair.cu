@@ -123,14 +123,29 @@ struct __align__(8) SmemTailT {
 // TMEM accumulator.  The accumulator's truncating adds leave ~1e-5 relative
 // error on large dots at d = 768, so the fp32 search keeps k + 8 candidates
 // and re-ranks them exactly (refine_fp32_kernel, retrieval.cu).
-template <bool TF>
+//
+// Pair tile height.  SM = false: M = 256 (128 query rows per CTA), the
+// accumulator of a tile fills 256 TMEM columns of all 128 lanes.  SM = true
+// (small batches, nq <= 128): M = 128 (64 rows per CTA), so a lone query
+// tile wastes no MMA work on padding rows; tcgen05's 2-CTA M = 128 data path
+// puts rows 0-31 / 32-63 in lane quadrants 0 / 1 for tile columns 0-127 and
+// again in quadrants 2 / 3 for columns 128-255, 128 TMEM columns per tile.
+// Each epilogue warp then owns half the columns of 32 rows, so a row keeps
+// two top-k lists per unit (merged downstream like the segments).
+template <bool TF, bool SM = false>
 struct Cfg {
   static constexpr int BK = TF ? 32 : 64;  // elements per k-block (one 128-byte row)
   static constexpr int NT = TF ? 2 : 1;    // tiles per operand per stage (hi, lo)
+  static constexpr int BMv = SM ? 64 : BM;  // query rows per CTA
+  static constexpr int PMv = 2 * BMv;      // query rows per pair tile (the MMA's M)
+  static constexpr int A_BYTESv = BMv * ROW_BYTES;
+  static constexpr int ACC_COLS = SM ? BN / 2 : BN;  // TMEM columns per accumulator buffer
+  static constexpr int LPS = SM ? 2 : EG;            // top-k lists per (query, segment)
   static constexpr int STAGES = TF ? RS_PAIR_STAGES_TF32 : RS_PAIR_STAGES;
-  static constexpr int STAGE_BYTES = NT * (A_BYTES + B_BYTES);
-  static constexpr int OFF_B = NT * A_BYTES;  // stage layout: A hi | [A lo] | B hi | [B lo]
-  static constexpr uint32_t IDESC = TF ? umma_idesc_tf32_f32(PM, BN) : umma_idesc_bf16_f32(PM, BN);
+  static constexpr int STAGE_BYTES = NT * (A_BYTESv + B_BYTES);
+  static constexpr int OFF_B = NT * A_BYTESv;  // stage layout: A hi | [A lo] | B hi | [B lo]
+  static constexpr uint32_t IDESC = TF ? umma_idesc_tf32_f32(PMv, BN) : umma_idesc_bf16_f32(PMv, BN);
+  static_assert(!SM || EG == 1, "the M = 128 variant splits columns by lane quadrant, not by warp group");
   using Tail = SmemTailT<STAGES>;
   static constexpr size_t OFF_BUF = size_t(STAGES) * STAGE_BYTES;
   static constexpr size_t OFF_CN = OFF_BUF + size_t(BUF) * EPI_THREADS * 8;
@@ -226,12 +241,12 @@ __device__ unsigned long long g_pair_prof[1024][8];
 #define PROF(slot, stmt) stmt
 #endif
 
-template <bool TF>
+template <bool TF, bool SM>
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     score_topk_pair_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmql,
                            const __grid_constant__ CUtensorMap tmc, const __grid_constant__ CUtensorMap tmcl,
                            const Params p) {
-  using C = Cfg<TF>;
+  using C = Cfg<TF, SM>;
   using SmemTail = typename C::Tail;
   constexpr int STAGES = C::STAGES;
   // no static shared memory: the dynamic window starts at the CTA's shared
@@ -345,9 +360,9 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 #else
             if (leader) mbar_arrive_expect_tx(&tail->full[stage], 2 * C::STAGE_BYTES);
             const int32_t kx = kb * C::BK;
-            const int32_t qrow0 = qt * PM + int(half) * BM;
+            const int32_t qrow0 = qt * C::PMv + int(half) * C::BMv;
             tma_load_2d_pair(&tmq, full_leader, sa, kx, qrow0, pol_q);
-            if (TF) tma_load_2d_pair(&tmql, full_leader, sa + A_BYTES, kx, qrow0, pol_q);
+            if (TF) tma_load_2d_pair(&tmql, full_leader, sa + C::A_BYTESv, kx, qrow0, pol_q);
             if (G == 1) {
 #ifdef RS_EXP_L2_CORPUS_ROWS  // timing experiment only (wrong results): corpus reads wrap in an L2-sized window
               const int32_t crow0 = int32_t(c0 % RS_EXP_L2_CORPUS_ROWS) + int(half) * HB;
@@ -400,7 +415,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             bulk_copy_g2s(cns + acc * BN, p.cn + c0, bytes, &tail->tfull[acc]);
           }
           if (!leader) continue;
-          const uint32_t d_tmem = tmem_base + acc * BN;
+          const uint32_t d_tmem = tmem_base + acc * C::ACC_COLS;
           for (int kb = 0; kb < p.kblocks; ++kb) {
             PROF(2, mbar_wait(&tail->full[stage], phase));
             tc_fence_after();
@@ -412,7 +427,8 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                 umma_bf16_ss_pair(d_tmem, umma_desc_sw128(a_addr + kk * 32), umma_desc_sw128(b_addr + kk * 32),
                                   C::IDESC, (kb | kk) != 0);
               } else {
-                const uint64_t ahi = umma_desc_sw128(a_addr + kk * 32), alo = umma_desc_sw128(a_addr + A_BYTES + kk * 32);
+                const uint64_t ahi = umma_desc_sw128(a_addr + kk * 32);
+                const uint64_t alo = umma_desc_sw128(a_addr + C::A_BYTESv + kk * 32);
                 const uint64_t bhi = umma_desc_sw128(b_addr + kk * 32), blo = umma_desc_sw128(b_addr + B_BYTES + kk * 32);
                 umma_tf32_ss_pair(d_tmem, alo, bhi, C::IDESC, (kb | kk) != 0);  // small terms first
                 umma_tf32_ss_pair(d_tmem, ahi, blo, C::IDESC, 1);
@@ -432,8 +448,13 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   } else if (warp >= EPI_WARP0 && warp < EPI_WARP0 + 4 * EG) {
     // ===== epilogue (both CTAs): 128 queries x 256 chunks per tile =====
     const int ew = (warp - EPI_WARP0) & 3;  // == warp % 4: the TMEM lane quadrant this warp may read
-    const int eg = (warp - EPI_WARP0) >> 2; // column slice [eg*CPG, (eg+1)*CPG) of every tile
-    const int row = ew * 32 + lane;
+    // column slice of every tile this warp filters, and the list it feeds:
+    // M = 256: warp group eg owns [eg*CPG, (eg+1)*CPG) of its quadrant's rows;
+    // M = 128: quadrant ew holds rows (ew&1)*32.. for tile columns (ew>>1)*128..
+    const int eg = SM ? (ew >> 1) : ((warp - EPI_WARP0) >> 2);
+    constexpr int SLICE = SM ? BN / 2 : CPG;
+    const int row = SM ? (ew & 1) * 32 + lane : ew * 32 + lane;
+    const int tcol0 = SM ? eg * SLICE : 0;  // tile column held at this accumulator's TMEM column 0
     const int et = (warp - EPI_WARP0) * 32 + lane;
     TopK rt;
     rt.k = p.k;
@@ -450,7 +471,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       int qt, seg;
       int64_t r0, r1;
       unit_coords(int64_t(u) * G + pp, p, qt, seg, r0, r1);
-      const int64_t qrow = int64_t(qt) * PM + int64_t(half) * BM + row;
+      const int64_t qrow = int64_t(qt) * C::PMv + int64_t(half) * C::BMv + row;
       const bool real_row = qrow < p.nq;
       rt.qn = real_row ? p.qn[qrow] : 0.0f;
       rt.reset();
@@ -481,10 +502,10 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         const float4 cm1 = __ldg(reinterpret_cast<const float4*>(p.cmin + (c0 >> 5)) + 1);
         PROF(3, mbar_wait(&tail->tfull[acc], (tile_iter >> 1) & 1));
         tc_fence_after();
-        const uint32_t t_row = tmem_base + (uint32_t(ew * 32) << 16) + acc * BN;
+        const uint32_t t_row = tmem_base + (uint32_t(ew * 32) << 16) + acc * C::ACC_COLS - tcol0;
         const uint32_t id0 = uint32_t(p.id_base + c0);
 #pragma unroll 1
-        for (int base = eg * CPG; base < (eg + 1) * CPG; base += EPI_COLS) {
+        for (int base = eg * SLICE; base < (eg + 1) * SLICE; base += EPI_COLS) {
           if (base >= valid) break;  // warp-uniform
           uint32_t r[EPI_COLS];
           __syncwarp();
@@ -546,7 +567,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 #ifndef RS_PAIR_NO_SHARED_TAU
       if (real_row && rt.kth_bits() < 0x7f800000u) red_min_relaxed_gpu_u32(p.qtau + qrow, rt.kth_bits());
 #endif
-      if (qrow < p.nq) rt.finish(p.part + ((qrow * p.segments + seg) * EG + eg) * p.k);
+      if (qrow < p.nq) rt.finish(p.part + ((qrow * p.segments + seg) * C::LPS + eg) * p.k);
     }
   }
 #if RS_PAIR_PROFILE
@@ -579,25 +600,43 @@ extern "C" int rs_debug_pair_profile_reset() {
 }
 #endif
 
+namespace {
+
+template <bool TF, bool SM>
+int set_smem_attr() {
+  static bool done = false;
+  if (!done) {
+    RS_CHECK_CUDA(cudaFuncSetAttribute(score_topk_pair_kernel<TF, SM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(Cfg<TF, SM>::SMEM_BYTES)),
+                  "cudaFuncSetAttribute(score_topk_pair_kernel)");
+    done = true;
+  }
+  return RS_OK;
+}
+
+template <bool TF, bool SM>
+int launch_t(const CUtensorMap& tmq, const CUtensorMap& tmql, const CUtensorMap& tmc, const CUtensorMap& tmcl,
+             const Params& p, int ctas, cudaStream_t st) {
+  int rc = set_smem_attr<TF, SM>();
+  if (rc) return rc;
+  score_topk_pair_kernel<TF, SM><<<CL * ctas, NUM_THREADS, Cfg<TF, SM>::SMEM_BYTES, st>>>(tmq, tmql, tmc, tmcl, p);
+  RS_CHECK_LAUNCH("score_topk_pair_kernel");
+  return RS_OK;
+}
+
+}  // namespace
+
+int pair_tile_rows(bool small) { return small ? Cfg<false, true>::PMv : Cfg<false, false>::PMv; }
+
 int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap* tmql, const CUtensorMap& tmc,
                            const CUtensorMap* tmcl, const float* qn, const float* cn, const float* cmin, int64_t nq,
-                           int64_t n, int dim, int k, int64_t id_base, const SearchPlan& plan, uint64_t* part,
-                           int32_t* counter, int32_t walk_bias, uint32_t* qtau, cudaStream_t st) {
+                           int64_t n, int dim, int k, int64_t id_base, const SearchPlan& plan, bool small,
+                           uint64_t* part, int32_t* counter, int32_t walk_bias, uint32_t* qtau, cudaStream_t st) {
   const bool tf = tmql != nullptr;
   RS_REQUIRE(tf == (tmcl != nullptr), "tf32 path needs both lo maps");
   RS_REQUIRE(!tf || G == 1, "the tf32 path has no multicast (RS_PAIR_GROUP) variant");
-  static bool attr_set[2] = {false, false};
-  if (!attr_set[tf]) {
-    if (tf)
-      RS_CHECK_CUDA(cudaFuncSetAttribute(score_topk_pair_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(Cfg<true>::SMEM_BYTES)),
-                    "cudaFuncSetAttribute(score_topk_pair_kernel<tf32>)");
-    else
-      RS_CHECK_CUDA(cudaFuncSetAttribute(score_topk_pair_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(Cfg<false>::SMEM_BYTES)),
-                    "cudaFuncSetAttribute(score_topk_pair_kernel<bf16>)");
-    attr_set[tf] = true;
-  }
+  RS_REQUIRE(!small || G == 1, "the M = 128 variant has no multicast (RS_PAIR_GROUP) variant");
+  RS_REQUIRE(plan.lists_per_seg == (small ? 2 : kPairEpiGroups), "plan lists per segment do not match the kernel");
   RS_REQUIRE(plan.segments >= 1 && plan.segments <= kMaxSegments, "segments out of range (%d)", plan.segments);
   RS_CHECK_CUDA(cudaMemsetAsync(counter, 0, sizeof(int32_t) * (1 + plan.segments), st),
                 "cudaMemsetAsync(unit counter, segment frontiers)");
@@ -612,8 +651,8 @@ int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap* tmql, cons
   p.kblocks = (dim + bk - 1) / bk;
   p.k = k;
   p.id_base = id_base;
-  // the plan counts cluster units (256*G query rows); the kernel works in
-  // 256-row pair tiles, padded to a multiple of G (pad rows are >= nq)
+  // the plan counts cluster units (G pair tiles); the kernel works in pair
+  // tiles, padded to a multiple of G (pad rows are >= nq)
   p.qtiles = plan.qtiles * G;
   p.segments = plan.segments;
   p.seg_rows = plan.seg_rows;
@@ -623,12 +662,12 @@ int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap* tmql, cons
   p.walk_bias = walk_bias;
   p.qtau = qtau;
   p.cunits = int64_t(plan.qtiles) * plan.segments;
-  if (tf)
-    score_topk_pair_kernel<true><<<CL * plan.ctas, NUM_THREADS, Cfg<true>::SMEM_BYTES, st>>>(tmq, *tmql, tmc, *tmcl, p);
-  else
-    score_topk_pair_kernel<false><<<CL * plan.ctas, NUM_THREADS, Cfg<false>::SMEM_BYTES, st>>>(tmq, tmq, tmc, tmc, p);
-  RS_CHECK_LAUNCH("score_topk_pair_kernel");
-  return RS_OK;
+  const CUtensorMap& ql = tf ? *tmql : tmq;
+  const CUtensorMap& cl = tf ? *tmcl : tmc;
+  if (tf) return small ? launch_t<true, true>(tmq, ql, tmc, cl, p, plan.ctas, st)
+                       : launch_t<true, false>(tmq, ql, tmc, cl, p, plan.ctas, st);
+  return small ? launch_t<false, true>(tmq, ql, tmc, cl, p, plan.ctas, st)
+               : launch_t<false, false>(tmq, ql, tmc, cl, p, plan.ctas, st);
 }
 
 }  // namespace rs

@@ -245,3 +245,25 @@ def test_wrapped_segment_walk_keeps_lower_id_ties(bias):
     D0, I0, _ = run_search(q, c, k, algo="tcgen05")
     np.testing.assert_array_equal(I0, I)
     np.testing.assert_array_equal(D0, D)
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("nq", [1, 37, 128])
+def test_small_batch_m128_tile(nq, dtype):
+    """nq <= 128 runs the CTA pair's M = 128 tile (two top-k lists per row and
+    segment, one per column half); duplicates + a forced wrap-around walk."""
+    n, d, k, base = 200_000, 256, 35, 100_003
+    q, c = make_data(nq, n, d, dtype, seed=nq)
+    c[base::89] = c[base]
+    q[0] = c[base]
+    ix = IndexFlatL2(d, dtype=dtype, capacity=n)
+    ix.set_walk_bias(5)
+    ix.add(c.cuda())
+    D, I = ix.search(q.cuda(), k)
+    torch.cuda.synchronize()
+    plan = ix.last_plan()
+    ix.close()
+    D, I = D.cpu().numpy(), I.cpu().numpy()
+    assert plan["algo"] == "tcgen05" and plan["qtiles"] == 1 and plan["segments"] > 1
+    np.testing.assert_array_equal(I[0], base + 89 * np.arange(k))
+    assert_parity(q, c, k, D, I, dtype)
