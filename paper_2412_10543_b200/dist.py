@@ -4,8 +4,10 @@ NVLink/NVSwitch) for the single exchange step.
 * Corpus sharding: rank r owns rows [r*N/P, (r+1)*N/P) with global ids
   starting at ``id_base = r*N/P``; every rank scores ALL queries against its
   shard (fused score + top-k) -> sorted top-k keys [nq, k] with global ids.
-* Exchange: ``all_gather_into_tensor`` of the keys (nq*k*8 bytes per rank;
-  3.4 MB at 8,192 x 35 + ...), the only collective of the path.
+* Exchange: ``all_to_all_single`` of the keys — rank r receives every
+  shard's list for its own query slice only (nq*k*8/P bytes from each peer;
+  2.3 MB out per rank at 8,192 x 35) — the only collective of the path
+  (``all_gather_into_tensor`` of the full key matrices is kept as an option).
 * Query sharding of the config stage: rank r gates the whole batch (the gate
   is order-dependent and O(nq)), selects its own query slice [q0, q1) and
   runs the k-way merge (K2) of the P shard lists for that slice, joined with
@@ -61,21 +63,36 @@ def gpu_ops(index, pipeline_params, window, *, threshold=0.90, default_space=Non
     return ShardOps(search_keys, gate, select, merge)
 
 
-def sharded_retrieve_select(ops: ShardOps, queries, profiles, qlen, free_bytes, k: int, *, group=None):
+def sharded_retrieve_select(ops: ShardOps, queries, profiles, qlen, free_bytes, k: int, *, group=None,
+                            exchange: str = "all_to_all"):
     """One batch through the sharded path on this rank.  All inputs are the
     full batch (replicated); returns (q0, q1, configs, D, I) for this rank's
-    query slice."""
+    query slice.
+
+    ``exchange="all_to_all"`` (default): each rank sends the keys of query
+    slice r to rank r only (``all_to_all_single``, nq*k*8 bytes out per rank,
+    and in: the P lists of its own slice).  ``"all_gather"``: every rank
+    receives every rank's full key matrix (P x more traffic)."""
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     nq = queries.shape[0]
-    keys = ops.search_keys(queries, k)                                  # [nq, k] local shard
-    gathered = torch.empty((world * nq, k), dtype=keys.dtype, device=keys.device)  # rank-major
-    dist.all_gather_into_tensor(gathered, keys.contiguous(), group=group)
-    spaces = ops.gate(profiles)                                         # full batch, in order
+    keys = ops.search_keys(queries, k).contiguous()                     # [nq, k] local shard
     q0, q1 = shard_range(nq, rank, world)
+    if exchange == "all_to_all":
+        sizes = [shard_range(nq, r, world)[1] - shard_range(nq, r, world)[0] for r in range(world)]
+        recv = torch.empty(((q1 - q0) * world, k), dtype=keys.dtype, device=keys.device)  # source-rank-major
+        dist.all_to_all_single(recv, keys, output_split_sizes=[q1 - q0] * world, input_split_sizes=sizes,
+                               group=group)
+        flat, stride = recv.reshape(-1), (q1 - q0) * k                  # list l of query q at l*nq_slice*k + (q-q0)*k
+    elif exchange == "all_gather":
+        gathered = torch.empty((world * nq, k), dtype=keys.dtype, device=keys.device)  # rank-major
+        dist.all_gather_into_tensor(gathered, keys, group=group)
+        flat, stride = gathered.reshape(-1)[q0 * k:], nq * k            # list l of query q at l*nq*k + (q-q0)*k
+    else:
+        raise ValueError(f"unknown exchange {exchange!r}")
+    spaces = ops.gate(profiles)                                         # full batch, in order
     configs = ops.select(spaces[q0:q1], profiles[q0:q1], qlen[q0:q1], free_bytes[q0:q1])
-    flat = gathered.reshape(-1)[q0 * k:]                                # list l of query q at l*nq*k + (q-q0)*k
-    D, I = ops.merge(flat, world, k, nq * k, q1 - q0, configs)
+    D, I = ops.merge(flat, world, k, stride, q1 - q0, configs)
     return q0, q1, configs, D, I
 
 

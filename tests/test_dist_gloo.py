@@ -97,7 +97,7 @@ class Sliceable:
         return (self.pr[s], self.conf[s])
 
 
-def worker(rank, world, port, out_q):
+def worker(rank, world, port, out_q, exchange="all_to_all"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     corpus, queries, prof, conf, qlen, free = data()
@@ -106,7 +106,8 @@ def worker(rank, world, port, out_q):
     ops_gate = ops.gate
     ops = rdist.ShardOps(ops.search_keys, lambda p: ops_gate((p.pr, p.conf)), ops.select, ops.merge)
     profiles = Sliceable(prof, conf)
-    q0, q1, cfg, Dm, Im = rdist.sharded_retrieve_select(ops, torch.from_numpy(queries), profiles, qlen, free, K)
+    q0, q1, cfg, Dm, Im = rdist.sharded_retrieve_select(ops, torch.from_numpy(queries), profiles, qlen, free, K,
+                                                        exchange=exchange)
     out_q.put((rank, q0, q1, cfg, Dm, Im))
     dist.destroy_process_group()
 
@@ -128,11 +129,12 @@ def test_shard_range_partitions_exactly():
 
 
 @pytest.mark.timeout(300)
-def test_two_rank_gloo_matches_single_process():
+@pytest.mark.parametrize("exchange", ["all_to_all", "all_gather"])
+def test_two_rank_gloo_matches_single_process(exchange):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = free_port()
-    procs = [ctx.Process(target=worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=worker, args=(r, 2, port, q, exchange)) for r in range(2)]
     for p in procs:
         p.start()
     results = sorted([q.get(timeout=240) for _ in range(2)], key=lambda t: t[0])

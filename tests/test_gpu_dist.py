@@ -1,5 +1,5 @@
 """The sharded path's GPU ops (fused search on a shard with global ids, the
-NCCL all-gather, query-slice select, k-way merge + join) on one B200: a
+NCCL all-to-all (or all-gather) exchange, query-slice select, k-way merge + join) on one B200: a
 single-rank NCCL group runs the exact code bench.py runs per rank under
 torchrun, and must equal the single-index pipeline."""
 
@@ -37,7 +37,8 @@ def nccl_group():
     dist.destroy_process_group()
 
 
-def test_sharded_path_equals_single_index(nccl_group):
+@pytest.mark.parametrize("exchange", ["all_to_all", "all_gather"])
+def test_sharded_path_equals_single_index(nccl_group, exchange):
     dev = torch.device("cuda", 0)
     nq, n, d, k = 500, 30_000, 256, 35
     g = torch.Generator().manual_seed(4)
@@ -56,7 +57,7 @@ def test_sharded_path_equals_single_index(nccl_group):
     ix = IndexFlatL2(d, capacity=n, id_base=base)
     ix.add(corpus.to(dev))
     ops = rdist.gpu_ops(ix, params, batch.GateWindow(dev))
-    q0, q1, cfg, D, I = rdist.sharded_retrieve_select(ops, queries, profiles, qlen, free, k)
+    q0, q1, cfg, D, I = rdist.sharded_retrieve_select(ops, queries, profiles, qlen, free, k, exchange=exchange)
     torch.cuda.synchronize()
     assert (q0, q1) == (0, nq)
 
