@@ -279,10 +279,16 @@ int rs_admit_fifo(const rs_space* spaces, const rs_profile* profiles, const uint
  * `dtype` plus fp32 squared norms.  Search returns, per query, the k smallest
  * D = ||q||^2 + ||c||^2 - 2<q,c> (fp32 accumulate, clamped at 0), ascending,
  * ties to the lower chunk id; missing entries are I = -1, D = +inf.
- * Chunk ids are id_base + row (id_base = the shard's first global id). */
+ * Chunk ids are id_base + row (id_base = the shard's first global id).
+ * An index handle owns its search workspace (partial lists, query norms, the
+ * kernel's unit counter and shared thresholds): searches on ONE handle must be
+ * ordered on one stream (or synchronised); use one handle per concurrent
+ * stream.  Distinct handles are independent. */
 enum rs_dtype { RS_F32 = 0, RS_BF16 = 1 };
-/* RS_ALGO_TCGEN05: CTA-pair tcgen05 kernel (default for bf16);
- * RS_ALGO_TCGEN05_1SM: single-CTA tcgen05 kernel; RS_ALGO_SIMT: CUDA cores. */
+/* RS_ALGO_TCGEN05: CTA-pair tcgen05 kernel (default: bf16, or 3xTF32 + an
+ * exact fp32 re-rank for an fp32 corpus; an M = 128 pair tile for nq <= 128);
+ * RS_ALGO_TCGEN05_1SM: single-CTA tcgen05 kernel (bf16); RS_ALGO_SIMT: CUDA
+ * cores (also k > 40). */
 enum rs_algo { RS_ALGO_AUTO = 0, RS_ALGO_SIMT = 1, RS_ALGO_TCGEN05 = 2, RS_ALGO_TCGEN05_1SM = 3 };
 
 typedef struct rs_index rs_index;
