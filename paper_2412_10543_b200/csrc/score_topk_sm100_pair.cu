@@ -358,10 +358,16 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             (void)full_leader;
             if (leader) mbar_arrive(&tail->full[stage]);
 #else
-            if (leader) mbar_arrive_expect_tx(&tail->full[stage], 2 * C::STAGE_BYTES);
             const int32_t kx = kb * C::BK;
             const int32_t qrow0 = qt * C::PMv + int(half) * C::BMv;
+#ifdef RS_EXP_HALF_A  // timing experiment only (wrong results): the query tile is reloaded every other tile
+            const bool load_a = (j & 1) == 0;
+            if (leader) mbar_arrive_expect_tx(&tail->full[stage], 2 * (C::STAGE_BYTES - (load_a ? 0 : C::A_BYTESv)));
+            if (load_a) tma_load_2d_pair(&tmq, full_leader, sa, kx, qrow0, pol_q);
+#else
+            if (leader) mbar_arrive_expect_tx(&tail->full[stage], 2 * C::STAGE_BYTES);
             tma_load_2d_pair(&tmq, full_leader, sa, kx, qrow0, pol_q);
+#endif
             if (TF) tma_load_2d_pair(&tmql, full_leader, sa + C::A_BYTESv, kx, qrow0, pol_q);
             if (G == 1) {
 #ifdef RS_EXP_L2_CORPUS_ROWS  // timing experiment only (wrong results): corpus reads wrap in an L2-sized window

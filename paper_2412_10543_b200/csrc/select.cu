@@ -23,6 +23,8 @@ struct SelConst {
   int64_t pt;        // per-token bytes
   int64_t C, T, O;   // chunk size, template tokens, out budget
   int64_t tok_limit; // largest token count whose 102*tok*pt+99 fits int64
+  int64_t pa;        // 102*pt = 100*pa + pb (the fast exact form of buffered())
+  int32_t pb;
   int32_t max_chunks, cstep, istep, allow_fallback;
   int32_t has_cost;
   double a, b, s;    // CostModel
@@ -30,6 +32,14 @@ struct SelConst {
 
 __device__ __forceinline__ int64_t buffered(int64_t tokens, int64_t pt) {
   return (102 * tokens * pt + 99) / 100;  // memory.py:76-78
+}
+
+// The same value without a 64-bit division: with 102*pt = 100*pa + pb,
+// (102*pt*t + 99) / 100 = pa*t + (pb*t + 99) / 100 exactly (100*pa*t is a
+// multiple of 100); pb*t + 99 fits uint32 for t < kFastTok.
+constexpr int64_t kFastTok = 20000000;
+__device__ __forceinline__ int64_t buffered_fast(int32_t t, int64_t pa, int32_t pb) {
+  return pa * int64_t(t) + int64_t((uint32_t(pb) * uint32_t(t) + 99u) / 100u);
 }
 
 // sim.py:84-92 in the reference's IEEE-double evaluation order, no FMA.
@@ -91,12 +101,18 @@ struct Grid {
 
 // int64 range guard: a conservative bound over every candidate and the
 // fallback; true = the query's byte arithmetic could overflow.
-__device__ __forceinline__ bool range_overflow(const Grid& gr, int64_t q, const SelConst& P) {
+__device__ __forceinline__ int64_t query_tmax(const Grid& gr, int64_t q, const SelConst& P) {
   const int64_t nmax = gr.n_hi > P.max_chunks ? gr.n_hi : P.max_chunks;
   const int64_t per = P.C > gr.il_hi ? P.C : gr.il_hi;
   const int64_t tail = P.O > gr.il_hi ? P.O : gr.il_hi;
-  const int64_t tmax = q + nmax * per + P.T + tail;
-  bool bad = nmax > 65535 || per > (int64_t(1) << 30) || q > (int64_t(1) << 40) || tmax > P.tok_limit;
+  return q + nmax * per + P.T + tail;  // bounds every token count of the query's candidates and fallback
+}
+__device__ __forceinline__ bool range_overflow(const Grid& gr, int64_t q, const SelConst& P) {
+  const int64_t nmax = gr.n_hi > P.max_chunks ? gr.n_hi : P.max_chunks;
+  const int64_t per = P.C > gr.il_hi ? P.C : gr.il_hi;
+  const int64_t tmax = query_tmax(gr, q, P);
+  bool bad = nmax > 65535 || per > (int64_t(1) << 30) || q > (int64_t(1) << 40) || tmax > P.tok_limit ||
+             gr.G >= (int64_t(1) << 30);  // grid indices are int32 in the scan
   if (!bad) bad = buffered(tmax, P.pt) > (int64_t)(INT64_MAX / 2) / (nmax + 1);
   return bad;
 }
@@ -105,31 +121,71 @@ __device__ __forceinline__ bool range_overflow(const Grid& gr, int64_t q, const 
 // (bytes, grid index) over the candidates with bytes <= fr.  On a fit sets
 // c.{method,num_chunks,interlen,kv_bytes} and status BEST_FIT; returns false
 // (c untouched) when nothing fits.
-__device__ __forceinline__ bool best_fit_warp(const Grid& gr, int64_t q, int64_t fr, const SelConst& P, int lane,
-                                              rs_config& c) {
-  const int64_t rr_call = buffered(q + P.C + P.T + P.O, P.pt);  // one rerank call
-  int64_t best_b = -1;
-  int32_t best_g = -1;
-  for (int64_t g = lane; g < gr.G; g += 32) {
-    int64_t bytes;
-    if (g < gr.n_rr) {
-      const int64_t nc = gr.n_lo + g * P.cstep;
-      bytes = nc * rr_call;
-    } else if (g < gr.n_rr + gr.n_st) {
-      const int64_t nc = gr.n_lo + (g - gr.n_rr) * P.cstep;
-      bytes = buffered(q + nc * P.C + P.T + P.O, P.pt);
-    } else {
-      const int64_t r = g - gr.n_rr - gr.n_st;
-      const int64_t i_n = r / gr.ni;
-      const int64_t nc = gr.n_lo + i_n * P.cstep;
-      const int64_t il = gr.il_lo + (r - i_n * gr.ni) * P.istep;
-      bytes = nc * buffered(q + P.C + P.T + il, P.pt) + buffered(q + nc * il + P.T + P.O, P.pt);
-    }
-    if (bytes <= fr && bytes >= best_b) {  // g ascends per lane: ties -> later g
+//
+// Each lane walks its grid indices g = lane, lane + 32, ... in increasing
+// order through the three method blocks (so ">=" keeps the later g on byte
+// ties); the map_reduce block is walked as (i_n, i_il) with an incremental
+// carry instead of a per-candidate division, and token counts below
+// kFastTok use the division-free buffered_fast.
+template <bool FAST>
+__device__ __forceinline__ void best_fit_scan(const Grid& gr, int64_t q, int64_t fr, const SelConst& P, int lane,
+                                              int64_t& best_b, int32_t& best_g) {
+  auto buf = [&](int64_t t) -> int64_t {
+    if constexpr (FAST) return buffered_fast(int32_t(t), P.pa, P.pb);
+    else return buffered(t, P.pt);
+  };
+  const int64_t rr_call = buf(q + P.C + P.T + P.O);  // one rerank call
+  const int32_t nn = int32_t(gr.nn);
+  // map_rerank block: g = i
+  for (int32_t i = lane; i < int32_t(gr.n_rr); i += 32) {
+    const int64_t bytes = (gr.n_lo + int64_t(i) * P.cstep) * rr_call;
+    if (bytes <= fr && bytes >= best_b) {
       best_b = bytes;
-      best_g = (int32_t)g;
+      best_g = i;
     }
   }
+  // stuff block: g = n_rr + i
+  for (int32_t i = lane; i < int32_t(gr.n_st); i += 32) {
+    const int64_t nc = gr.n_lo + int64_t(i) * P.cstep;
+    const int64_t bytes = buf(q + nc * P.C + P.T + P.O);
+    if (bytes <= fr && bytes >= best_b) {
+      best_b = bytes;
+      best_g = int32_t(gr.n_rr) + i;
+    }
+  }
+  // map_reduce block: g = n_rr + n_st + i_n * ni + i_il
+  const int32_t ni = int32_t(gr.ni);
+  const int32_t n_mr = nn * ni;
+  if (n_mr > 0) {
+    const int32_t off = int32_t(gr.n_rr + gr.n_st);
+    const int32_t dn = 32 / ni, dil = 32 % ni;  // per-step carry of (i_n, i_il)
+    int32_t i_n = lane / ni, i_il = lane % ni;
+    for (int32_t r = lane; r < n_mr; r += 32) {
+      const int64_t nc = gr.n_lo + int64_t(i_n) * P.cstep;
+      const int64_t il = gr.il_lo + int64_t(i_il) * P.istep;
+      const int64_t bytes = nc * buf(q + P.C + P.T + il) + buf(q + nc * il + P.T + P.O);
+      if (bytes <= fr && bytes >= best_b) {
+        best_b = bytes;
+        best_g = off + r;
+      }
+      i_n += dn;
+      i_il += dil;
+      if (i_il >= ni) {
+        i_il -= ni;
+        ++i_n;
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ bool best_fit_warp(const Grid& gr, int64_t q, int64_t fr, const SelConst& P, int lane,
+                                              rs_config& c) {
+  int64_t best_b = -1;
+  int32_t best_g = -1;
+  if (query_tmax(gr, q, P) < kFastTok)  // warp-uniform
+    best_fit_scan<true>(gr, q, fr, P, lane, best_b, best_g);
+  else
+    best_fit_scan<false>(gr, q, fr, P, lane, best_b, best_g);
   warp_argmax(best_b, best_g);
   if (best_g < 0) return false;
   gr.decode(best_g, P, c);
@@ -220,28 +276,29 @@ __global__ void __launch_bounds__(256) select_kernel(const rs_space* __restrict_
 
   if (lane == 0) out[qi] = c;
 
-  if (P.has_cost && lane == 0) {
+  if (P.has_cost) {
     // Critical-path delay of the admitted plan (plan_calls memory.py:117-148,
     // sim.dispatch concurrency sim.py:226-228): j-th independent call runs
     // with running_before + j sequences; a reducer waits for its mappers and
-    // then runs with running_before.
+    // then runs with running_before.  Lanes take calls j = lane, lane + 32..;
+    // the max is exact in any order, so the warp reduction is bit-identical
+    // to the sequential scan.
     double d = 0.0;
     if (c.status == RS_SELECT_BEST_FIT || c.status == RS_SELECT_FALLBACK) {
       const int64_t c0 = running ? running[qi] : 0;
       const int64_t nc = c.num_chunks;
       if (c.method == RS_STUFF) {
-        d = fmax(d, call_latency(q + nc * P.C + P.T, P.O, c0, P.a, P.b, P.s));
-      } else if (c.method == RS_MAP_RERANK) {
-        for (int64_t j = 0; j < nc; ++j)
-          d = fmax(d, call_latency(q + P.C + P.T, P.O, c0 + j, P.a, P.b, P.s));
+        d = call_latency(q + nc * P.C + P.T, P.O, c0, P.a, P.b, P.s);
       } else {
-        const int64_t il = c.interlen;
-        for (int64_t j = 0; j < nc; ++j)
-          d = fmax(d, call_latency(q + P.C + P.T, il, c0 + j, P.a, P.b, P.s));
-        d = __dadd_rn(d, call_latency(q + nc * il + P.T, P.O, c0, P.a, P.b, P.s));
+        const int64_t out = c.method == RS_MAP_RERANK ? P.O : int64_t(c.interlen);
+        for (int64_t j = lane; j < nc; j += 32) d = fmax(d, call_latency(q + P.C + P.T, out, c0 + j, P.a, P.b, P.s));
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) d = fmax(d, __shfl_xor_sync(0xffffffffu, d, off));
+        if (c.method == RS_MAP_REDUCE)
+          d = __dadd_rn(d, call_latency(q + nc * int64_t(c.interlen) + P.T, P.O, c0, P.a, P.b, P.s));
       }
     }
-    delay[qi] = d;
+    if (lane == 0) delay[qi] = d;
   }
 }
 
@@ -443,6 +500,8 @@ int make_const(const rs_select_params* p, const rs_cost_model* cost, SelConst* o
   c.T = p->template_tokens;
   c.O = p->out_budget;
   c.tok_limit = (INT64_MAX - 99) / (102 * c.pt);
+  c.pa = (102 * c.pt) / 100;
+  c.pb = int32_t((102 * c.pt) % 100);
   c.max_chunks = p->max_chunks;
   c.cstep = p->chunk_step;
   c.istep = p->interlen_step;
