@@ -267,3 +267,37 @@ def test_small_batch_m128_tile(nq, dtype):
     assert plan["algo"] == "tcgen05" and plan["qtiles"] == 1 and plan["segments"] > 1
     np.testing.assert_array_equal(I[0], base + 89 * np.arange(k))
     assert_parity(q, c, k, D, I, dtype)
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_incremental_adds_and_reset(dtype):
+    """Rows appended in ragged pieces (partial 32-row norm chunks, the
+    epilogue's dot bound must be recomputed for them) search exactly like one
+    add; reset() empties the index for reuse."""
+    nq, n, d, k = 300, 20_011, 128, 35
+    q, c = make_data(nq, n, d, dtype, seed=13)
+    # make the late rows the near neighbours, with norms below the early chunk minima
+    c[n - 500:] *= 0.5
+    q[: nq // 2] = c[n - 500: n - 500 + nq // 2] * 1.01
+    ix = IndexFlatL2(d, dtype=dtype, capacity=n)
+    for lo, hi in ((0, 1000), (1000, 1001), (1001, 7777), (7777, n - 500), (n - 500, n - 37), (n - 37, n)):
+        ix.add(c[lo:hi].cuda())
+    D, I = ix.search(q.cuda(), k)
+    D, I = D.cpu().numpy(), I.cpu().numpy()
+    assert_parity(q, c, k, D, I, dtype)
+    D1, I1, _ = run_search(q, c, k)
+    np.testing.assert_array_equal(I, I1)
+    ix.reset()
+    ix.add(c[:5000].cuda())
+    D2, I2 = ix.search(q.cuda(), k)
+    assert_parity(q, c[:5000], k, D2.cpu().numpy(), I2.cpu().numpy(), dtype)
+    ix.close()
+
+
+def test_ids_near_the_uint32_limit():
+    nq, n, d, k = 64, 3000, 64, 20
+    q, c = make_data(nq, n, d, torch.bfloat16, seed=2)
+    base = (1 << 32) - 2 - n
+    D, I, _ = run_search(q, c, k, id_base=base)
+    assert I.max() < (1 << 32) - 1 and I.min() >= base
+    assert_parity(q, c, k, D, I, torch.bfloat16, id_base=base)
