@@ -54,7 +54,6 @@ using namespace sm100;
 #endif
 
 constexpr int BM = 128;         // query rows per CTA (TMEM lanes)
-constexpr int PM = 2 * BM;      // query rows per pair tile
 constexpr int BN = kTcBN;       // corpus columns per tile (both CTAs)
 constexpr int HB = BN / 2;      // corpus rows staged per CTA
 #ifndef RS_PAIR_STAGES_TF32
@@ -67,7 +66,6 @@ constexpr int BUF = RS_PAIR_BUF;
 constexpr int CHECK = 8;
 constexpr int EPI_COLS = 32;    // TMEM columns per tcgen05.ld / wait
 constexpr int ROW_BYTES = 128;  // one SWIZZLE_128B row of a k-block (64 bf16 / 32 fp32)
-constexpr int A_BYTES = BM * ROW_BYTES;
 constexpr int B_BYTES = HB * ROW_BYTES;
 constexpr int TMEM_COLS = 2 * BN;
 constexpr int EG = kPairEpiGroups;       // epilogue warp groups (column slices)
@@ -321,13 +319,6 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           if (u >= 0) {
             const int64_t uu = int64_t(u) * G;
             start = ld_relaxed_gpu_s32(p.seg_pos + uu / p.qtiles) + p.walk_bias * int32_t(uu % p.qtiles + 1);
-#ifdef RS_EXP_NO_FRONTIER  // timing experiment: ascending walk from tile 0
-            start = 0;
-#endif
-#ifdef RS_EXP_STAGGER  // timing experiment: join RS_EXP_STAGGER*(qt%8) tiles behind the frontier
-            start -= RS_EXP_STAGGER * int32_t(uu % 8);
-            if (start < 0) start = 0;
-#endif
           }
           tail->uid[slot] = u;
           tail->ustart[slot] = start;
@@ -353,11 +344,6 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             PROF(0, mbar_wait(&tail->empty[stage], phase ^ 1));
             uint8_t* sa = smem + size_t(stage) * C::STAGE_BYTES;
             const uint32_t full_leader = mapa_shared(smem_u32(&tail->full[stage]), pair_leader);
-#ifdef RS_PAIR_NO_TMA  // timing experiment only: MMA pipeline with no operand traffic
-            (void)sa;
-            (void)full_leader;
-            if (leader) mbar_arrive(&tail->full[stage]);
-#else
             const int32_t kx = kb * C::BK;
             const int32_t qrow0 = qt * C::PMv + int(half) * C::BMv;
 #ifdef RS_EXP_HALF_A  // timing experiment only (wrong results): the query tile is reloaded every other tile
@@ -383,7 +369,6 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
               tma_load_2d_pair_mc(&tmc, full_leader, sa + C::OFF_B + pp * BPIECE * ROW_BYTES, kx,
                                   int32_t(c0) + int(half) * HB + pp * BPIECE, mc_half, pol_c);
             }
-#endif
             if (++stage == STAGES) {
               stage = 0;
               phase ^= 1;
@@ -516,7 +501,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           uint32_t r[EPI_COLS];
           __syncwarp();
           tmem_ld_32x32b_x32(t_row + base, r);
-          // this chunk's dot bound (epi_group8b), selected while the load is in flight
+          // this chunk's dot bound (epi_chunk32b), selected while the load is in flight
           const int ci = base >> 5;
           const float4 ch = ci < 4 ? cm0 : cm1;
           const int cj = ci & 3;
@@ -532,23 +517,10 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           if (__uint_as_float(r[0]) == 12345.0f) rt.append_raw(0.0f, id0);
           continue;
 #endif
-#ifdef RS_PAIR_EPI_GROUP_VOTE  // variant: one vote + branch per 8-column group
-          if (base + EPI_COLS <= valid) {
-#pragma unroll
-            for (int g = 0; g < EPI_COLS; g += 8)
-              epi_group8b<KREG, EPI_THREADS, BUF, CHECK, true>(rt, r + g, cn_t + base + g, id0 + base + g, 8, thr);
-          } else {
-#pragma unroll
-            for (int g = 0; g < EPI_COLS; g += 8)
-              epi_group8b<KREG, EPI_THREADS, BUF, CHECK, false>(rt, r + g, cn_t + base + g, id0 + base + g,
-                                                       valid - base - g, thr);
-          }
-#else
           if (base + EPI_COLS <= valid)
             epi_chunk32b<KREG, EPI_THREADS, BUF, CHECK, true>(rt, r, cn_t + base, id0 + base, EPI_COLS, thr);
           else
             epi_chunk32b<KREG, EPI_THREADS, BUF, CHECK, false>(rt, r, cn_t + base, id0 + base, valid - base, thr);
-#endif
         }
 #ifndef RS_PAIR_NO_SHARED_TAU
         if ((j & 3) == 0 && real_row) {

@@ -176,69 +176,6 @@ __device__ __forceinline__ void epi_group8(RowTopK<ROWS, BUF>& rt, const uint32_
   }
 }
 
-// Packed-pair variant: the exact distances of 8 columns with 4 FADD2 + 4 FFMA2
-// (|q|^2 + |c|^2 pairs, then -2<q,c> + that), min-folded to one compare; the
-// slow path (some lane of the warp has a candidate — frequent at warp scale,
-// rare per lane) is 3 predicated instructions per column: compare, store
-// through the write pointer, bump the pointer.  Distances are bit-identical
-// to epi_group8 (same fl(fl(qn + cn) - 2s) rounding, clamp at flush).
-template <int ROWS, int BUF, int CHECK, bool FULL>
-__device__ __forceinline__ void epi_group8x(RowTopK<ROWS, BUF>& rt, const uint32_t* r, const float* cn,
-                                            uint32_t id, int lim) {
-  static_assert(BUF >= CHECK, "buffer must hold one group");
-  const float4 a = *reinterpret_cast<const float4*>(cn);
-  const float4 b = *reinterpret_cast<const float4*>(cn + 4);
-  const float2 q2 = make_float2(rt.qn, rt.qn);
-  const float2 m2 = make_float2(-2.0f, -2.0f);
-  const float2 e0 = __ffma2_rn(make_float2(__uint_as_float(r[0]), __uint_as_float(r[1])), m2,
-                               __fadd2_rn(q2, make_float2(a.x, a.y)));
-  const float2 e1 = __ffma2_rn(make_float2(__uint_as_float(r[2]), __uint_as_float(r[3])), m2,
-                               __fadd2_rn(q2, make_float2(a.z, a.w)));
-  const float2 e2 = __ffma2_rn(make_float2(__uint_as_float(r[4]), __uint_as_float(r[5])), m2,
-                               __fadd2_rn(q2, make_float2(b.x, b.y)));
-  const float2 e3 = __ffma2_rn(make_float2(__uint_as_float(r[6]), __uint_as_float(r[7])), m2,
-                               __fadd2_rn(q2, make_float2(b.z, b.w)));
-  const float e[8] = {e0.x, e0.y, e1.x, e1.y, e2.x, e2.y, e3.x, e3.y};
-  float mn = __int_as_float(0x7f800000);
-#pragma unroll
-  for (int j = 0; j < 8; ++j)
-    if (FULL || j < lim) mn = fminf(mn, e[j]);
-  if (__any_sync(0xffffffffu, mn <= rt.tau)) {
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-      if ((FULL || j < lim) && e[j] <= rt.tau) rt.append_raw(e[j], id + j);
-    if (__any_sync(0xffffffffu, rt.buffered() > BUF - CHECK)) rt.flush();
-  }
-}
-
-// Branch-free variant: at warp scale nearly every 8-column group holds some
-// lane's candidate (k ln(n/k) hits per row over n columns, x 32 rows), so the
-// vote + slow path of epi_group8x is almost always taken; here every column
-// is compare + predicated store + predicated pointer bump, with one warp vote
-// per group only for the (rare) buffer flush.
-template <int ROWS, int BUF, int CHECK, bool FULL>
-__device__ __forceinline__ void epi_group8p(RowTopK<ROWS, BUF>& rt, const uint32_t* r, const float* cn,
-                                            uint32_t id, int lim) {
-  static_assert(BUF >= CHECK, "buffer must hold one group");
-  const float4 a = *reinterpret_cast<const float4*>(cn);
-  const float4 b = *reinterpret_cast<const float4*>(cn + 4);
-  const float2 q2 = make_float2(rt.qn, rt.qn);
-  const float2 m2 = make_float2(-2.0f, -2.0f);
-  const float2 e0 = __ffma2_rn(make_float2(__uint_as_float(r[0]), __uint_as_float(r[1])), m2,
-                               __fadd2_rn(q2, make_float2(a.x, a.y)));
-  const float2 e1 = __ffma2_rn(make_float2(__uint_as_float(r[2]), __uint_as_float(r[3])), m2,
-                               __fadd2_rn(q2, make_float2(a.z, a.w)));
-  const float2 e2 = __ffma2_rn(make_float2(__uint_as_float(r[4]), __uint_as_float(r[5])), m2,
-                               __fadd2_rn(q2, make_float2(b.x, b.y)));
-  const float2 e3 = __ffma2_rn(make_float2(__uint_as_float(r[6]), __uint_as_float(r[7])), m2,
-                               __fadd2_rn(q2, make_float2(b.z, b.w)));
-  const float e[8] = {e0.x, e0.y, e1.x, e1.y, e2.x, e2.y, e3.x, e3.y};
-#pragma unroll
-  for (int j = 0; j < 8; ++j)
-    if ((FULL || j < lim) && e[j] <= rt.tau) rt.append_raw(e[j], id + j);
-  if (__any_sync(0xffffffffu, rt.buffered() > BUF - CHECK)) rt.flush();
-}
-
 // ---------------------------------------------------------------------------
 // Register-resident streaming top-k (the CTA-pair kernel's epilogue state).
 //
@@ -366,18 +303,14 @@ struct RegTopK {
   }
 };
 
-// Branch-free fast path over 8 columns for RegTopK (see epi_group8p).
+// Exact distances and predicated appends of 8 columns for RegTopK (the slow
+// path of epi_chunk32b).
 template <int KREG, int ROWS, int BUF, int CHECK, bool FULL>
 __device__ __forceinline__ void epi_group8r(RegTopK<KREG, ROWS, BUF>& rt, const uint32_t* r, const float* cn,
                                             uint32_t id, int lim) {
   static_assert(BUF >= CHECK, "buffer must hold one group");
-#ifdef RS_EXP_NO_CN_LDS  // timing experiment only (wrong results): no corpus-norm smem reads
-  const float4 a = make_float4(1.0f, 1.0f, 1.0f, 1.0f), b = a;
-  (void)cn;
-#else
   const float4 a = *reinterpret_cast<const float4*>(cn);
   const float4 b = *reinterpret_cast<const float4*>(cn + 4);
-#endif
   const float2 q2 = make_float2(rt.qn, rt.qn);
   const float2 m2 = make_float2(-2.0f, -2.0f);
   const float2 e0 = __ffma2_rn(make_float2(__uint_as_float(r[0]), __uint_as_float(r[1])), m2,
@@ -389,20 +322,13 @@ __device__ __forceinline__ void epi_group8r(RegTopK<KREG, ROWS, BUF>& rt, const 
   const float2 e3 = __ffma2_rn(make_float2(__uint_as_float(r[6]), __uint_as_float(r[7])), m2,
                                __fadd2_rn(q2, make_float2(b.z, b.w)));
   const float e[8] = {e0.x, e0.y, e1.x, e1.y, e2.x, e2.y, e3.x, e3.y};
-#ifdef RS_EXP_NO_APPEND  // timing experiment only (wrong results): filter math, no candidates
-  float m = e[0];
-#pragma unroll
-  for (int j = 1; j < 8; ++j) m = fminf(m, e[j]);
-  if (m == -12345.0f) rt.append_raw(m, id);
-  return;
-#endif
 #pragma unroll
   for (int j = 0; j < 8; ++j)
     if ((FULL || j < lim) && e[j] <= rt.tau) rt.append_raw(e[j], id + j);
   if (__any_sync(0xffffffffu, rt.buffered() > BUF - CHECK)) rt.flush();
 }
 
-// Bound-filtered variant.  For the columns of a 32-column chunk,
+// Bound-filtered epilogue (epi_chunk32b below).  For the columns of a 32-column chunk,
 //   e_j = |q|^2 + |c_j|^2 - 2<q,c_j>  >=  |q|^2 + min_chunk|c|^2 - 2<q,c_j>,
 // so e_j <= tau needs <q,c_j> >= thr = (|q|^2 + min|c|^2 - tau) / 2 (minus a
 // rounding margin, chunk_threshold).  The fast path is therefore the raw TMEM
@@ -410,18 +336,6 @@ __device__ __forceinline__ void epi_group8r(RegTopK<KREG, ROWS, BUF>& rt, const 
 // where some lane of the warp passes compute the exact distances (the same
 // FADD2/FFMA2 rounding as epi_group8r) and append.  With normalised corpora
 // the bound is tight; otherwise it is looser but never drops a candidate.
-template <int KREG, int ROWS, int BUF, int CHECK, bool FULL>
-__device__ __forceinline__ void epi_group8b(RegTopK<KREG, ROWS, BUF>& rt, const uint32_t* r, const float* cn,
-                                            uint32_t id, int lim, float thr) {
-  static_assert(BUF >= CHECK, "buffer must hold one group");
-  float m = __uint_as_float(r[0]);
-#pragma unroll
-  for (int j = 1; j < 8; ++j)
-    if (FULL || j < lim) m = fmaxf(m, __uint_as_float(r[j]));
-  if (!__any_sync(0xffffffffu, m >= thr)) return;
-  epi_group8r<KREG, ROWS, BUF, CHECK, FULL>(rt, r, cn, id, lim);
-}
-
 // A whole 32-column TMEM chunk through the dot bound: four independent 8-way
 // max trees, four votes, and a single branch in the common case that no lane
 // of the warp has a candidate anywhere in the chunk (a one-warp-per-SMSP
@@ -454,7 +368,7 @@ __device__ __forceinline__ void epi_chunk32b(RegTopK<KREG, ROWS, BUF>& rt, const
 }
 
 // Dot threshold of a chunk whose smallest corpus norm is cmin (see
-// epi_group8b); +inf tau (list not full) gives -inf: everything passes.  The
+// epi_chunk32b); +inf tau (list not full) gives -inf: everything passes.  The
 // margin covers the fp32 rounding of both this bound and the exact distance.
 __device__ __forceinline__ float chunk_threshold(float qn, float cmin, float tau) {
   const float t = 0.5f * (qn + cmin - tau);
