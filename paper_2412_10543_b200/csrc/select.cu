@@ -240,7 +240,10 @@ __device__ __forceinline__ void fallback_warp(bool joint, int64_t q, int64_t fr,
   }
 }
 
-__global__ void __launch_bounds__(256) select_kernel(const rs_space* __restrict__ spaces,
+#ifndef RS_SELECT_MIN_BLOCKS
+#define RS_SELECT_MIN_BLOCKS 4  // <= 64 registers: 4 blocks of 256 per SM (issue-bound kernel)
+#endif
+__global__ void __launch_bounds__(256, RS_SELECT_MIN_BLOCKS) select_kernel(const rs_space* __restrict__ spaces,
                                                      const rs_profile* __restrict__ profiles,
                                                      const int32_t* __restrict__ qlen,
                                                      const int64_t* __restrict__ free_bytes, int64_t n,
