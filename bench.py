@@ -131,7 +131,14 @@ class ClockSampler:
 
             nv.nvmlInit()
             self.nv = nv
-            self.h = [nv.nvmlDeviceGetHandleByIndex(g) for g in self.gpus]
+            self.h = []
+            for g in self.gpus:  # skip indices this node does not have
+                try:
+                    self.h.append(nv.nvmlDeviceGetHandleByIndex(g))
+                except Exception:
+                    pass
+            if not self.h:
+                raise RuntimeError("no NVML device")
             self.bits = (nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
                          nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap)
             self.smax = float(nv.nvmlDeviceGetMaxClockInfo(self.h[0], nv.NVML_CLOCK_SM))
@@ -266,8 +273,10 @@ def main():
     from paper_2412_10543_b200.pipeline import RetrieveSelect
     from paper_2412_10543_b200.retriever import IndexFlatL2
 
-    rank, world = rdist.init_from_env("nccl")
-    local = int(os.environ.get("LOCAL_RANK", rank))
+    # RS_BENCH_BACKEND / RS_BENCH_DEVICE: plumbing checks only (e.g. two ranks
+    # sharing one GPU over gloo); the measured configuration is NCCL, one GPU per rank
+    rank, world = rdist.init_from_env(os.environ.get("RS_BENCH_BACKEND", "nccl"))
+    local = int(os.environ.get("RS_BENCH_DEVICE", os.environ.get("LOCAL_RANK", rank)))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     nq, n, d = cfg["nq"], cfg["n"], cfg["d"]

@@ -107,6 +107,6 @@ def init_from_env(backend: str | None = None):
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     backend = backend or ("nccl" if torch.cuda.is_available() else "gloo")
     if backend == "nccl":
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
+        torch.cuda.set_device(int(os.environ.get("RS_BENCH_DEVICE", os.environ.get("LOCAL_RANK", rank))))
     dist.init_process_group(backend, rank=rank, world_size=world)
     return rank, world
