@@ -304,10 +304,13 @@ def main():
         del blk, rows
     torch.cuda.synchronize()
     if world > 1:
-        parts = [torch.empty(rdist.shard_range(nq, r, world)[1] - rdist.shard_range(nq, r, world)[0], d,
-                             device=dev) for r in range(world)]
-        dist.all_gather(parts, q_local.contiguous())
-        queries = torch.cat(parts).to(tdtype)
+        # slices may differ by one row: gather equal padded blocks, then trim
+        sizes = [rdist.shard_range(nq, r, world)[1] - rdist.shard_range(nq, r, world)[0] for r in range(world)]
+        pad = torch.zeros(max(sizes), d, device=dev)
+        pad[:nql] = q_local
+        parts = [torch.empty(max(sizes), d, device=dev) for _ in range(world)]
+        dist.all_gather(parts, pad)
+        queries = torch.cat([p_[:sz] for p_, sz in zip(parts, sizes)]).to(tdtype)
     else:
         queries = q_local.to(tdtype)
 
