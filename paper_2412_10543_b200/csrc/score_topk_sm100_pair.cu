@@ -64,7 +64,10 @@ constexpr int KREG = kTcMaxK;   // register top-k capacity (k <= 40)
 // than BUF - CHECK entries, so every flush batches many candidates per lane
 constexpr int BUF = RS_PAIR_BUF;
 constexpr int CHECK = 8;
-constexpr int EPI_COLS = 32;    // TMEM columns per tcgen05.ld / wait
+constexpr int EPI_COLS = 32;    // TMEM columns per tcgen05.ld
+#ifndef RS_PAIR_EPI_PAIRED
+#define RS_PAIR_EPI_PAIRED 0       // 1: two loads per tcgen05.wait::ld
+#endif
 constexpr int ROW_BYTES = 128;  // one SWIZZLE_128B row of a k-block (64 bf16 / 32 fp32)
 constexpr int B_BYTES = HB * ROW_BYTES;
 constexpr int TMEM_COLS = 2 * BN;
@@ -495,33 +498,56 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         tc_fence_after();
         const uint32_t t_row = tmem_base + (uint32_t(ew * 32) << 16) + acc * C::ACC_COLS - tcol0;
         const uint32_t id0 = uint32_t(p.id_base + c0);
+        // this chunk's dot bound (epi_chunk32b)
+        auto chunk_thr = [&](int base) -> float {
+          const int ci = base >> 5;
+          const float4 ch = ci < 4 ? cm0 : cm1;
+          const int cj = ci & 3;
+          const float cmin = cj < 2 ? (cj == 0 ? ch.x : ch.y) : (cj == 2 ? ch.z : ch.w);
+#ifdef RS_EXP_NO_SLOW  // timing experiment only (wrong results): no candidate ever passes the bound
+          (void)cmin;
+          return __int_as_float(0x7f800000);
+#else
+          return chunk_threshold(rt.qn, cmin, rt.tau);
+#endif
+        };
+        auto filter = [&](const uint32_t(&r)[EPI_COLS], int base, float thr) {
+#ifdef RS_PAIR_EPI_NOP  // timing experiment only: the MMA pipeline without the top-k work
+          if (__uint_as_float(r[0]) == 12345.0f) rt.append_raw(0.0f, id0);
+          return;
+#endif
+          if (base + EPI_COLS <= valid)
+            epi_chunk32b<KREG, EPI_THREADS, BUF, CHECK, true>(rt, r, cn_t + base, id0 + base, EPI_COLS, thr);
+          else
+            epi_chunk32b<KREG, EPI_THREADS, BUF, CHECK, false>(rt, r, cn_t + base, id0 + base, valid - base, thr);
+        };
+#if RS_PAIR_EPI_PAIRED
+        // two 32-column loads in flight per wait (4 waits per 256-column tile)
+#pragma unroll 1
+        for (int base = eg * SLICE; base < (eg + 1) * SLICE; base += 2 * EPI_COLS) {
+          if (base >= valid) break;  // warp-uniform
+          const bool two = base + EPI_COLS < valid;
+          uint32_t r0[EPI_COLS], r1[EPI_COLS];
+          __syncwarp();
+          tmem_ld_32x32b_x32(t_row + base, r0);
+          if (two) tmem_ld_32x32b_x32(t_row + base + EPI_COLS, r1);
+          const float thr0 = chunk_thr(base);
+          tmem_wait_ld();
+          filter(r0, base, thr0);
+          if (two) filter(r1, base + EPI_COLS, chunk_thr(base + EPI_COLS));
+        }
+#else
 #pragma unroll 1
         for (int base = eg * SLICE; base < (eg + 1) * SLICE; base += EPI_COLS) {
           if (base >= valid) break;  // warp-uniform
           uint32_t r[EPI_COLS];
           __syncwarp();
           tmem_ld_32x32b_x32(t_row + base, r);
-          // this chunk's dot bound (epi_chunk32b), selected while the load is in flight
-          const int ci = base >> 5;
-          const float4 ch = ci < 4 ? cm0 : cm1;
-          const int cj = ci & 3;
-          const float cmin = cj < 2 ? (cj == 0 ? ch.x : ch.y) : (cj == 2 ? ch.z : ch.w);
-#ifdef RS_EXP_NO_SLOW  // timing experiment only (wrong results): no candidate ever passes the bound
-          const float thr = __int_as_float(0x7f800000);
-          (void)cmin;
-#else
-          const float thr = chunk_threshold(rt.qn, cmin, rt.tau);
-#endif
+          const float thr = chunk_thr(base);  // computed while the load is in flight
           tmem_wait_ld();
-#ifdef RS_PAIR_EPI_NOP  // timing experiment only: the MMA pipeline without the top-k work
-          if (__uint_as_float(r[0]) == 12345.0f) rt.append_raw(0.0f, id0);
-          continue;
-#endif
-          if (base + EPI_COLS <= valid)
-            epi_chunk32b<KREG, EPI_THREADS, BUF, CHECK, true>(rt, r, cn_t + base, id0 + base, EPI_COLS, thr);
-          else
-            epi_chunk32b<KREG, EPI_THREADS, BUF, CHECK, false>(rt, r, cn_t + base, id0 + base, valid - base, thr);
+          filter(r, base, thr);
         }
+#endif
 #ifndef RS_PAIR_NO_SHARED_TAU
         if ((j & 3) == 0 && real_row) {
           // publish this list's k-th best (a bound for every other unit of
