@@ -539,7 +539,7 @@ int ensure_ws(rs_index* ix, int64_t nq, size_t part_bytes) {
     RS_CHECK_CUDA(cudaMalloc(&ix->qnorm, sizeof(float) * nq), "cudaMalloc(qnorm)");
     if (ix->qtau) cudaFree(ix->qtau);
     ix->qtau = nullptr;
-    RS_CHECK_CUDA(cudaMalloc(&ix->qtau, sizeof(uint32_t) * nq), "cudaMalloc(qtau)");
+    RS_CHECK_CUDA(cudaMalloc(&ix->qtau, sizeof(uint32_t) * nq * rs::kSharedBoundWords), "cudaMalloc(qtau)");
     ix->qnorm_cap = nq;
   }
   if (part_bytes > ix->part_cap) {

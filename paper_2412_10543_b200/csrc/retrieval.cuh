@@ -63,6 +63,8 @@ int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap* tmql, cons
                            uint64_t* part, int32_t* counter, int32_t walk_bias, uint32_t* qtau, cudaStream_t st);
 // query rows per pair tile: 256, or 128 for the small-batch (M = 128) variant
 int pair_tile_rows(bool small);
+// 32-bit words of shared-bound state per query the pair kernel needs (qtau + cascade)
+constexpr int64_t kSharedBoundWords = 5;
 // queries up to which a search uses the M = 128 pair tile (one tile, no padding rows)
 constexpr int64_t kSmallBatchMax = 128;
 // per 32-row chunk minimum of the squared norms over rows [r0, r1) of a shard

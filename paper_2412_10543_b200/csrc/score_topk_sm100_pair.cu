@@ -172,6 +172,8 @@ struct Params {
   int32_t* seg_pos;  // per segment: absolute tile index the most advanced pair last started (zeroed)
   int32_t walk_bias; // test hook: unit of query tile qt starts walk_bias*(qt+1) tiles past the frontier
   uint32_t* qtau;    // per query: best k-th distance bits published by any unit (memset 0xff per search)
+  uint32_t* qcas;    // per query: the kCas smallest rank-r distances of finished lists (r = ceil(k/kCas))
+  int32_t cas_rank;  // r
   int64_t cunits;    // cluster units = (qtiles / G) * segments
 };
 
@@ -205,6 +207,37 @@ struct TileWalk {
     return r0 + t * BN;
   }
 };
+
+// Shared admission bound of a query (threshold sharing across units).  Two
+// valid upper bounds of the query's final k-th distance:
+//  * qtau: the smallest k-th distance any list has reached (a list's k
+//    entries are real rows), published every 4 tiles and at unit end;
+//  * qcas[kCas-1]: each finished list inserts its rank-r distance (r =
+//    ceil(k/kCas)) once into a per-query cascade of kCas atomicMin slots, so
+//    slot kCas-1 holds the kCas-th smallest of them — kCas disjoint lists
+//    (distinct segments / column halves) with >= r rows each at or below
+//    it, i.e. >= k rows.  Once a few segments of a query are done this is
+//    far tighter than any single list's k-th distance, so later units admit
+//    ~k/kCas candidates instead of ~k.
+constexpr int kCas = 4;
+static_assert(1 + kCas == kSharedBoundWords, "qtau allocation (retrieval.cu)");
+__device__ __forceinline__ uint32_t shared_bound(const Params& p, int64_t qrow) {
+  const uint32_t a = ld_relaxed_gpu_u32(p.qtau + qrow);
+  const uint32_t b = ld_relaxed_gpu_u32(p.qcas + qrow * kCas + (kCas - 1));
+  return a < b ? a : b;
+}
+// Concurrent insertion into ascending slots by an atomicMin cascade: each
+// level keeps min(v, old) and passes max(v, old) down, so (values being
+// conserved per level) slot i ends as the (i+1)-th smallest inserted value,
+// and at any moment slot i's value is backed by i+1 distinct inserts.
+__device__ __forceinline__ void cascade_min_insert(uint32_t* slots, uint32_t v) {
+#pragma unroll
+  for (int i = 0; i < kCas; ++i) {
+    const uint32_t old = atomicMin(slots + i, v);
+    v = v > old ? v : old;
+    if (v == 0xffffffffu) break;
+  }
+}
 
 // Consumer side of the unit ring: wait for slot i, read the unit id, release
 // the slot to the leader's producer.  Returns the unit (-1 = no more work).
@@ -472,7 +505,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 #ifndef RS_PAIR_NO_SHARED_TAU
       // threshold sharing: start from the best k-th distance any unit of this
       // query has published (units of other segments, finished or running)
-      if (real_row) rt.seed(ld_relaxed_gpu_u32(p.qtau + qrow));
+      if (real_row) rt.seed(shared_bound(p, qrow));
       uint32_t tau_pending = 0xffffffffu;
 #endif
       const TileWalk walk(r0, r1, start);
@@ -489,7 +522,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         const float* cn_t = cns + acc * BN;
 #ifndef RS_PAIR_NO_SHARED_TAU
         // every 4th tile: fetch the shared threshold (consumed after the tile)
-        if ((j & 3) == 0 && real_row) tau_pending = ld_relaxed_gpu_u32(p.qtau + qrow);
+        if ((j & 3) == 0 && real_row) tau_pending = shared_bound(p, qrow);
 #endif
         // the tile's eight 32-column norm minima, loaded before the wait
         const float4 cm0 = __ldg(reinterpret_cast<const float4*>(p.cmin + (c0 >> 5)));
@@ -544,8 +577,8 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           __syncwarp();
           tmem_ld_32x32b_x32(t_row + base, r);
           const float thr = chunk_thr(base);  // computed while the load is in flight
-          tmem_wait_ld();
-          filter(r, base, thr);
+          PROF(6, tmem_wait_ld());
+          PROF(4, filter(r, base, thr));
         }
 #endif
 #ifndef RS_PAIR_NO_SHARED_TAU
@@ -569,7 +602,13 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       // every lane flushes (warp-collective), then writes its row if it is a real query
       PROF(5, rt.flush());
 #ifndef RS_PAIR_NO_SHARED_TAU
-      if (real_row && rt.kth_bits() < 0x7f800000u) red_min_relaxed_gpu_u32(p.qtau + qrow, rt.kth_bits());
+      if (real_row) {
+        if (rt.kth_bits() < 0x7f800000u) red_min_relaxed_gpu_u32(p.qtau + qrow, rt.kth_bits());
+        // this finished list holds >= r rows at or below its rank-r distance:
+        // insert it into the query's kCas-smallest cascade
+        const uint32_t rb = rt.rank_bits(p.cas_rank);
+        if (rb < 0x7f800000u) cascade_min_insert(p.qcas + qrow * kCas, rb);
+      }
 #endif
       if (qrow < p.nq) rt.finish(p.part + ((qrow * p.segments + seg) * C::LPS + eg) * p.k);
     }
@@ -644,7 +683,8 @@ int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap* tmql, cons
   RS_REQUIRE(plan.segments >= 1 && plan.segments <= kMaxSegments, "segments out of range (%d)", plan.segments);
   RS_CHECK_CUDA(cudaMemsetAsync(counter, 0, sizeof(int32_t) * (1 + plan.segments), st),
                 "cudaMemsetAsync(unit counter, segment frontiers)");
-  RS_CHECK_CUDA(cudaMemsetAsync(qtau, 0xff, sizeof(uint32_t) * size_t(nq), st), "cudaMemsetAsync(shared tau)");
+  RS_CHECK_CUDA(cudaMemsetAsync(qtau, 0xff, sizeof(uint32_t) * size_t(nq) * (1 + kCas), st),
+                "cudaMemsetAsync(shared bounds)");
   Params p{};
   p.qn = qn;
   p.cn = cn;
@@ -665,6 +705,8 @@ int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap* tmql, cons
   p.seg_pos = counter + 1;
   p.walk_bias = walk_bias;
   p.qtau = qtau;
+  p.qcas = qtau + nq;  // the caller allocates nq * (1 + kCas) words
+  p.cas_rank = (k + kCas - 1) / kCas;
   p.cunits = int64_t(plan.qtiles) * plan.segments;
   const CUtensorMap& ql = tf ? *tmql : tmq;
   const CUtensorMap& cl = tf ? *tmcl : tmc;

@@ -277,6 +277,14 @@ struct RegTopK {
   }
   // distance bits of the current k-th best (0x7f800000 = +inf until k entries)
   __device__ __forceinline__ uint32_t kth_bits() const { return kthk >> 1; }
+  // distance bits of the r-th best (1-based, r <= k; +inf when fewer entries)
+  __device__ __forceinline__ uint32_t rank_bits(int r) const {
+    uint32_t t = key[0];
+#pragma unroll
+    for (int j = 1; j < KREG; ++j)
+      if (j == r - 1) t = key[j];
+    return t >> 1;
+  }
 
   // Warp-collective: every lane inserts its buffered candidates (lockstep over
   // the warp's largest buffer; lanes past their own count insert kEmpty = no-op).

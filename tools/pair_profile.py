@@ -32,16 +32,17 @@ def main(n=2_000_000, nq=8192, d=1024):
     plan = ix.last_plan()
     ctas = 2 * plan["ctas"]
     a = a[:ctas]
-    # slot 7 = kernel cycles from warps 0, 1 and the 4 epilogue warps (each /4);
-    # warps 2, 3 finish immediately and add ~0
     names = {0: "producer wait empty (ring full)", 1: "mma wait tempty (epilogue-bound)",
              2: "mma wait full (operand-bound)", 3: "epilogue wait tfull (4 warps)",
-             5: "epilogue final flush (4 warps)"}
+             5: "epilogue final flush (4 warps)", 4: "epilogue filter (4 warps)",
+             6: "epilogue TMEM load wait (4 warps)"}
     for label, rows in (("leader", a[0::2]), ("peer", a[1::2])):
-        total = rows[:, 7] / 3.0  # warps: producer, mma, 4 epilogue (/4)
+        # slot 7: every warp's lane 0 adds its elapsed cycles / 4 (4 epilogue
+        # warps + TMEM, producer and MMA warps; the spare warp 4 exits at once)
+        total = rows[:, 7] / 1.75
         print(f"{label}: kernel {total.mean() / 1e6:.2f} Mcycles")
         for i, nm in names.items():
-            denom = total * (4 if i in (3, 5) else 1)
+            denom = total * (4 if i in (3, 4, 5, 6) else 1)
             print(f"   {nm:34s} {100 * (rows[:, i] / denom).mean():5.1f}%")
     print(plan)
 
