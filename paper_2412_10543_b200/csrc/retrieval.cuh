@@ -64,7 +64,10 @@ int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap* tmql, cons
 // query rows per pair tile: 256, or 128 for the small-batch (M = 128) variant
 int pair_tile_rows(bool small);
 // 32-bit words of shared-bound state per query the pair kernel needs (qtau + cascade)
-constexpr int64_t kSharedBoundWords = 5;
+#ifndef RS_PAIR_CAS
+#define RS_PAIR_CAS 4  // cascade slots per query (score_topk_sm100_pair.cu)
+#endif
+constexpr int64_t kSharedBoundWords = 1 + RS_PAIR_CAS;
 // queries up to which a search uses the M = 128 pair tile (one tile, no padding rows)
 constexpr int64_t kSmallBatchMax = 128;
 // per 32-row chunk minimum of the squared norms over rows [r0, r1) of a shard

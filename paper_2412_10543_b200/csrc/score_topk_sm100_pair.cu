@@ -219,7 +219,7 @@ struct TileWalk {
 //    it, i.e. >= k rows.  Once a few segments of a query are done this is
 //    far tighter than any single list's k-th distance, so later units admit
 //    ~k/kCas candidates instead of ~k.
-constexpr int kCas = 4;
+constexpr int kCas = RS_PAIR_CAS;
 static_assert(1 + kCas == kSharedBoundWords, "qtau allocation (retrieval.cu)");
 __device__ __forceinline__ uint32_t shared_bound(const Params& p, int64_t qrow) {
   const uint32_t a = ld_relaxed_gpu_u32(p.qtau + qrow);
