@@ -209,6 +209,31 @@ int rs_plan_calls(const rs_config* configs, const int32_t* qlen, int64_t n,
                   rs_call* calls, int64_t* total_bytes, uint8_t* status, void* workspace,
                   size_t workspace_bytes, void* stream);
 
+/* ---- cost table of every pruned candidate ---------------------------------
+ * For each query i, every config of its space in enumerate_candidates order
+ * (mapping.py:129-156): method, num_chunks, interlen, plan_bytes
+ * (memory.py:164-195) and — if `cost` is non-NULL — the plan's critical-path
+ * delay: the max of the independent calls' call_latency (sim.py:84-92) with
+ * concurrency running_before[i] + j (sim.py:223-229; NULL = 0), plus the
+ * reducer's latency for map_reduce.  Two passes like rs_plan_calls: out ==
+ * NULL writes offsets[0..n] (exclusive scan of the grid sizes; offsets[n] =
+ * total); then out[offsets[i] .. offsets[i+1]) are filled.  Returns
+ * RS_ERR_OVERFLOW if some query's byte arithmetic would exceed int64. */
+typedef struct rs_candidate {
+  int64_t kv_bytes;
+  double delay;
+  uint8_t method;      /* rs_method bit */
+  uint8_t reserved0;
+  uint16_t num_chunks;
+  uint16_t interlen;   /* 0 == None */
+  uint16_t reserved1;
+} rs_candidate;
+size_t rs_candidate_costs_workspace_size(int64_t n);
+int rs_candidate_costs(const rs_space* spaces, const int32_t* qlen, const int32_t* running_before, int64_t n,
+                       const rs_select_params* params /* host */, const rs_cost_model* cost /* host, nullable */,
+                       int64_t* offsets, rs_candidate* out, void* workspace, size_t workspace_bytes,
+                       void* stream);
+
 /* ---- profile ingestion (parse_profile_text, profiler.py:203-254) -----------
  * Host routine (the answers are strings on the host): parse n estimator
  * answers — UTF-8, answer i = text[offsets[i] .. offsets[i+1]) — into

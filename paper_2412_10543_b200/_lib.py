@@ -43,6 +43,9 @@ CALL_DTYPE = np.dtype([("kv_bytes", "<i8"), ("prompt_tokens", "<i4"), ("max_outp
 CALL_KINDS = ("single", "mapper", "reducer", "rerank")  # rs_call.kind -> CallKind value (memory.py:29-33)
 RS_PLAN_OK, RS_PLAN_NONE, RS_PLAN_INVALID_CHUNKS, RS_PLAN_CONTEXT_OVERFLOW, RS_PLAN_BAD_INTERLEN = range(5)
 assert CALL_DTYPE.itemsize == 24
+CANDIDATE_DTYPE = np.dtype([("kv_bytes", "<i8"), ("delay", "<f8"), ("method", "u1"), ("reserved0", "u1"),
+                            ("num_chunks", "<u2"), ("interlen", "<u2"), ("reserved1", "<u2")])
+assert CANDIDATE_DTYPE.itemsize == 24
 ADMIT_INFO_DTYPE = np.dtype([("admitted_bytes", "<i8"), ("admitted_calls", "<i4"), ("fixed_path", "<i4")])
 ADMIT_RESULT_DTYPE = np.dtype([("admitted", "<i8"), ("used_bytes", "<i8"), ("stop", "<i4"), ("reserved", "<i4")])
 (RS_ADMIT_DRAINED, RS_ADMIT_BLOCKED, RS_ADMIT_NO_PROFILE, RS_ADMIT_IMPOSSIBLE, RS_ADMIT_FIXED_SPACE,
@@ -118,6 +121,9 @@ SIGNATURES = {
     "rs_plan_calls_workspace_size": (ctypes.c_size_t, [_I64]),
     "rs_plan_calls": (ctypes.c_int, [_P, _P, _I64, ctypes.POINTER(SelectParamsC), _I64, _P, _P, _P, _P, _P,
                                      ctypes.c_size_t, _P]),
+    "rs_candidate_costs_workspace_size": (ctypes.c_size_t, [_I64]),
+    "rs_candidate_costs": (ctypes.c_int, [_P, _P, _P, _I64, ctypes.POINTER(SelectParamsC), ctypes.POINTER(CostModelC),
+                                          _P, _P, _P, ctypes.c_size_t, _P]),
     "rs_parse_profiles": (ctypes.c_int, [ctypes.c_char_p, _P, _I64, _P, _P, _P, _P, _P, _I32]),
     "rs_admit_fifo": (ctypes.c_int, [_P, _P, _P, _P, _I64, ctypes.POINTER(SelectParamsC),
                                      ctypes.POINTER(AdmitParamsC), _P, _P, _P, _P]),

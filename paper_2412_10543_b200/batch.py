@@ -342,6 +342,32 @@ def admit_fifo(spaces: torch.Tensor, profiles: torch.Tensor | None, qlen: torch.
     return configs[:n], info[:n], result
 
 
+def candidate_costs(spaces: torch.Tensor, qlen: torch.Tensor, params: SelectParams, *, cost: CostModel | None = None,
+                    running_before: torch.Tensor | None = None, stream=None):
+    """Every candidate of every query's pruned space (enumerate_candidates
+    order, mapping.py:129-156) with its plan_bytes and, given a cost model,
+    its plan's critical-path delay.  Returns device (offsets int64 [n+1],
+    records uint8 [total, 24] of rs_candidate); query i's candidates are
+    records[offsets[i]:offsets[i+1]]."""
+    n = spaces.shape[0]
+    dev = spaces.device
+    lib = _lib.lib_for_device(_dev_index(spaces))
+    offsets = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    ws = torch.empty(max(int(lib.rs_candidate_costs_workspace_size(n)), 4), dtype=torch.uint8, device=dev)
+    pc = params.c()
+    cp = ctypes.byref(cost.c()) if cost is not None else None
+    s = _lib.stream_ptr(stream)
+    _lib.check(lib.rs_candidate_costs(_lib.ptr(spaces), _lib.ptr(qlen), _lib.ptr(running_before), n, ctypes.byref(pc),
+                                      cp, _lib.ptr(offsets), 0, _lib.ptr(ws), ws.numel(), s),
+               "rs_candidate_costs(count)")
+    total = int(offsets[n].item())  # one host read to size the table
+    out = torch.empty((max(total, 1), 24), dtype=torch.uint8, device=dev)
+    _lib.check(lib.rs_candidate_costs(_lib.ptr(spaces), _lib.ptr(qlen), _lib.ptr(running_before), n, ctypes.byref(pc),
+                                      cp, _lib.ptr(offsets), _lib.ptr(out), _lib.ptr(ws), ws.numel(), s),
+               "rs_candidate_costs(fill)")
+    return offsets, out[:total]
+
+
 def call_latency_batch(prompt_tokens: torch.Tensor, max_output_tokens: torch.Tensor, concurrent: torch.Tensor,
                        cost: CostModel, stream=None) -> torch.Tensor:
     n = prompt_tokens.shape[0]

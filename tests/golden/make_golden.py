@@ -530,6 +530,47 @@ def gen_parse():
           sum(bool(r[2] and r[2][5]) for r in rows), "clamped")
 
 
+# -- G8: cost table of every pruned candidate ----------------------------------
+
+def gen_costs():
+    """Per candidate of random spaces: plan_bytes and the plan's critical-path
+    delay (the definition of gen_latency: independent calls dispatched with
+    concurrency c0 + j, the reducer after its mappers, sim.py:223-229)."""
+    rng = random.Random(77)
+    costs = [CostModel(), CostModel(1e-4, 1e-2, 0.0, 0.0), CostModel(3.3e-5, 7.1e-3, 0.037, 0.0)]
+    queries, cands = [], []
+    for trial in range(600):
+        ps_i = rng.randrange(len(PARAM_SETS))
+        model0, meta, out, tmpl, mc, gran = params_kw(PARAM_SETS[ps_i])
+        model = ModelSpec(model0.num_layers, model0.num_kv_heads, model0.head_dim, model0.bytes_per_element,
+                          max_context_tokens=10 ** 9)  # delays need no context check
+        space = FULL_SPACE if rng.random() < 0.05 else random_arbitrary_space(rng, mc)
+        qlen = rng.randint(1, 12000)
+        c0 = rng.randint(0, 200)
+        ci = rng.randrange(len(costs))
+        q = QueryRecord(id="c", text="t", query_token_len=qlen)
+        queries.append((trial, ps_i, *enc_space(space), qlen, c0, ci))
+        for cfg in enumerate_candidates(space, gran):
+            b = plan_bytes(qlen, cfg, meta.chunk_size, bytes_per_kv_token(model), out, tmpl)
+            plan = plan_calls(q, cfg, meta, model, out, template_tokens=tmpl, max_chunks=max(mc, cfg.num_chunks))
+            worst, j = 0.0, 0
+            for call in plan.calls:
+                if not call.depends_on:
+                    worst = max(worst, call_latency(call, c0 + j, costs[ci]))
+                    j += 1
+            for call in plan.calls:
+                if call.depends_on:
+                    worst = worst + call_latency(call, c0, costs[ci])
+            m, n, il = enc_cfg(cfg)
+            cands.append((trial, m, n, il, b, worst))
+    np.savez_compressed(os.path.join(OUT_DIR, "costs.npz"), queries=np.array(queries, dtype=np.int64),
+                        cand=np.array([c[:5] for c in cands], dtype=np.int64),
+                        delay=np.array([c[5] for c in cands], dtype=np.float64),
+                        costs=np.array([(c.prefill_secs_per_token, c.decode_secs_per_token_base,
+                                         c.batch_slowdown_per_seq) for c in costs], dtype=np.float64))
+    print("costs:", len(queries), "queries,", len(cands), "candidates")
+
+
 if __name__ == "__main__":
     gen_mapping()
     gen_select()
@@ -538,3 +579,4 @@ if __name__ == "__main__":
     gen_plan_calls()
     gen_known()
     gen_parse()
+    gen_costs()

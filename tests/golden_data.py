@@ -96,3 +96,9 @@ def parse_answers():
 
     with gzip.open(os.path.join(GOLDEN, "parse.json.gz"), "rt", encoding="utf-8") as f:
         return json.load(f)
+
+
+def candidate_costs():
+    """Per-candidate plan bytes and plan delays from the reference
+    (tests/golden/make_golden.py gen_costs)."""
+    return _load("costs.npz")

@@ -23,6 +23,21 @@ def main(n=100_000, reps=50):
     cost = batch.CostModel()
     window = batch.GateWindow(dev)
     out = torch.empty((n, 16), dtype=torch.uint8, device=dev)
+    # the full cost table (every candidate's bytes + plan delay): 70M records
+    for _ in range(2):
+        off, recs = batch.candidate_costs(spaces, qlen, params, cost=cost)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    reps_t = 5
+    for _ in range(reps_t):
+        off, recs = batch.candidate_costs(spaces, qlen, params, cost=cost)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps_t
+    print(f"{'cost table (2 passes)':22s} {ms * 1e3:8.1f} us/batch  {n / ms * 1e3 / 1e6:8.1f} M queries/s  "
+          f"{recs.shape[0] / ms * 1e3 / 1e9:8.2f} G candidates/s  ({recs.numel() / ms * 1e3 / 1e9:.0f} GB/s written)")
+    del off, recs
     for mode in ("select", "select+delay", "gate", "gate+select+delay"):
         def step():
             if "gate" in mode:
