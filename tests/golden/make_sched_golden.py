@@ -184,21 +184,37 @@ def record_sim(name, mode, fixed=None, capacity=None, n=200, profile_name="singl
                         {"info": enc_info(info), "used": self.used_bytes}])
             return info
 
+    import ragsched.profiler as rprof
+
+    gates = []
+    orig_gate = rprof.QueryProfiler.gate
+
+    def recording_gate(self, out):
+        d = orig_gate(self, out)
+        p = out.profile
+        gates.append([[int(p.complexity_high), int(p.needs_joint_reasoning), p.pieces_required,
+                       p.summary_len_range.low, p.summary_len_range.high, p.confidence],
+                      [list(enc_space(d.space)), bool(d.used_fallback), d.confidence],
+                      [self.threshold, list(enc_space(self.default_space)), self.max_chunks]])
+        return d
+
     wl = gen_workload(WorkloadSpec(num_queries=n, arrival=ArrivalSpec(mode, 2.0),
                                    length_profile=DATASET_PROFILES[profile_name],
                                    truth_distribution=TruthDistribution()), 42)
     saved = sim.Scheduler
     sim.Scheduler = Recording
+    rprof.QueryProfiler.gate = recording_gate
     try:
         report = sim.run(wl, DEFAULT_MODEL, capacity or DEFAULT_CAPACITY_BYTES, CostModel(), QualityModel(), 42,
                          PipelineParams(meta=DEFAULT_META, out_budget=out_budget, fixed_config=fixed,
                                         noise=NoiseParams()))
     finally:
         sim.Scheduler = saved
+        rprof.QueryProfiler.gate = orig_gate
     sc = dict(name=name, sim=True, ps=0, capacity=capacity or DEFAULT_CAPACITY_BYTES,
               allow_fallback=fixed is None)
     return {"name": name, "scenario": sc, "ops": ops, "trace": report.trace, "failed": False,
-            "results": len(report.results)}
+            "results": len(report.results), "gates": gates}
 
 
 if __name__ == "__main__":
@@ -213,7 +229,8 @@ if __name__ == "__main__":
                  ("sim_fixed_mr8_poisson_1g", ArrivalMode.POISSON,
                   RagConfig(SynthesisMethod.MAP_REDUCE, 8, 100), GiB)):
         r = record_sim(*args)
-        print(f"{r['name']:26s} ops={len(r['ops']):5d} trace={len(r['trace']):5d} results={r['results']}")
+        print(f"{r['name']:26s} ops={len(r['ops']):5d} trace={len(r['trace']):5d} results={r['results']} "
+              f"gates={len(r['gates'])} gate fallbacks={sum(g[1][1] for g in r['gates'])}")
         out.append(r)
     for sc in SCENARIOS:
         r = run(sc)

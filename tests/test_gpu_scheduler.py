@@ -93,3 +93,29 @@ def test_admit_chain_single_launch_for_a_burst():
     adms, admitted = sched.step(0.0)
     assert len(adms) == 30 and len(admitted) == 30
     assert _lib.launch_count() - l0 <= 4
+
+
+SIM_GATES = [r for r in TRACES if r.get("gates")]
+
+
+@pytest.mark.parametrize("rec", SIM_GATES, ids=[r["name"] for r in SIM_GATES])
+def test_gate_replays_reference_sim(rec):
+    """The confidence gate as the reference's sim.run drove it (QueryProfiler.gate
+    -> gate_profile, profiler.py:534-541): the same profiles in order through this
+    package's GPU gate_profile with its own window give the same decisions."""
+    from types import SimpleNamespace
+
+    from paper_2412_10543_b200 import profiler as G
+
+    window = G.RecentSpaceWindow()
+    for k, (prof, want, (thr, default_space, max_chunks)) in enumerate(rec["gates"]):
+        p = QueryProfile(bool(prof[0]), bool(prof[1]), prof[2], IntRange(prof[3], prof[4]), prof[5])
+        d = G.gate_profile(SimpleNamespace(profile=p), window, thr, default_space=dec_space(default_space),
+                           max_chunks=max_chunks)
+        m = 0
+        for x in d.space.synthesis_methods:
+            m |= {"map_rerank": 1, "stuff": 2, "map_reduce": 4}[x.value]
+        il = d.space.intermediate_length_range
+        got = [[m, d.space.num_chunks_range.low, d.space.num_chunks_range.high, il.low if il else 0,
+                il.high if il else 0], d.used_fallback, d.confidence]
+        assert got == want, (k, got, want)
