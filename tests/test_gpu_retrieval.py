@@ -61,6 +61,8 @@ SHAPES = [  # nq, n, d, k
     (64, 70000, 768, 40),
     (200, 3000, 72, 17),      # dim not a multiple of the 64-element k-block
     (1000, 20000, 256, 35),
+    (300, 6000, 4096, 35),    # long rows: 64 k-blocks per tile
+    (40, 9000, 1536, 7),
 ]
 
 
