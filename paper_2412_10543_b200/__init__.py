@@ -7,8 +7,10 @@ retrieval, all computed by hand-written sm_100a kernels in
 ``libragsched_b200.so`` (C ABI: ``include/ragsched_b200.h``).
 
 Names mirror the reference's namespace (``ragsched/__init__.py``): scalar
-functions keep the reference signatures; the batched fast path lives in
-``batch`` / ``pipeline`` / ``dist``.  Importing this package does not need a
+functions and the stateful ``Scheduler`` keep the reference signatures; the
+batched fast path lives in ``batch`` (gate, select, cost table, plan
+expansion, admission chain, answer parsing) / ``pipeline`` (retrieve +
+select) / ``dist`` (multi-GPU).  Importing this package does not need a
 GPU; calling any compute function does (no CPU fallback).
 """
 
@@ -26,17 +28,33 @@ from .mapping import (
     map_profile,
     space_reduction_factor,
 )
-from .memory import buffered_bytes, plan_bytes
+from .memory import CallKind, CallPlan, LlmCall, buffered_bytes, memory_requirement, plan_bytes, plan_calls
 from .profiler import (
     DEFAULT_FALLBACK_SPACE,
     GATE_THRESHOLD,
+    PROFILE_FIELDS,
     WINDOW_CAPACITY,
     GateDecision,
     RecentSpaceWindow,
+    UnparseableAnswer,
     gate_profile,
+    parse_profile_text,
 )
 from .retriever import IndexFlatL2, merge_topk
-from .scheduler import SchedulingImpossible, best_fit_select, fallback_config
+from .scheduler import (
+    Admission,
+    AdmittedCall,
+    CompletionInfo,
+    MemorySafetyViolation,
+    PendingQuery,
+    QueryRun,
+    Scheduler,
+    SchedulerParams,
+    SchedulingImpossible,
+    UnknownCall,
+    best_fit_select,
+    fallback_config,
+)
 from .sim import call_latency
 from .types import (
     DEFAULT_MAX_CHUNKS,
