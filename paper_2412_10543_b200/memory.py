@@ -8,10 +8,17 @@ host-side scalars that parameterise the kernels.
 
 from __future__ import annotations
 
+from dataclasses import dataclass, field
+from enum import Enum
+
+import numpy as np
 import torch
 
+from . import _lib
 from . import batch as _b
+from .types import DEFAULT_MAX_CHUNKS, ContextOverflow, InvalidChunkCount
 from .types import DEFAULT_TEMPLATE_TOKENS, SynthesisMethod, method_bit
+
 
 BUFFER_NUMERATOR = 102   # memory.py:25
 BUFFER_DENOMINATOR = 100  # memory.py:26
@@ -40,14 +47,6 @@ def plan_bytes(query_token_len: int, cfg, chunk_size: int, per_token_bytes: int,
 
 
 # -- per-call expansion (memory.py:29-67, :89-150) -----------------------------
-
-from dataclasses import dataclass, field  # noqa: E402
-from enum import Enum  # noqa: E402
-
-import numpy as np  # noqa: E402
-
-from . import _lib  # noqa: E402
-from .types import DEFAULT_MAX_CHUNKS, ContextOverflow, InvalidChunkCount  # noqa: E402
 
 
 class CallKind(str, Enum):

@@ -1,17 +1,32 @@
-"""Best-fit + fallback selection (reference ``scheduler.py:127-191``), on the
-GPU.  Scalar drop-ins with the reference signatures; the batched fast path is
-:func:`paper_2412_10543_b200.batch.select`.
+"""Best-fit + fallback selection (reference ``scheduler.py:127-191``) and the
+stateful FIFO ``Scheduler`` (``scheduler.py:194-469``), on the GPU.  Scalar
+drop-ins with the reference signatures; the batched fast paths are
+:func:`paper_2412_10543_b200.batch.select` and ``batch.admit_fifo``.
 """
 
 from __future__ import annotations
 
+import itertools
+from collections import deque
+from dataclasses import dataclass, field
+from types import SimpleNamespace
+
 import numpy as np
 import torch
 
+from . import _lib
 from . import batch as _b
+from . import memory as _mem
 from ._lib import SPACE_DTYPE
 from .mapping import EnumGranularity
-from .types import DEFAULT_MAX_CHUNKS, DEFAULT_TEMPLATE_TOKENS, RagConfig, SynthesisMethod
+from .types import (
+    DEFAULT_MAX_CHUNKS,
+    DEFAULT_TEMPLATE_TOKENS,
+    ContextOverflow,
+    InvalidChunkCount,
+    RagConfig,
+    SynthesisMethod,
+)
 
 
 class SchedulingImpossible(RuntimeError):
@@ -60,15 +75,6 @@ def fallback_config(profile, q, free_bytes: int, *, model, meta, out_budget: int
 # admitted configs into their calls.  The host applies those decisions to the
 # per-call state (active runs, backlog, trace), which the reference keeps in
 # Python objects too; completions and the backlog pass are pure bookkeeping.
-
-import itertools  # noqa: E402
-from collections import deque  # noqa: E402
-from dataclasses import dataclass, field  # noqa: E402
-from types import SimpleNamespace  # noqa: E402
-
-from . import _lib  # noqa: E402
-from . import memory as _mem  # noqa: E402
-from .types import ContextOverflow, InvalidChunkCount  # noqa: E402
 
 
 class UnknownCall(KeyError):
