@@ -1,0 +1,96 @@
+"""Randomised GPU retrieval check (GPU box): random shapes, dtypes, k,
+duplicate rows, non-normalised and zero rows, id bases, ragged incremental
+adds, forced wrap-around walks and every algorithm, each compared with the
+float64 oracle (oracle/retrieval_oracle.check_topk — test infrastructure).
+usage: python tools/fuzz_retrieval.py [seconds] [seed]"""
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from oracle import retrieval_oracle as ro  # noqa: E402
+from paper_2412_10543_b200 import IndexFlatL2  # noqa: E402
+
+RTOL = {torch.bfloat16: 1e-3, torch.float32: 1e-5}
+
+
+def case(rng):
+    dtype = torch.bfloat16 if rng.random() < 0.65 else torch.float32
+    d = int(rng.choice([64, 128, 256, 512, 768, 1024, 72, 200, 1536]))
+    n = int(rng.choice([1, 7, 35, 300, 4096, 20_000, 50_000, int(rng.integers(1, 60_000))]))
+    nq = int(rng.choice([1, 5, 64, 128, 129, 256, 300, 700]))
+    k = int(rng.integers(1, 41))
+    algo = "auto"
+    r = rng.random()
+    if r < 0.1:
+        algo = "simt"
+    elif r < 0.2 and dtype == torch.bfloat16:
+        algo = "tcgen05_1sm"
+    c = torch.randn(n, d, generator=torch.Generator().manual_seed(int(rng.integers(1 << 30))))
+    style = rng.random()
+    if style < 0.5:
+        c = c / c.norm(dim=1, keepdim=True)
+    elif style < 0.8:  # widely varying norms: the epilogue's dot bound is loose
+        c = c * torch.from_numpy(rng.uniform(0.05, 3.0, (n, 1)).astype(np.float32))
+    if rng.random() < 0.3 and n > 10:  # exact duplicates
+        step = int(rng.integers(2, 50))
+        c[step::step] = c[0]
+    if rng.random() < 0.1 and n > 3:
+        c[1] = 0.0
+    src = torch.from_numpy(rng.integers(0, n, nq))
+    q = torch.randn(nq, d, generator=torch.Generator().manual_seed(int(rng.integers(1 << 30))))
+    q = q / q.norm(dim=1, keepdim=True)
+    nb = torch.from_numpy(rng.random(nq) < 0.5)
+    q[nb] = c[src[nb]] + 0.3 * q[nb] / d ** 0.5
+    if rng.random() < 0.2 and n > 0:
+        q[0] = c[0]
+    q, c = q.to(dtype), c.to(dtype)
+    base = int(rng.choice([0, 0, int(rng.integers(0, 1 << 31))]))
+    base = min(base, (1 << 32) - 2 - n)
+    bias = int(rng.choice([0, 0, 0, int(rng.integers(1, 9))]))
+    pieces = int(rng.integers(1, 4))
+    return dict(dtype=dtype, d=d, n=n, nq=nq, k=k, algo=algo, q=q, c=c, base=base, bias=bias, pieces=pieces)
+
+
+def run(cs):
+    ix = IndexFlatL2(cs["d"], dtype=cs["dtype"], capacity=max(cs["n"], 1), id_base=cs["base"])
+    ix.set_algo(cs["algo"])
+    if cs["bias"]:
+        ix.set_walk_bias(cs["bias"])
+    cuts = sorted(set([0, cs["n"]] + list(np.random.default_rng(cs["n"]).integers(0, cs["n"] + 1, cs["pieces"] - 1))))
+    for a, b in zip(cuts, cuts[1:]):
+        if b > a:
+            ix.add(cs["c"][a:b].cuda())
+    D, I = ix.search(cs["q"].cuda(), cs["k"])
+    torch.cuda.synchronize()
+    plan = ix.last_plan()
+    ix.close()
+    D, I = D.cpu().numpy(), I.cpu().numpy()
+    I0 = np.where(I >= 0, I - cs["base"], -1)
+    res = ro.check_topk(D, I0, cs["q"], cs["c"], cs["k"], RTOL[cs["dtype"]])
+    return res, plan
+
+
+def main(seconds=300, seed=0, max_cases=None):
+    rng = np.random.default_rng(seed)
+    t0 = time.time()
+    n_cases = n_bad = 0
+    while time.time() - t0 < seconds and (max_cases is None or n_cases < max_cases):
+        cs = case(rng)
+        res, plan = run(cs)
+        n_cases += 1
+        desc = {x: (str(cs[x]) if x == "dtype" else cs[x]) for x in ("dtype", "d", "n", "nq", "k", "algo", "base", "bias",
+                                                                      "pieces")}
+        if res["violations"] or res["exact_rows"] < 0.8 * res["rows"]:
+            n_bad += 1
+            print("FAIL", desc, plan, res["violations"][:3], res["exact_rows"], res["rows"], flush=True)
+    print(f"fuzz: {n_cases} cases, {n_bad} failures in {time.time() - t0:.0f} s (seed {seed})")
+    return n_bad
+
+
+if __name__ == "__main__":
+    sys.exit(1 if main(int(sys.argv[1]) if len(sys.argv) > 1 else 300, int(sys.argv[2]) if len(sys.argv) > 2 else 0)
+             else 0)
