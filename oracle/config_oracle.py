@@ -291,3 +291,63 @@ def plan_delay(qlen, cfg, p: SelectParams, cost: CostModel, running_before: int)
         if not ind:
             worst = worst + call_latency(pr, out, running_before, cost)
     return worst
+
+
+# -- FIFO admission chain (Scheduler.step, scheduler.py:335-410) ---------------
+
+(ADMIT_DRAINED, ADMIT_BLOCKED, ADMIT_NO_PROFILE, ADMIT_IMPOSSIBLE, ADMIT_FIXED_SPACE, ADMIT_INVALID_CHUNKS,
+ ADMIT_CONTEXT_OVERFLOW, ADMIT_BAD_INTERLEN) = range(8)
+_PLAN_TO_ADMIT = {PLAN_INVALID_CHUNKS: ADMIT_INVALID_CHUNKS, PLAN_CONTEXT_OVERFLOW: ADMIT_CONTEXT_OVERFLOW,
+                  PLAN_BAD_INTERLEN: ADMIT_BAD_INTERLEN}
+
+
+def admit_chain(entries, p: SelectParams, capacity: int, used: int, max_context_tokens: int,
+                allow_fallback: bool = True):
+    """The new-query loop of Scheduler.step over _try_admit_new
+    (scheduler.py:335-410) with the accounting of _start_run (:281-333).
+    ``entries``: (space, joint, has_profile, qlen) in queue order.  Returns
+    (admitted, used_after, stop, stop_cfg): admitted = [(cfg, bytes, status,
+    admitted_bytes, admitted_calls, fixed_path)], stop_cfg = the config of the
+    entry that raised (plan errors and the fixed path's capacity check)."""
+    out = []
+    for space, joint, hasp, q in entries:
+        free = capacity - used
+        fixed = False
+        r = best_fit_select(space, q, free, p)
+        if r is not None:
+            cfg, b = r
+            status = ST_BEST_FIT
+        elif allow_fallback:
+            if not hasp:
+                return out, used, ADMIT_NO_PROFILE, None          # :356-359
+            r = fallback_config(joint, q, free, p)
+            if r is None:
+                return out, used, (ADMIT_IMPOSSIBLE if used == 0 else ADMIT_BLOCKED), None  # :370-378
+            cfg, b = r
+            status = ST_FALLBACK
+        else:                                                    # fixed-config baseline :380-395
+            grid = enumerate_grid(space, p.chunk_step, p.interlen_step)
+            if len(grid) != 1:
+                return out, used, ADMIT_FIXED_SPACE, None
+            cfg, b, status, fixed = grid[0], None, ST_BEST_FIT, True
+        st, calls, total = plan_calls(q, cfg, p, max_context_tokens)
+        if st != PLAN_OK:
+            return out, used, _PLAN_TO_ADMIT[st], cfg
+        indep = [c for c in calls if c[0] != KIND_REDUCER]
+        if fixed:
+            smallest = min(c[3] for c in indep)
+            if smallest > capacity:
+                return out, used, ADMIT_IMPOSSIBLE, cfg
+            if smallest > free:
+                return out, used, ADMIT_BLOCKED, cfg
+            adm, n_adm = 0, 0
+            for c in indep:                                      # each call against the free bytes left
+                if c[3] <= free - adm:
+                    adm += c[3]
+                    n_adm += 1
+            b = total
+        else:
+            adm, n_adm = sum(c[3] for c in indep), len(indep)
+        used += adm
+        out.append((cfg, b, status, adm, n_adm, fixed))
+    return out, used, ADMIT_DRAINED, None
