@@ -78,16 +78,17 @@ def fallback_config(profile, q, free_bytes: int, *, model, meta, out_budget: int
 
 
 class UnknownCall(KeyError):
-    """scheduler.py:33-34."""
+    """A completion names a query or call that is not running."""
 
 
 class MemorySafetyViolation(RuntimeError):
-    """scheduler.py:37-38."""
+    """The KV accounting left [0, capacity] (a bug, never an input error)."""
 
 
 @dataclass(frozen=True)
 class SchedulerParams:
-    """scheduler.py:45-56."""
+    """Model, corpus, output budget, template tokens, chunk cap, grid steps;
+    ``allow_fallback`` off = the fixed-config baseline (scheduler.py:45-56)."""
 
     model: object
     meta: object
@@ -100,7 +101,8 @@ class SchedulerParams:
 
 @dataclass
 class PendingQuery:
-    """scheduler.py:59-71."""
+    """A waiting-queue entry: the query, its pruned space and the gate
+    metadata the caller reports later."""
 
     query: object
     space: object
@@ -114,7 +116,7 @@ class PendingQuery:
 
 @dataclass(frozen=True)
 class Admission:
-    """scheduler.py:74-82."""
+    """What step() decided for one query."""
 
     query_id: str
     chosen_config: RagConfig
@@ -125,7 +127,7 @@ class Admission:
 
 @dataclass(frozen=True)
 class AdmittedCall:
-    """scheduler.py:85-93."""
+    """One LLM call that entered the running batch."""
 
     query_id: str
     call_index: int
@@ -136,7 +138,7 @@ class AdmittedCall:
 
 @dataclass(frozen=True)
 class CompletionInfo:
-    """scheduler.py:96-102."""
+    """What complete() reports back."""
 
     query_done: bool
     config: RagConfig
@@ -147,7 +149,7 @@ class CompletionInfo:
 
 @dataclass
 class QueryRun:
-    """scheduler.py:105-124."""
+    """Per-query call state: which plan calls are admitted / completed."""
 
     pending: PendingQuery
     config: RagConfig
@@ -159,13 +161,13 @@ class QueryRun:
     rerank_confidences: dict = field(default_factory=dict)
 
     def deferred(self) -> list[int]:
-        return [i for i in range(len(self.plan.calls)) if i not in self.admitted]
+        return sorted(set(range(len(self.plan.calls))).difference(self.admitted))
 
     def ready(self, idx: int) -> bool:
-        return self.plan.calls[idx].depends_on <= self.completed
+        return self.plan.calls[idx].depends_on.issubset(self.completed)
 
     def fully_admitted(self) -> bool:
-        return len(self.admitted) == len(self.plan.calls)
+        return not self.deferred()
 
     def done(self) -> bool:
         return len(self.completed) == len(self.plan.calls)
@@ -216,59 +218,59 @@ class Scheduler:
     # -- admission ---------------------------------------------------------
 
     def _check_accounting(self) -> None:
-        if not 0 <= self.used_bytes <= self.capacity_bytes:
+        if self.used_bytes < 0 or self.used_bytes > self.capacity_bytes:
             raise self._k.MemorySafetyViolation(f"used {self.used_bytes} outside [0, {self.capacity_bytes}]")
 
-    def _admit_call(self, run, idx: int, now: float, admitted: list, deferred: bool) -> None:
-        call = run.plan.calls[idx]
-        self.used_bytes += call.kv_bytes
+    def _log(self, event: str, now: float, query: str, **fields) -> None:
+        # trace records keep the reference's key order (event, t, query, ...)
+        self.trace.append({"event": event, "t": now, "query": query, **fields})
+
+    def _take(self, run, idx: int, now: float, sink: list, from_backlog: bool) -> None:
+        """Admit one call: account its KV bytes and report it."""
+        c = run.plan.calls[idx]
+        qid = run.pending.query.id
+        self.used_bytes += c.kv_bytes
         self._check_accounting()
         run.admitted.add(idx)
-        admitted.append(self._k.AdmittedCall(query_id=run.pending.query.id, call_index=idx,
-                                             prompt_tokens=call.prompt_tokens,
-                                             max_output_tokens=call.max_output_tokens, kv_bytes=call.kv_bytes))
-        if deferred:
-            self.trace.append({"event": "admit_deferred", "t": now, "query": run.pending.query.id, "call": idx,
-                               "kv_bytes": call.kv_bytes})
+        sink.append(self._k.AdmittedCall(query_id=qid, call_index=idx, prompt_tokens=c.prompt_tokens,
+                                         max_output_tokens=c.max_output_tokens, kv_bytes=c.kv_bytes))
+        if from_backlog:
+            self._log("admit_deferred", now, qid, call=idx, kv_bytes=c.kv_bytes)
 
-    def _admit_backlog(self, now: float, admitted: list) -> bool:
-        """scheduler.py:257-270: deferred work of admitted queries, FIFO; True
-        when a ready call does not fit (blocks new admissions)."""
-        for qid in list(self.backlog_order):
+    def _admit_backlog(self, now: float, sink: list) -> bool:
+        """Deferred work first, in admission order (scheduler.py:257-270): a
+        ready call that does not fit blocks everything behind it (returns
+        True)."""
+        for qid in tuple(self.backlog_order):
             run = self.active[qid]
-            for idx in run.deferred():
-                call = run.plan.calls[idx]
-                if not run.ready(idx):
-                    continue
-                if call.kv_bytes > self.free_bytes:
+            for idx in (i for i in run.deferred() if run.ready(i)):
+                if run.plan.calls[idx].kv_bytes > self.free_bytes:
                     return True
-                self._admit_call(run, idx, now, admitted, deferred=True)
+                self._take(run, idx, now, sink, from_backlog=True)
             if run.fully_admitted():
                 self.backlog_order.remove(qid)
         return False
 
-    def _start_run(self, pending, cfg, plan, is_fallback: bool, now: float, admitted: list, *,
+    def _start_run(self, pending, cfg, plan, is_fallback: bool, now: float, sink: list, *,
                    admit_all_independent: bool):
-        """scheduler.py:281-333 (the plan comes from rs_plan_calls)."""
+        """Open the query's run and admit its independent calls
+        (scheduler.py:281-333); the plan is rs_plan_calls' expansion."""
+        qid = pending.query.id
         run = self._k.QueryRun(pending=pending, config=cfg, plan=plan, is_fallback=is_fallback, admission_time=now)
-        self.active[pending.query.id] = run
+        self.active[qid] = run
         for idx in plan.independent_calls():
-            call = plan.calls[idx]
-            if call.kv_bytes <= self.free_bytes:
-                self._admit_call(run, idx, now, admitted, deferred=False)
+            if plan.calls[idx].kv_bytes <= self.free_bytes:
+                self._take(run, idx, now, sink, from_backlog=False)
             elif admit_all_independent:
-                raise self._k.MemorySafetyViolation(
-                    f"call {idx} of {pending.query.id} should fit after best-fit selection")
-        deferred = tuple(run.deferred())
-        if deferred:
-            self.backlog_order.append(pending.query.id)
-        admission = self._k.Admission(query_id=pending.query.id, chosen_config=cfg,
-                                      admitted_calls=tuple(sorted(run.admitted)), deferred_calls=deferred,
-                                      is_fallback=is_fallback)
-        self.trace.append({"event": "admission", "t": now, "query": pending.query.id, "config": cfg.describe(),
-                           "admitted": list(admission.admitted_calls), "deferred": list(admission.deferred_calls),
-                           "fallback": is_fallback})
-        return admission
+                raise self._k.MemorySafetyViolation(f"call {idx} of {qid} should fit after best-fit selection")
+        later = tuple(run.deferred())
+        if later:
+            self.backlog_order.append(qid)
+        now_in = tuple(sorted(run.admitted))
+        self._log("admission", now, qid, config=cfg.describe(), admitted=list(now_in), deferred=list(later),
+                  fallback=is_fallback)
+        return self._k.Admission(query_id=qid, chosen_config=cfg, admitted_calls=now_in, deferred_calls=later,
+                                 is_fallback=is_fallback)
 
     def _pack(self, pending) -> tuple:
         key = id(pending)
@@ -378,46 +380,48 @@ class Scheduler:
         return "context window exceeded"
 
     def step(self, now: float):
-        """scheduler.py:397-410: deferred work first, then new queries in FIFO
-        order until the head cannot make progress."""
-        admissions: list = []
-        admitted: list = []
-        blocked = self._admit_backlog(now, admitted)
-        if not blocked and self.waiting:
-            self._admit_new(now, admissions, admitted)
-        return admissions, admitted
+        """One admission round (scheduler.py:397-410): the backlog, then — if
+        it did not block — new queries in FIFO order."""
+        decided, started = [], []
+        if not self._admit_backlog(now, started) and self.waiting:
+            self._admit_new(now, decided, started)
+        return decided, started
 
     # -- completion --------------------------------------------------------
 
     def complete(self, query_id: str, call_index: int, now: float, rerank_confidence: float | None = None):
-        """scheduler.py:414-466."""
+        """Release a finished call's KV bytes; settle the query after its last
+        call (map_rerank: the highest-confidence call wins, lowest index on
+        ties) — scheduler.py:414-466."""
         k = self._k
         run = self.active.get(query_id)
         if run is None:
             raise k.UnknownCall(f"no active query {query_id}")
-        if call_index not in run.admitted or call_index in run.completed:
+        if call_index in run.completed or call_index not in run.admitted:
             raise k.UnknownCall(f"call {call_index} of {query_id} is not running")
-        call = run.plan.calls[call_index]
-        self.used_bytes -= call.kv_bytes
+        done_before = set(run.completed)
+        self.used_bytes -= run.plan.calls[call_index].kv_bytes
         self._check_accounting()
         run.completed.add(call_index)
         if rerank_confidence is not None:
             run.rerank_confidences[call_index] = rerank_confidence
-        self.trace.append({"event": "completion", "t": now, "query": query_id, "call": call_index})
+        self._log("completion", now, query_id, call=call_index)
+        # deferred calls this completion made ready (they were not before)
         newly_ready = tuple(i for i in run.deferred()
-                            if run.ready(i) and not (run.plan.calls[i].depends_on <= (run.completed - {call_index})))
+                            if run.ready(i) and not run.plan.calls[i].depends_on.issubset(done_before))
+        info = dict(config=run.config, is_fallback=run.is_fallback, newly_ready=newly_ready)
         if not run.done():
-            return k.CompletionInfo(query_done=False, config=run.config, is_fallback=run.is_fallback,
-                                    newly_ready=newly_ready)
-        winning = None
-        if run.config.synthesis_method.value == "map_rerank" and run.rerank_confidences:
-            winning = max(sorted(run.rerank_confidences), key=lambda i: run.rerank_confidences[i])
+            return k.CompletionInfo(query_done=False, **info)
+        conf = run.rerank_confidences
+        winner = None
+        if conf and run.config.synthesis_method.value == "map_rerank":
+            best = max(conf.values())
+            winner = min(i for i, v in conf.items() if v == best)
         del self.active[query_id]
         if query_id in self.backlog_order:
             self.backlog_order.remove(query_id)
-        self.trace.append({"event": "query_done", "t": now, "query": query_id, "winning_rerank": winning})
-        return k.CompletionInfo(query_done=True, config=run.config, is_fallback=run.is_fallback,
-                                newly_ready=newly_ready, winning_rerank=winning)
+        self._log("query_done", now, query_id, winning_rerank=winner)
+        return k.CompletionInfo(query_done=True, winning_rerank=winner, **info)
 
     def idle(self) -> bool:
         return not self.waiting and not self.active
