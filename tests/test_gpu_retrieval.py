@@ -63,6 +63,8 @@ SHAPES = [  # nq, n, d, k
     (1000, 20000, 256, 35),
     (300, 6000, 4096, 35),    # long rows: 64 k-blocks per tile
     (40, 9000, 1536, 7),
+    (33, 1000, 8, 5),         # one 16-byte row: a single partial k-block
+    (77, 3001, 16, 35),
 ]
 
 
