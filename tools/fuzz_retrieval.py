@@ -84,7 +84,9 @@ def main(seconds=300, seed=0, max_cases=None):
         n_cases += 1
         desc = {x: (str(cs[x]) if x == "dtype" else cs[x]) for x in ("dtype", "d", "n", "nq", "k", "algo", "base", "bias",
                                                                       "pieces")}
-        if res["violations"] or res["exact_rows"] < 0.8 * res["rows"]:
+        # id differences inside oracle near-ties are allowed (check_topk); the
+        # exact-row rate is only a smoke signal on batches large enough for it
+        if res["violations"] or (res["rows"] >= 16 and res["exact_rows"] < 0.8 * res["rows"]):
             n_bad += 1
             print("FAIL", desc, plan, res["violations"][:3], res["exact_rows"], res["rows"], flush=True)
     print(f"fuzz: {n_cases} cases, {n_bad} failures in {time.time() - t0:.0f} s (seed {seed})")
