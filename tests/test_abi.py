@@ -116,3 +116,36 @@ def test_packing_roundtrip():
     pr = batch.pack_profiles([p])[0]
     assert (pr["complexity_high"], pr["needs_joint_reasoning"], pr["pieces_required"], pr["summary_lo"],
             pr["summary_hi"], pr["confidence"]) == (1, 1, 4, 30, 90, 0.93)
+
+
+def test_argument_errors_return_codes_without_a_device(lib):
+    """Argument validation happens before any CUDA call: bad inputs come back as
+    RS_ERR_INVALID_ARG with a message (the Python layer raises ValueError),
+    nothing throws across the ABI."""
+    sp = _lib.SelectParamsC(131072, 1000, 10, 64, 35, 1, 10, 1, 0)
+    bad_sp = _lib.SelectParamsC(0, 1000, 10, 64, 35, 1, 10, 1, 0)
+    ap = _lib.AdmitParamsC(0, 0, 131072)  # capacity must be positive
+    res = lib.rs_admit_fifo(None, None, None, None, 0, ctypes.byref(sp), ctypes.byref(ap), None, None, None, None)
+    assert res == _lib.RS_ERR_INVALID_ARG and lib.rs_last_error()
+    dummy = ctypes.c_int64(0)
+    assert lib.rs_candidate_costs(None, None, None, 1, ctypes.byref(bad_sp), None, ctypes.addressof(dummy), None,
+                                  None, 0, None) == _lib.RS_ERR_INVALID_ARG
+    assert b"per_token_bytes" in lib.rs_last_error()
+    assert lib.rs_select(None, None, None, None, -1, ctypes.byref(sp), None, None, None, None,
+                         None) == _lib.RS_ERR_INVALID_ARG
+    assert lib.rs_plan_calls(None, None, 5, ctypes.byref(sp), 131072, None, None, None, None, None, 0,
+                             None) == _lib.RS_ERR_INVALID_ARG
+    assert lib.rs_parse_profiles(b"", None, -1, None, None, None, None, None, 0) == _lib.RS_ERR_INVALID_ARG
+    with pytest.raises(ValueError):
+        _lib.check(_lib.RS_ERR_INVALID_ARG, "probe")
+
+
+def test_parse_profiles_runs_on_the_host(lib):
+    """rs_parse_profiles is host code: it works in this GPU-less container."""
+    from paper_2412_10543_b200 import batch
+
+    recs, clamped, status, lines = batch.parse_profiles(
+        ["Complexity: High\nJoint Reasoning needed: No\nPieces: 12\nSummary range: 40-90", "nothing"], [0.5, 1.0])
+    assert list(status) == [batch.RS_PARSE_OK, batch.RS_PARSE_UNPARSEABLE]
+    assert recs[0]["pieces_required"] == 10 and clamped[0] == batch.RS_CLAMPED_PIECES
+    assert recs[0]["confidence"] == 0.5 and list(lines[0]) == [0, 1, 2, 3]
