@@ -234,10 +234,38 @@ __global__ void fill_empty_kernel(int64_t n, float* D, int64_t* I, uint64_t* key
   }
 }
 
+// One sorted list per query (the join after a single-shard search): the
+// merge is a prefix copy with the keep limit, one thread per output slot.
+__global__ void copy_topk_kernel(const uint64_t* __restrict__ keys, int64_t nq, int k_in, int64_t q_stride, int k,
+                                 const rs_config* __restrict__ keep, float* __restrict__ D, int64_t* __restrict__ I,
+                                 uint64_t* __restrict__ keys_out) {
+  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < nq * k; t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t q = t / k;
+    const int j = int(t - q * k);
+    int limit = k;
+    if (keep) {
+      const rs_config c = keep[q];
+      limit = (c.status == RS_SELECT_BEST_FIT || c.status == RS_SELECT_FALLBACK) ? c.num_chunks : 0;
+      if (limit > k) limit = k;
+    }
+    const uint64_t v = j < k_in && j < limit ? keys[q * q_stride + j] : kEmptyKey;
+    const bool real = v != kEmptyKey;
+    if (keys_out) keys_out[t] = v;
+    if (D) D[t] = real ? key_dist(v) : __int_as_float(0x7f800000);
+    if (I) I[t] = real ? int64_t(uint32_t(v)) : int64_t(-1);
+  }
+}
+
 int launch_merge(const uint64_t* keys, int64_t nq, int nlists, int k_in, int64_t list_stride, int64_t q_stride,
                  int k, const rs_config* keep, float* D, int64_t* I, uint64_t* keys_out, cudaStream_t st) {
   RS_REQUIRE(nlists >= 1 && nlists <= 4096, "nlists out of range (%d)", nlists);
   RS_REQUIRE(k_in >= 1 && k_in <= 255, "k_in out of range (%d)", k_in);
+  if (nlists == 1) {
+    const int64_t blocks = std::min<int64_t>(ceil_div(nq * k, 256), 148 * 16);
+    copy_topk_kernel<<<(unsigned)blocks, 256, 0, st>>>(keys, nq, k_in, q_stride, k, keep, D, I, keys_out);
+    RS_CHECK_LAUNCH("copy_topk_kernel");
+    return RS_OK;
+  }
   const size_t smem = size_t(kMergeWarps) * nlists;
   const int64_t blocks = std::min<int64_t>(ceil_div(nq, kMergeWarps), 65535);
   if (smem > 48 * 1024) {
@@ -254,53 +282,76 @@ int launch_merge(const uint64_t* keys, int64_t nq, int nlists, int k_in, int64_t
 // each MMA's products into the fp32 TMEM accumulator with truncation, so at
 // d = 768 a near neighbour's dot (~0.9) drifts by ~1.4e-5 relative — above the
 // north star's 1e-5 fp32 tolerance.  The fused kernel therefore keeps
-// kc = k + kRefineExtra candidates per query, and this kernel recomputes
+// kc = k + kRefineExtra candidates per query, and the two kernels below recompute
 // their distances with fp32 FMAs on CUDA cores (lanes over the dimension,
 // float4 loads, warp reduction; error ~1e-7), ranks them by (distance, id)
 // and emits the top k — the FAISS semantics the oracle checks, at a cost of
 // nq * kc * d FMAs (negligible next to the GEMM).
-__global__ void __launch_bounds__(256) refine_fp32_kernel(const uint64_t* __restrict__ cand, int kc,
-                                                          const float* __restrict__ Q, const float* __restrict__ qn,
-                                                          const float* __restrict__ C, const float* __restrict__ cn,
-                                                          int64_t nq, int dim, int64_t id_base, int k,
-                                                          const rs_config* __restrict__ keep, float* __restrict__ D,
-                                                          int64_t* __restrict__ I, uint64_t* __restrict__ keys_out) {
+// Scoring: one warp per (query, 8 candidates); its four 8-lane groups each
+// hold one candidate row in flight (float4 loads spread over the group,
+// three in-group shuffles), two rows per group.  Thousands of independent
+// warps keep the random row gathers in flight — a warp per query left the
+// SMs ~12% occupied and latency-bound on these loads.
+constexpr int kRefinePerWarp = 8;
+__global__ void __launch_bounds__(256) refine_score_kernel(const uint64_t* __restrict__ cand, int kc,
+                                                           const float* __restrict__ Q, const float* __restrict__ qn,
+                                                           const float* __restrict__ C, const float* __restrict__ cn,
+                                                           int64_t nq, int dim, int64_t id_base,
+                                                           uint64_t* __restrict__ exact) {
   const int lane = threadIdx.x & 31;
-  const int64_t q = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  if (q >= nq) return;
+  const int chunks = (kc + kRefinePerWarp - 1) / kRefinePerWarp;
+  const int64_t wid = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (wid >= nq * chunks) return;
+  const int64_t q = wid / chunks;
+  const int c0 = int(wid - q * chunks) * kRefinePerWarp;
+  const int grp = lane >> 3, gl = lane & 7;
+  const unsigned gmask = 0xFFu << (grp * 8);
   const float4* qv = reinterpret_cast<const float4*>(Q + q * dim);
   const int d4 = dim / 4;
   const float qq = qn[q];
-  // lane j owns candidates j and j + 32 (kc <= 40 < 64)
-  uint64_t mine[2] = {kEmptyKey, kEmptyKey};
-  for (int j = 0; j < kc; ++j) {
+  for (int j = c0 + grp; j < c0 + kRefinePerWarp && j < kc; j += 4) {
     const uint64_t key = cand[q * kc + j];
-    if (key == kEmptyKey) break;  // sorted: the rest is padding
-    const int64_t row = int64_t(uint32_t(key)) - id_base;
-    const float4* cv = reinterpret_cast<const float4*>(C + row * dim);
-    float acc = 0.0f;
-    for (int i = lane; i < d4; i += 32) {
-      const float4 a = qv[i], b = cv[i];
-      acc = fmaf(a.x, b.x, acc);
-      acc = fmaf(a.y, b.y, acc);
-      acc = fmaf(a.z, b.z, acc);
-      acc = fmaf(a.w, b.w, acc);
-    }
+    uint64_t out = kEmptyKey;
+    if (key != kEmptyKey) {  // group-uniform
+      const int64_t row = int64_t(uint32_t(key)) - id_base;
+      const float4* cv = reinterpret_cast<const float4*>(C + row * dim);
+      float acc = 0.0f;
+      for (int i = gl; i < d4; i += 8) {
+        const float4 a = qv[i], b = cv[i];
+        acc = fmaf(a.x, b.x, acc);
+        acc = fmaf(a.y, b.y, acc);
+        acc = fmaf(a.z, b.z, acc);
+        acc = fmaf(a.w, b.w, acc);
+      }
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-    float dist = fmaf(-2.0f, acc, qq + cn[row]);
-    dist = dist > 0.0f ? dist : 0.0f;  // FAISS clamps round-off at 0 (and NaN -> 0)
-    const uint64_t ek = (uint64_t(__float_as_uint(dist)) << 32) | uint32_t(key);
-    if (j == lane) mine[0] = ek;
-    if (j == lane + 32) mine[1] = ek;
+      for (int off = 4; off > 0; off >>= 1) acc += __shfl_xor_sync(gmask, acc, off);
+      float dist = fmaf(-2.0f, acc, qq + cn[row]);
+      dist = dist > 0.0f ? dist : 0.0f;  // FAISS clamps round-off at 0 (and NaN -> 0)
+      out = (uint64_t(__float_as_uint(dist)) << 32) | uint32_t(key);
+    }
+    if (gl == 0) exact[q * kc + j] = out;
   }
+}
+
+// Ranking: one warp per query; lane j owns candidates j and j + 32 (kc <= 40
+// < 64); ranks by (exact distance, id) and writes the top k with the keep
+// limit.  Keys are unique except the padding.
+__global__ void __launch_bounds__(256) refine_rank_kernel(const uint64_t* __restrict__ exact, int kc, int64_t nq,
+                                                          int k, const rs_config* __restrict__ keep,
+                                                          float* __restrict__ D, int64_t* __restrict__ I,
+                                                          uint64_t* __restrict__ keys_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t q = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (q >= nq) return;
+  uint64_t mine[2];
+  mine[0] = lane < kc ? exact[q * kc + lane] : kEmptyKey;
+  mine[1] = lane + 32 < kc ? exact[q * kc + lane + 32] : kEmptyKey;
   int limit = k;
   if (keep) {
     const rs_config c = keep[q];
     limit = (c.status == RS_SELECT_BEST_FIT || c.status == RS_SELECT_FALLBACK) ? c.num_chunks : 0;
     if (limit > k) limit = k;
   }
-  // rank of each owned key among all candidates (keys are unique except padding)
   int rank[2] = {0, 0};
   for (int j = 0; j < 64; ++j) {
     const uint64_t o = shfl_u64(mine[j >> 5], j & 31);
@@ -319,14 +370,16 @@ __global__ void __launch_bounds__(256) refine_fp32_kernel(const uint64_t* __rest
   }
 }
 
-int launch_refine_fp32(const uint64_t* cand, int kc, const float* Q, const float* qn, const float* C,
-                       const float* cn, int64_t nq, int dim, int64_t id_base, int k, const rs_config* keep, float* D,
-                       int64_t* I, uint64_t* keys_out, cudaStream_t st) {
+int launch_refine_fp32(const uint64_t* cand, uint64_t* exact, int kc, const float* Q, const float* qn,
+                       const float* C, const float* cn, int64_t nq, int dim, int64_t id_base, int k,
+                       const rs_config* keep, float* D, int64_t* I, uint64_t* keys_out, cudaStream_t st) {
   RS_REQUIRE(kc >= k && kc <= 64 && dim % 4 == 0, "refine: bad shape");
-  const int64_t blocks = ceil_div(nq * 32, 256);
-  refine_fp32_kernel<<<(unsigned)blocks, 256, 0, st>>>(cand, kc, Q, qn, C, cn, nq, dim, id_base, k, keep, D, I,
-                                                       keys_out);
-  RS_CHECK_LAUNCH("refine_fp32_kernel");
+  const int64_t warps = nq * ((kc + kRefinePerWarp - 1) / kRefinePerWarp);
+  refine_score_kernel<<<(unsigned)ceil_div(warps * 32, 256), 256, 0, st>>>(cand, kc, Q, qn, C, cn, nq, dim, id_base,
+                                                                          exact);
+  RS_CHECK_LAUNCH("refine_score_kernel");
+  refine_rank_kernel<<<(unsigned)ceil_div(nq * 32, 256), 256, 0, st>>>(exact, kc, nq, k, keep, D, I, keys_out);
+  RS_CHECK_LAUNCH("refine_rank_kernel");
   return RS_OK;
 }
 
@@ -851,7 +904,7 @@ static int search_impl(rs_index* ix, const void* queries, int64_t nq, int32_t k,
     const int kc = std::min(k + kRefineExtra, kTcMaxK);
     rc = run_partial(ix, queries, nq, kc, id_base, st, &plan);
     if (rc) return rc;
-    const size_t cb = size_t(nq) * kc * sizeof(uint64_t);
+    const size_t cb = 2 * size_t(nq) * kc * sizeof(uint64_t);  // merged candidates + their exact keys
     if (cb > ix->cand_cap) {
       if (ix->cand) cudaFree(ix->cand);
       ix->cand = nullptr;
@@ -861,7 +914,7 @@ static int search_impl(rs_index* ix, const void* queries, int64_t nq, int32_t k,
     rc = launch_merge(ix->part, nq, plan.lists(), kc, kc, int64_t(plan.lists()) * kc, kc, nullptr, nullptr, nullptr,
                       ix->cand, st);
     if (rc) return rc;
-    return launch_refine_fp32(ix->cand, kc, static_cast<const float*>(queries), ix->qnorm,
+    return launch_refine_fp32(ix->cand, ix->cand + size_t(nq) * kc, kc, static_cast<const float*>(queries), ix->qnorm,
                               static_cast<const float*>(ix->data), ix->norms, nq, ix->dim, id_base, k, keep, D, I,
                               keys, st);
   }

@@ -123,7 +123,7 @@ struct __align__(8) SmemTailT {
 // and every 8-element k-step issues lo*hi + hi*lo + hi*hi into the same fp32
 // TMEM accumulator.  The accumulator's truncating adds leave ~1e-5 relative
 // error on large dots at d = 768, so the fp32 search keeps k + 8 candidates
-// and re-ranks them exactly (refine_fp32_kernel, retrieval.cu).
+// and re-ranks them exactly (refine_score_kernel + refine_rank_kernel, retrieval.cu).
 //
 // Pair tile height.  SM = false: M = 256 (128 query rows per CTA), the
 // accumulator of a tile fills 256 TMEM columns of all 128 lanes.  SM = true
