@@ -226,6 +226,65 @@ __global__ void __launch_bounds__(kMergeWarps * 32) merge_topk_kernel(
   }
 }
 
+// k-way merge for up to 64 lists per query, all state in registers: lane
+// l owns lists l and l + 32, holding each list's current head and the key
+// after it (prefetched, so the winner's global load leaves the critical
+// path).  The warp's minimum key is found with two 32-bit REDUX reductions
+// (distance bits, then the id among lanes tied on distance) and a ballot —
+// ids are unique, so the (distance, id) minimum is unique too.
+__global__ void __launch_bounds__(kMergeWarps * 32) merge_topk64_kernel(
+    const uint64_t* __restrict__ keys, int64_t nq, int nlists, int k_in, int64_t list_stride, int64_t q_stride,
+    int k, const rs_config* __restrict__ keep, float* __restrict__ D, int64_t* __restrict__ I,
+    uint64_t* __restrict__ keys_out) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int64_t q = int64_t(blockIdx.x) * kMergeWarps + w; q < nq; q += int64_t(gridDim.x) * kMergeWarps) {
+    const uint64_t* base = keys + q * q_stride;
+    uint64_t cur[2], nxt[2];
+    int head[2] = {0, 0};
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const int l = lane + 32 * t;
+      const uint64_t* lp = base + int64_t(l) * list_stride;
+      cur[t] = l < nlists ? lp[0] : kEmptyKey;
+      nxt[t] = (l < nlists && k_in > 1) ? lp[1] : kEmptyKey;
+    }
+    int limit = k;
+    if (keep) {
+      const rs_config c = keep[q];
+      limit = (c.status == RS_SELECT_BEST_FIT || c.status == RS_SELECT_FALLBACK) ? c.num_chunks : 0;
+      if (limit > k) limit = k;
+    }
+    int j = 0;
+    for (; j < limit; ++j) {
+      const int tb = cur[1] < cur[0] ? 1 : 0;
+      const uint64_t mine = cur[tb];
+      const uint32_t hi = uint32_t(mine >> 32);
+      const uint32_t dmin = __reduce_min_sync(0xffffffffu, hi);
+      const uint32_t idmin = __reduce_min_sync(0xffffffffu, hi == dmin ? uint32_t(mine) : 0xffffffffu);
+      const uint64_t v = (uint64_t(dmin) << 32) | idmin;
+      if (v == kEmptyKey) break;  // every list is exhausted
+      const unsigned win = __ballot_sync(0xffffffffu, mine == v);
+      if (lane == 0) {
+        if (keys_out) keys_out[q * k + j] = v;
+        if (D) D[q * k + j] = key_dist(v);
+        if (I) I[q * k + j] = int64_t(uint32_t(v));
+      }
+      if (lane == __ffs(win) - 1) {
+        // advance the winning list: the prefetched key moves up, the next one is requested
+        const int h = ++head[tb];
+        cur[tb] = nxt[tb];
+        const int l = lane + 32 * tb;
+        nxt[tb] = h + 1 < k_in ? base[int64_t(l) * list_stride + h + 1] : kEmptyKey;
+      }
+    }
+    for (int jj = j + lane; jj < k; jj += 32) {  // padding past the limit / the lists
+      if (keys_out) keys_out[q * k + jj] = kEmptyKey;
+      if (D) D[q * k + jj] = __int_as_float(0x7f800000);
+      if (I) I[q * k + jj] = -1;
+    }
+  }
+}
+
 __global__ void fill_empty_kernel(int64_t n, float* D, int64_t* I, uint64_t* keys) {
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
     if (D) D[i] = __int_as_float(0x7f800000);
@@ -268,6 +327,12 @@ int launch_merge(const uint64_t* keys, int64_t nq, int nlists, int k_in, int64_t
   }
   const size_t smem = size_t(kMergeWarps) * nlists;
   const int64_t blocks = std::min<int64_t>(ceil_div(nq, kMergeWarps), 65535);
+  if (nlists <= 64) {
+    merge_topk64_kernel<<<(unsigned)blocks, kMergeWarps * 32, 0, st>>>(keys, nq, nlists, k_in, list_stride, q_stride,
+                                                                       k, keep, D, I, keys_out);
+    RS_CHECK_LAUNCH("merge_topk64_kernel");
+    return RS_OK;
+  }
   if (smem > 48 * 1024) {
     RS_CHECK_CUDA(cudaFuncSetAttribute(merge_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
                   "cudaFuncSetAttribute(merge_topk_kernel)");
