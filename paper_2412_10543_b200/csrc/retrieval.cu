@@ -750,10 +750,13 @@ int run_partial(rs_index* ix, const void* queries, int64_t nq, int k, int64_t id
       if (rc) return rc;
       rc = encode_kmajor_map(&tmql, ix->qlo, nq, ix->dim, qrows, RS_F32);
       if (rc) return rc;
-      rc = encode_kmajor_map(&tmcl, ix->lo, ix->ntotal, ix->dim, crows, RS_F32);
-      if (rc) return rc;
+      if (RS_TF32_STORED_LO) {
+        rc = encode_kmajor_map(&tmcl, ix->lo, ix->ntotal, ix->dim, crows, RS_F32);
+        if (rc) return rc;
+      }
     }
-    rc = pair ? launch_score_topk_pair(tmq, tf ? &tmql : nullptr, tmc, tf ? &tmcl : nullptr, ix->qnorm, ix->norms,
+    rc = pair ? launch_score_topk_pair(tmq, tf ? &tmql : nullptr, tmc, (tf && RS_TF32_STORED_LO) ? &tmcl : nullptr,
+                                       ix->qnorm, ix->norms,
                                        ix->cmin, nq, ix->ntotal, ix->dim, k, id_base, plan, small, ix->part,
                                        ix->sched_counter, ix->walk_bias, ix->qtau, st)
               : launch_score_topk_tc(tmq, tmc, ix->qnorm, ix->norms, nq, ix->ntotal, ix->dim, k, id_base, plan,
@@ -808,7 +811,8 @@ extern "C" int rs_index_create(int32_t dim, int32_t dtype, int64_t capacity, int
     if (e == cudaSuccess) e = cudaMalloc(&ix->norms, sizeof(float) * (capacity + rs::kTcBN));
     if (e == cudaSuccess) e = cudaMalloc(&ix->norm_max, sizeof(float));
     if (e == cudaSuccess) e = cudaMalloc(&ix->sched_counter, sizeof(int32_t) * (1 + rs::kMaxSegments));
-    if (e == cudaSuccess && dtype == RS_F32) e = cudaMalloc(&ix->lo, size_t(capacity) * dim * sizeof(float));
+    if (e == cudaSuccess && dtype == RS_F32 && RS_TF32_STORED_LO)
+      e = cudaMalloc(&ix->lo, size_t(capacity) * dim * sizeof(float));
     if (e == cudaSuccess) e = cudaMalloc(&ix->cmin, sizeof(float) * (rs::ceil_div(capacity, 256) * 8 + 8));
     if (e == cudaSuccess) e = cudaMemset(ix->norm_max, 0, sizeof(float));
     if (e != cudaSuccess) {
@@ -885,7 +889,7 @@ extern "C" int rs_index_add(rs_index* ix, const void* emb, int64_t n, void* stre
   if (rc) return rc;
   rc = rs::launch_chunk_min(ix->norms, ix->ntotal, ix->ntotal + n, ix->cmin, st);
   if (rc) return rc;
-  if (ix->dtype == RS_F32) {  // 3xTF32 residuals of the new rows
+  if (ix->dtype == RS_F32 && RS_TF32_STORED_LO) {  // 3xTF32 residuals of the new rows
     const size_t off = size_t(ix->ntotal) * ix->dim;
     rc = rs::launch_tf32_lo(static_cast<const float*>(ix->data) + off, n * ix->dim, ix->lo + off, st);
     if (rc) return rc;

@@ -32,6 +32,13 @@ SearchPlan plan_search(int64_t nq, int64_t n, int bq, int bn, int ctas_capacity,
 
 // tcgen05/TMA/TMEM bf16 kernel (score_topk_sm100.cu).
 constexpr int kTcMaxK = 40;
+// fp32 (3xTF32) path: 1 (default) = residuals precomputed at add() and
+// streamed as a second tensor; 0 = the corpus tf32 residual is formed in shared
+// memory by the pair kernel's converter warp (corpus stored and streamed once;
+// measured slower: cfg1 0.99M vs 1.45M q/s, the one converter warp limits)
+#ifndef RS_TF32_STORED_LO
+#define RS_TF32_STORED_LO 1
+#endif
 // fp32 (3xTF32) path: extra candidates kept for the exact fp32 re-rank
 constexpr int kRefineExtra = 8;
 constexpr int kTcBM = 128;

@@ -87,7 +87,9 @@ constexpr int EPI_WARP0 = 0;
 constexpr int WARP_TMEM = 4 * EG + 1;
 constexpr int WARP_PROD = 4 * EG + 2;
 constexpr int WARP_MMA = 4 * EG + 3;
+constexpr int WARP_CVT = 4 * EG;  // tf32 path: the corpus residual converter
 #else
+constexpr int WARP_CVT = 3;
 constexpr int EPI_WARP0 = 4;
 constexpr int WARP_PROD = 0;
 constexpr int WARP_MMA = 1;
@@ -106,6 +108,7 @@ static_assert(HB % G == 0 && BPIECE % 8 == 0, "corpus piece must be whole swizzl
 template <int S>
 struct __align__(8) SmemTailT {
   uint64_t full[S];
+  uint64_t braw[S];  // tf32 path: this CTA's raw corpus tile landed (local TMA)
   uint64_t empty[S];
   uint64_t tfull[2];
   uint64_t tempty[2];
@@ -114,6 +117,7 @@ struct __align__(8) SmemTailT {
   int32_t uid[URING];
   int32_t ustart[URING];  // absolute frontier tile the unit starts at
   uint32_t tmem_base;
+  int32_t cvt_stop;  // tf32 path: stages the producer issued (set when it is done)
 };
 
 // Operand precision.  bf16: one kind::f16 MMA per 16-element k-step.  fp32
@@ -133,6 +137,14 @@ struct __align__(8) SmemTailT {
 // again in quadrants 2 / 3 for columns 128-255, 128 TMEM columns per tile.
 // Each epilogue warp then owns half the columns of 32 rows, so a row keeps
 // two top-k lists per unit (merged downstream like the segments).
+//
+// With RS_TF32_STORED_LO = 0 (a measured-slower option; the default streams
+// precomputed residuals) the corpus residual is formed in shared memory: each CTA's raw fp32 corpus tile arrives by a local TMA on
+// braw[s]; the converter warp writes lo = x - trunc_tf32(x) next to it,
+// issues fence.proxy.async (generic-proxy stores -> the tensor core's async
+// proxy) and arrives on the leader's full[s], which therefore counts the
+// producer's expect_tx arrival plus both CTAs' converter arrivals.  The
+// corpus is then streamed at 4 bytes per element and stored once.
 template <bool TF, bool SM = false>
 struct Cfg {
   static constexpr int BK = TF ? 32 : 64;  // elements per k-block (one 128-byte row)
@@ -310,7 +322,8 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   }
   if (warp == WARP_MMA && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&tail->full[s], 1);
+      mbar_init(&tail->full[s], (TF && !RS_TF32_STORED_LO) ? 3 : 1);
+      mbar_init(&tail->braw[s], 1);
       mbar_init(&tail->empty[s], G);  // one MMA commit per pair of the cluster
     }
     for (int a = 0; a < 2; ++a) {
@@ -321,6 +334,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       mbar_init(&tail->ufull[i], 1);
       mbar_init(&tail->uempty[i], scheduler ? UCONSUMERS : 1);
     }
+    tail->cvt_stop = 0x7fffffff;
     fence_barrier_init();
   }
   if (warp == WARP_TMEM) {
@@ -344,6 +358,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       const uint64_t pol_c = p.qtiles == 1 ? policy_evict_first() : policy_evict_normal();
       int stage = 0;
       uint32_t phase = 0;
+      int32_t issued = 0;  // k-block stages issued (the tf32 converter's stop count)
       for (uint32_t i = 0;; ++i) {
         int u;
         int32_t start = 0;
@@ -387,7 +402,11 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             if (leader) mbar_arrive_expect_tx(&tail->full[stage], 2 * (C::STAGE_BYTES - (load_a ? 0 : C::A_BYTESv)));
             if (load_a) tma_load_2d_pair(&tmq, full_leader, sa, kx, qrow0, pol_q);
 #else
-            if (leader) mbar_arrive_expect_tx(&tail->full[stage], 2 * C::STAGE_BYTES);
+            if (leader) {
+              // tf32 + in-kernel residual: only the query halves complete on full[s] by TMA
+              const uint32_t tx = (TF && !RS_TF32_STORED_LO) ? 2 * C::NT * C::A_BYTESv : 2 * C::STAGE_BYTES;
+              mbar_arrive_expect_tx(&tail->full[stage], tx);
+            }
             tma_load_2d_pair(&tmq, full_leader, sa, kx, qrow0, pol_q);
 #endif
             if (TF) tma_load_2d_pair(&tmql, full_leader, sa + C::A_BYTESv, kx, qrow0, pol_q);
@@ -397,20 +416,70 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 #else
               const int32_t crow0 = int32_t(c0) + int(half) * HB;
 #endif
-              tma_load_2d_pair(&tmc, full_leader, sa + C::OFF_B, kx, crow0, pol_c);
-              if (TF) tma_load_2d_pair(&tmcl, full_leader, sa + C::OFF_B + B_BYTES, kx, crow0, pol_c);
+              if (TF && !RS_TF32_STORED_LO) {
+                mbar_arrive_expect_tx(&tail->braw[stage], B_BYTES);
+                tma_load_2d(&tmc, &tail->braw[stage], sa + C::OFF_B, kx, crow0, pol_c);
+              } else {
+                tma_load_2d_pair(&tmc, full_leader, sa + C::OFF_B, kx, crow0, pol_c);
+                if (TF) tma_load_2d_pair(&tmcl, full_leader, sa + C::OFF_B + B_BYTES, kx, crow0, pol_c);
+              }
             } else {
               // piece pp of this half's corpus rows, written into the same smem
               // offset of every CTA holding this half in the cluster's G pairs
               tma_load_2d_pair_mc(&tmc, full_leader, sa + C::OFF_B + pp * BPIECE * ROW_BYTES, kx,
                                   int32_t(c0) + int(half) * HB + pp * BPIECE, mc_half, pol_c);
             }
+            ++issued;
             if (++stage == STAGES) {
               stage = 0;
               phase ^= 1;
             }
           }
         }
+      }
+      if (TF && !RS_TF32_STORED_LO) {
+        // no more tiles: publish the stage count, then wake the converter on
+        // the next stage's barrier once its previous use has drained (so the
+        // arrival cannot complete a second phase the converter has not seen)
+        mbar_wait(&tail->empty[stage], phase ^ 1);
+        *reinterpret_cast<volatile int32_t*>(&tail->cvt_stop) = issued;
+        mbar_arrive(&tail->braw[stage]);
+      }
+    }
+  } else if (TF && !RS_TF32_STORED_LO && warp == WARP_CVT) {
+    // ===== tf32 residual converter (both CTAs): lo = x - trunc_tf32(x) of
+    //       this CTA's corpus half, written beside the raw tile =====
+    int stage = 0, done = 0;
+    uint32_t phase = 0;
+    const uint32_t full_leader0 = mapa_shared(smem_u32(&tail->full[0]), pair_leader);
+    for (;;) {
+      mbar_wait(&tail->braw[stage], phase);
+      // the barrier completed either by a corpus tile or by the producer's
+      // final arrival, which follows its store of the issued-stage count
+      if (done == *reinterpret_cast<volatile int32_t*>(&tail->cvt_stop)) break;
+      ++done;
+      const float4* src = reinterpret_cast<const float4*>(smem + size_t(stage) * C::STAGE_BYTES + C::OFF_B);
+      float4* dst = reinterpret_cast<float4*>(smem + size_t(stage) * C::STAGE_BYTES + C::OFF_B + B_BYTES);
+#pragma unroll 4
+      for (int i = lane; i < B_BYTES / 16; i += 32) {
+        float4 v = src[i];
+        v.x -= __uint_as_float(__float_as_uint(v.x) & 0xffffe000u);
+        v.y -= __uint_as_float(__float_as_uint(v.y) & 0xffffe000u);
+        v.z -= __uint_as_float(__float_as_uint(v.z) & 0xffffe000u);
+        v.w -= __uint_as_float(__float_as_uint(v.w) & 0xffffe000u);
+        dst[i] = v;
+      }
+      fence_proxy_async_shared();  // the tensor core reads these stores through the async proxy
+      __syncwarp();
+      if (lane == 0) {
+        if (leader)
+          mbar_arrive(&tail->full[stage]);
+        else
+          mbar_arrive_cluster(full_leader0 + uint32_t(stage) * 8u);
+      }
+      if (++stage == STAGES) {
+        stage = 0;
+        phase ^= 1;
       }
     }
   } else if (warp == WARP_MMA) {
@@ -444,7 +513,10 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           if (!leader) continue;
           const uint32_t d_tmem = tmem_base + acc * C::ACC_COLS;
           for (int kb = 0; kb < p.kblocks; ++kb) {
-            PROF(2, mbar_wait(&tail->full[stage], phase));
+            if (TF && !RS_TF32_STORED_LO)  // the peer's converter stores are released at cluster scope
+              PROF(2, mbar_wait_cluster(&tail->full[stage], phase));
+            else
+              PROF(2, mbar_wait(&tail->full[stage], phase));
             tc_fence_after();
             const uint32_t a_addr = smem_u32(smem + size_t(stage) * C::STAGE_BYTES);
             const uint32_t b_addr = a_addr + C::OFF_B;
@@ -676,7 +748,7 @@ int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap* tmql, cons
                            int64_t n, int dim, int k, int64_t id_base, const SearchPlan& plan, bool small,
                            uint64_t* part, int32_t* counter, int32_t walk_bias, uint32_t* qtau, cudaStream_t st) {
   const bool tf = tmql != nullptr;
-  RS_REQUIRE(tf == (tmcl != nullptr), "tf32 path needs both lo maps");
+  RS_REQUIRE(!tf || !RS_TF32_STORED_LO || tmcl != nullptr, "tf32 path with stored residuals needs the corpus lo map");
   RS_REQUIRE(!tf || G == 1, "the tf32 path has no multicast (RS_PAIR_GROUP) variant");
   RS_REQUIRE(!small || G == 1, "the M = 128 variant has no multicast (RS_PAIR_GROUP) variant");
   RS_REQUIRE(plan.lists_per_seg == (small ? 2 : kPairEpiGroups), "plan lists per segment do not match the kernel");
@@ -709,7 +781,7 @@ int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap* tmql, cons
   p.cas_rank = (k + kCas - 1) / kCas;
   p.cunits = int64_t(plan.qtiles) * plan.segments;
   const CUtensorMap& ql = tf ? *tmql : tmq;
-  const CUtensorMap& cl = tf ? *tmcl : tmc;
+  const CUtensorMap& cl = (tf && tmcl) ? *tmcl : tmc;
   if (tf) return small ? launch_t<true, true>(tmq, ql, tmc, cl, p, plan.ctas, st)
                        : launch_t<true, false>(tmq, ql, tmc, cl, p, plan.ctas, st);
   return small ? launch_t<false, true>(tmq, ql, tmc, cl, p, plan.ctas, st)
