@@ -7,9 +7,11 @@ confidence gate + Algorithm-1 pruning, best-fit / fallback selection with the
 KV-memory and delay cost models, exact top-k retrieval over the corpus, and
 the join (each query's chunk ids truncated to its chosen ``num_chunks``).
 For N > 1 (``torchrun``, one process per GPU, NCCL) the corpus is sharded
-across the GPUs (strong scaling: the workload is fixed), the per-shard top-k
-lists are exchanged with one all-gather and merged per query slice, and the
-config stage is sharded by query.
+across the GPUs (strong scaling: the workload is fixed), each rank's top-k
+lists reach the owners of its query slices through the library's peer-memory
+exchange (CUDA IPC over NVLink: a scatter kernel stores them into the owners'
+regions, the owner's merge kernel waits on epoch flags; ``--exchange
+all_to_all`` uses NCCL instead), and the config stage is sharded by query.
 
 Prints ONE JSON line (rank 0).  Inputs are synthetic (seeded), larger than L2.
 """
@@ -251,6 +253,9 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--exchange", default="peer", choices=["peer", "all_to_all", "all_gather"],
+                    help="key exchange of the sharded path (N>1): the library's NVLink peer-memory kernels "
+                         "(default) or NCCL")
     ap.add_argument("--corpus-rows", type=int, default=None, help="override the corpus size (debug)")
     ap.add_argument("--queries", type=int, default=None,
                     help="override the queries per step (e.g. 128: the HBM-bound small-batch regime)")
@@ -324,6 +329,7 @@ def main():
     cost = batch.CostModel()
     index.reserve(nq, K)
 
+    exchange_used = None
     if world == 1:
         pipe = RetrieveSelect(index, params, k=K, cost=cost)
 
@@ -332,9 +338,27 @@ def main():
     else:
         window = batch.GateWindow(dev)
         ops = rdist.gpu_ops(index, params, window, cost=cost)
+        exchange, peer = args.exchange, None
+        if exchange == "peer":
+            try:
+                peer = rdist.PeerExchange(nq, K, device=dev)
+            except RuntimeError as e:  # e.g. no CUDA IPC between the ranks' containers: NCCL instead, reported
+                exchange_note = f"all_to_all (peer exchange unavailable: {str(e)[:120]})"
+                exchange = "all_to_all"
+        if peer is not None:
+            # the first batch through both exchanges must agree before the peer path is timed
+            a = rdist.sharded_retrieve_select(ops, queries, profiles, qlen, free, K, exchange="all_to_all")
+            b = rdist.sharded_retrieve_select(ops, queries, profiles, qlen, free, K, exchange="peer", peer=peer)
+            bad = torch.tensor([float(not (torch.equal(a[3], b[3]) and torch.equal(a[4], b[4])) or peer.error())],
+                               device=dev)
+            dist.all_reduce(bad, op=dist.ReduceOp.MAX)
+            if bad.item():
+                exchange_note = "all_to_all (peer exchange disagreed with NCCL on the check batch: disabled)"
+                exchange, peer = "all_to_all", None
+        exchange_used = exchange_note if exchange != args.exchange else exchange
 
         def step():
-            return rdist.sharded_retrieve_select(ops, queries, profiles, qlen, free, K)
+            return rdist.sharded_retrieve_select(ops, queries, profiles, qlen, free, K, exchange=exchange, peer=peer)
 
     def barrier():
         if world > 1:
@@ -398,7 +422,8 @@ def main():
                 return pipe.run_host(q_host, p_host, ql_host, fr_host, pinned_out=outbufs)
             qd, pd = q_host.to(dev, non_blocking=True), p_host.to(dev, non_blocking=True)
             qld, frd = ql_host.to(dev, non_blocking=True), fr_host.to(dev, non_blocking=True)
-            q0, q1, cfgs, D, I = rdist.sharded_retrieve_select(ops, qd, pd, qld, frd, K)
+            q0, q1, cfgs, D, I = rdist.sharded_retrieve_select(ops, qd, pd, qld, frd, K, exchange=exchange,
+                                                               peer=peer)
             out = (cfgs.cpu(), I.cpu())
             torch.cuda.synchronize()
             return out
@@ -476,6 +501,7 @@ def main():
             "config": {"workload": f"{args.workload}: {cfg['desc']}", "queries_per_step": nq, "corpus_rows": n,
                        "dim": d, "k": K, "corpus_shard_rows": n_shard,
                        "parallelism": f"corpus-sharded x{world}, query-sharded config stage",
+                       "exchange": exchange_used,
                        "l2": "inputs larger than L2 (corpus shard >> 126 MB), no flush"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_total,
             "clocks": clk, "plan": index.last_plan(),

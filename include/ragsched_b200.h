@@ -356,6 +356,49 @@ int rs_index_last_plan(const rs_index* index, int32_t* segments, int32_t* qtiles
 int rs_merge_topk(const uint64_t* keys, int64_t nq, int32_t nlists, int32_t k_in, int64_t list_stride,
                   int32_t k, const rs_config* cfg, float* D, int64_t* I, void* stream);
 
+/* ---- peer-memory key exchange (multi-GPU, one process per GPU) -----------
+ * The exchange step of the corpus-sharded search (the
+ * reference has none — it replaces the NCCL all-to-all of dist.py): every
+ * rank stores the key rows of query slice r (r*nq/world .. (r+1)*nq/world)
+ * straight into rank r's receive region over NVLink / NVSwitch, and rank r's
+ * merge waits in-kernel on the sources' epoch flags, then merges its slice.
+ * Regions are plain cudaMalloc allocations shared by CUDA IPC; the caller
+ * moves the 64-byte handles between processes (e.g. torch.distributed).
+ * Region layout: uint32 flags[RS_PEER_MAX] (flags[s] = last epoch source s
+ * delivered) | uint32 counter | int32 error | pad to 512 B | uint64
+ * keys[2 (epoch parity)][world (source)][slice_cap][k].  Epochs start at 1
+ * and increase by one per exchange; a rank may run at most one exchange
+ * ahead of the slowest peer's merge (guaranteed by stream order, since each
+ * rank's next scatter follows its own merge, which waits for every peer). */
+#define RS_PEER_MAX 64
+typedef struct rs_peer_exchange {
+  int32_t rank, world; /* world <= RS_PEER_MAX                                  */
+  int32_t k;           /* keys per query row                                    */
+  int32_t reserved;
+  int64_t slice_cap;   /* >= ceil(nq / world) for every nq exchanged            */
+  void* region[RS_PEER_MAX]; /* every rank's region as mapped in THIS process   */
+} rs_peer_exchange;
+
+int rs_peer_region_bytes(int32_t world, int64_t slice_cap, int32_t k, uint64_t* bytes);
+/* cudaMalloc + zero-fill on `device`; ipc_handle receives 64 bytes. */
+int rs_peer_alloc(uint64_t bytes, int32_t device, void** region, void* ipc_handle);
+int rs_peer_open(const void* ipc_handle, int32_t device, void** region);
+int rs_peer_close(void* region);
+int rs_peer_free(void* region);
+/* keys: device [nq, k] packed keys of this rank's shard (rs_index_search_keys);
+ * stores them into the owners' regions (parity epoch & 1); the last block to
+ * finish raises flags[rank] = epoch in every region (release, system scope). */
+int rs_peer_scatter_keys(const rs_peer_exchange* ex, const uint64_t* keys, int64_t nq, uint32_t epoch,
+                         void* stream);
+/* This rank's slice of the batch of nq queries: waits until every source's
+ * flag reaches `epoch` (at most timeout_ms; 0 = 60000), then the k-way merge
+ * of the world lists with rs_merge_topk's contract (D/I [slice, k]).  A
+ * timeout sets the region's error word (rs_peer_error) instead of hanging. */
+int rs_peer_merge_topk(const rs_peer_exchange* ex, int64_t nq, uint32_t epoch, int32_t k, const rs_config* cfg,
+                       float* D, int64_t* I, int32_t timeout_ms, void* stream);
+/* Reads (and optionally clears) this rank's error word; synchronous. */
+int rs_peer_error(const rs_peer_exchange* ex, int32_t clear, int32_t* error);
+
 /* Squared L2 norms of n rows of `dtype` (fp32 accumulate). */
 int rs_row_norms(const void* x, int64_t n, int32_t dim, int32_t dtype, float* out, void* stream);
 

@@ -92,6 +92,17 @@ _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
 _I32 = ctypes.c_int32
 
+PEER_MAX = 64
+PEER_HANDLE_BYTES = 64
+
+
+class PeerExchangeC(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("k", ctypes.c_int32),
+                ("reserved", ctypes.c_int32), ("slice_cap", ctypes.c_int64), ("region", _P * PEER_MAX)]
+
+
+_PX = ctypes.POINTER(PeerExchangeC)
+
 # exported symbol -> (restype, argtypes)
 SIGNATURES = {
     "rs_abi_version": (ctypes.c_int, []),
@@ -127,6 +138,14 @@ SIGNATURES = {
     "rs_parse_profiles": (ctypes.c_int, [ctypes.c_char_p, _P, _I64, _P, _P, _P, _P, _P, _I32]),
     "rs_admit_fifo": (ctypes.c_int, [_P, _P, _P, _P, _I64, ctypes.POINTER(SelectParamsC),
                                      ctypes.POINTER(AdmitParamsC), _P, _P, _P, _P]),
+    "rs_peer_region_bytes": (ctypes.c_int, [_I32, _I64, _I32, ctypes.POINTER(ctypes.c_uint64)]),
+    "rs_peer_alloc": (ctypes.c_int, [ctypes.c_uint64, _I32, ctypes.POINTER(_P), _P]),
+    "rs_peer_open": (ctypes.c_int, [_P, _I32, ctypes.POINTER(_P)]),
+    "rs_peer_close": (ctypes.c_int, [_P]),
+    "rs_peer_free": (ctypes.c_int, [_P]),
+    "rs_peer_scatter_keys": (ctypes.c_int, [_PX, _P, _I64, ctypes.c_uint32, _P]),
+    "rs_peer_merge_topk": (ctypes.c_int, [_PX, _I64, ctypes.c_uint32, _I32, _P, _P, _P, _I32, _P]),
+    "rs_peer_error": (ctypes.c_int, [_PX, _I32, ctypes.POINTER(_I32)]),
     "rs_launch_count": (ctypes.c_uint64, []),
     "rs_index_enable_timing": (ctypes.c_int, [_P, _I32]),
     "rs_index_kernel_times": (ctypes.c_int, [_P, _P, _I32, ctypes.POINTER(_I32)]),

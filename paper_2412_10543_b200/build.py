@@ -21,7 +21,7 @@ INCLUDE = os.path.join(ROOT, "include")
 OBJ = os.path.join(HERE, "_obj")
 LIB = os.path.join(HERE, "libragsched_b200.so")
 SOURCES = ["abi.cu", "select.cu", "gate.cu", "plan.cu", "retrieval.cu", "score_topk_sm100.cu", "score_topk_sm100_pair.cu",
-           "parse.cpp", "costs.cu"]
+           "parse.cpp", "costs.cu", "peer.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

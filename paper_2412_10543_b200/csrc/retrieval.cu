@@ -232,10 +232,45 @@ __global__ void __launch_bounds__(kMergeWarps * 32) merge_topk_kernel(
 // path).  The warp's minimum key is found with two 32-bit REDUX reductions
 // (distance bits, then the id among lanes tied on distance) and a ballot —
 // ids are unique, so the (distance, id) minimum is unique too.
+//
+// WAIT (the peer-exchange merge, peer.cu): the lists are written by other
+// GPUs over NVLink while the kernel starts, so each block first waits on the
+// sources' epoch flags and then reads the keys with ld.global.cv.
+template <bool WAIT>
+__device__ __forceinline__ uint64_t merge_key(const uint64_t* p) {
+  if constexpr (WAIT) return __ldcv(reinterpret_cast<const unsigned long long*>(p));
+  return *p;
+}
+
+__device__ __forceinline__ void peer_wait(const PeerWait& pw) {
+  if (threadIdx.x == 0) {
+    uint64_t t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (int s = 0; s < pw.n; ++s) {
+      for (;;) {
+        uint32_t f;
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(f) : "l"(pw.flags + s) : "memory");
+        if (int32_t(f - pw.epoch) >= 0) break;
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > pw.timeout_ns) {  // a source never arrived: flag it, merge what is there
+          atomicExch(pw.error, 1);
+          s = pw.n;
+          break;
+        }
+        __nanosleep(200);
+      }
+    }
+  }
+  __syncthreads();
+}
+
+template <bool WAIT>
 __global__ void __launch_bounds__(kMergeWarps * 32) merge_topk64_kernel(
-    const uint64_t* __restrict__ keys, int64_t nq, int nlists, int k_in, int64_t list_stride, int64_t q_stride,
+    const uint64_t* keys, int64_t nq, int nlists, int k_in, int64_t list_stride, int64_t q_stride,
     int k, const rs_config* __restrict__ keep, float* __restrict__ D, int64_t* __restrict__ I,
-    uint64_t* __restrict__ keys_out) {
+    uint64_t* __restrict__ keys_out, PeerWait pw) {
+  if constexpr (WAIT) peer_wait(pw);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int64_t q = int64_t(blockIdx.x) * kMergeWarps + w; q < nq; q += int64_t(gridDim.x) * kMergeWarps) {
     const uint64_t* base = keys + q * q_stride;
@@ -245,8 +280,8 @@ __global__ void __launch_bounds__(kMergeWarps * 32) merge_topk64_kernel(
     for (int t = 0; t < 2; ++t) {
       const int l = lane + 32 * t;
       const uint64_t* lp = base + int64_t(l) * list_stride;
-      cur[t] = l < nlists ? lp[0] : kEmptyKey;
-      nxt[t] = (l < nlists && k_in > 1) ? lp[1] : kEmptyKey;
+      cur[t] = l < nlists ? merge_key<WAIT>(lp) : kEmptyKey;
+      nxt[t] = (l < nlists && k_in > 1) ? merge_key<WAIT>(lp + 1) : kEmptyKey;
     }
     int limit = k;
     if (keep) {
@@ -274,7 +309,7 @@ __global__ void __launch_bounds__(kMergeWarps * 32) merge_topk64_kernel(
         const int h = ++head[tb];
         cur[tb] = nxt[tb];
         const int l = lane + 32 * tb;
-        nxt[tb] = h + 1 < k_in ? base[int64_t(l) * list_stride + h + 1] : kEmptyKey;
+        nxt[tb] = h + 1 < k_in ? merge_key<WAIT>(base + int64_t(l) * list_stride + h + 1) : kEmptyKey;
       }
     }
     for (int jj = j + lane; jj < k; jj += 32) {  // padding past the limit / the lists
@@ -328,8 +363,8 @@ int launch_merge(const uint64_t* keys, int64_t nq, int nlists, int k_in, int64_t
   const size_t smem = size_t(kMergeWarps) * nlists;
   const int64_t blocks = std::min<int64_t>(ceil_div(nq, kMergeWarps), 65535);
   if (nlists <= 64) {
-    merge_topk64_kernel<<<(unsigned)blocks, kMergeWarps * 32, 0, st>>>(keys, nq, nlists, k_in, list_stride, q_stride,
-                                                                       k, keep, D, I, keys_out);
+    merge_topk64_kernel<false><<<(unsigned)blocks, kMergeWarps * 32, 0, st>>>(
+        keys, nq, nlists, k_in, list_stride, q_stride, k, keep, D, I, keys_out, PeerWait{});
     RS_CHECK_LAUNCH("merge_topk64_kernel");
     return RS_OK;
   }
@@ -514,6 +549,17 @@ int launch_simt(int dtype, const void* Q, const float* qn, int64_t nq, const voi
 }
 
 }  // namespace
+
+int launch_merge_wait(const uint64_t* keys, int64_t nq, int nlists, int k_in, int64_t list_stride, int64_t q_stride,
+                      int k, const rs_config* keep, float* D, int64_t* I, const PeerWait& pw, cudaStream_t st) {
+  RS_REQUIRE(nlists >= 1 && nlists <= 64, "nlists out of range (%d)", nlists);
+  RS_REQUIRE(k_in >= 1 && k_in <= 255, "k_in out of range (%d)", k_in);
+  const int64_t blocks = std::min<int64_t>(ceil_div(nq, kMergeWarps), 65535);
+  merge_topk64_kernel<true><<<(unsigned)blocks, kMergeWarps * 32, 0, st>>>(keys, nq, nlists, k_in, list_stride,
+                                                                          q_stride, k, keep, D, I, nullptr, pw);
+  RS_CHECK_LAUNCH("merge_topk64_kernel<wait>");
+  return RS_OK;
+}
 
 // ---- 3xTF32 operand split ------------------------------------------------------
 __global__ void tf32_lo_kernel(const float4* __restrict__ x, int64_t n4, float4* __restrict__ lo) {

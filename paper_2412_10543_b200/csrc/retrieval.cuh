@@ -24,6 +24,21 @@ struct SearchPlan {
   int32_t lists() const { return segments * lists_per_seg; }
 };
 
+// In-kernel wait of the peer-exchange merge (peer.cu): every flag of
+// flags[0..n) must reach `epoch` (wrapping compare) before the lists are read;
+// after timeout_ns the kernel sets *error = 1 and merges what is there.
+struct PeerWait {
+  const uint32_t* flags = nullptr;
+  int32_t n = 0;
+  uint32_t epoch = 0;
+  int32_t* error = nullptr;
+  uint64_t timeout_ns = 0;
+};
+
+// K2 merge (nlists <= 64) that first waits on `pw` (lists written by peers)
+int launch_merge_wait(const uint64_t* keys, int64_t nq, int nlists, int k_in, int64_t list_stride, int64_t q_stride,
+                      int k, const rs_config* keep, float* D, int64_t* I, const PeerWait& pw, cudaStream_t st);
+
 // upper bound of SearchPlan::segments (plan_search never exceeds it)
 constexpr int kMaxSegments = 4096;
 

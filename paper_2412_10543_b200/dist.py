@@ -4,10 +4,14 @@ NVLink/NVSwitch) for the single exchange step.
 * Corpus sharding: rank r owns rows [r*N/P, (r+1)*N/P) with global ids
   starting at ``id_base = r*N/P``; every rank scores ALL queries against its
   shard (fused score + top-k) -> sorted top-k keys [nq, k] with global ids.
-* Exchange: ``all_to_all_single`` of the keys — rank r receives every
-  shard's list for its own query slice only (nq*k*8/P bytes from each peer;
-  2.3 MB out per rank at 8,192 x 35) — the only collective of the path
-  (``all_gather_into_tensor`` of the full key matrices is kept as an option).
+* Exchange: rank r receives every shard's list for its own query slice only
+  (nq*k*8/P bytes from each peer; 2.3 MB out per rank at 8,192 x 35) — the
+  only collective of the path.  ``exchange="peer"``: ``PeerExchange``, the
+  library's own NVLink exchange (``rs_peer_*``: a scatter kernel stores the
+  key rows straight into the owners' CUDA-IPC-mapped regions and raises epoch
+  flags; the owner's merge kernel waits on them in-kernel).
+  ``"all_to_all"``: NCCL ``all_to_all_single``; ``"all_gather"``: every rank
+  receives every full key matrix (P x more traffic).
 * Query sharding of the config stage: rank r gates the whole batch (the gate
   is order-dependent and O(nq)), selects its own query slice [q0, q1) and
   runs the k-way merge (K2) of the P shard lists for that slice, joined with
@@ -23,8 +27,12 @@ import os
 from dataclasses import dataclass
 from typing import Callable
 
+import ctypes
+
 import torch
 import torch.distributed as dist
+
+from . import _lib
 
 
 def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
@@ -63,8 +71,96 @@ def gpu_ops(index, pipeline_params, window, *, threshold=0.90, default_space=Non
     return ShardOps(search_keys, gate, select, merge)
 
 
+class PeerExchange:
+    """Peer-memory exchange of the sharded search's key lists over NVLink
+    (``rs_peer_*``, csrc/peer.cu).  Every rank allocates one region, shares its
+    CUDA IPC handle through ``torch.distributed`` (plumbing only) and maps the
+    others'.  ``merge(keys, nq, k, keep)`` scatters this rank's [nq, k_in] keys
+    to the slice owners and returns the merged (D, I) of this rank's slice;
+    both kernels run on the current stream, with no host synchronisation."""
+
+    def __init__(self, nq_max: int, k_in: int, *, group=None, device=None, timeout_ms: int = 0):
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.lib = _lib.lib_for_device(self.device.index)
+        self.k_in, self.timeout_ms, self.epoch = int(k_in), int(timeout_ms), 0
+        if self.world > _lib.PEER_MAX:
+            raise ValueError(f"peer exchange supports at most {_lib.PEER_MAX} ranks")
+        self.slice_cap = max(1, -(-int(nq_max) // self.world))
+        nbytes = ctypes.c_uint64()
+        _lib.check(self.lib.rs_peer_region_bytes(self.world, self.slice_cap, self.k_in, ctypes.byref(nbytes)))
+        own = ctypes.c_void_p()
+        handle = ctypes.create_string_buffer(_lib.PEER_HANDLE_BYTES)
+        _lib.check(self.lib.rs_peer_alloc(nbytes.value, self.device.index, ctypes.byref(own), handle),
+                   "rs_peer_alloc")
+        self._own = own.value
+        handles = [None] * self.world
+        dist.all_gather_object(handles, handle.raw, group=group)
+        self._opened = []
+        self._ex = _lib.PeerExchangeC(self.rank, self.world, self.k_in, 0, self.slice_cap)
+        err = None
+        try:
+            for r, h in enumerate(handles):
+                if r == self.rank:
+                    self._ex.region[r] = self._own
+                    continue
+                p = ctypes.c_void_p()
+                buf = ctypes.create_string_buffer(h, _lib.PEER_HANDLE_BYTES)
+                _lib.check(self.lib.rs_peer_open(buf, self.device.index, ctypes.byref(p)), "rs_peer_open")
+                self._opened.append(p.value)
+                self._ex.region[r] = p.value
+        except Exception as e:  # noqa: BLE001 - reported collectively below
+            err = f"rank {self.rank}: {e}"
+        # doubles as the barrier: every rank has mapped every region before the first store
+        errs = [None] * self.world
+        dist.all_gather_object(errs, err, group=group)
+        errs = [e for e in errs if e]
+        if errs:
+            self.close()
+            raise RuntimeError("peer exchange setup failed: " + "; ".join(errs))
+
+    def slice(self, nq: int) -> tuple[int, int]:
+        return shard_range(nq, self.rank, self.world)
+
+    def merge(self, keys: torch.Tensor, nq: int, k: int, keep: torch.Tensor | None = None, stream=None):
+        """Scatter ``keys`` [nq, k_in] (this rank's shard, global ids) and merge
+        this rank's slice -> (D [slice, k] fp32, I [slice, k] int64)."""
+        if keys.dtype != torch.int64 or keys.shape != (nq, self.k_in) or not keys.is_contiguous():
+            raise ValueError(f"keys must be a contiguous int64 [{nq}, {self.k_in}] tensor")
+        self.epoch = (self.epoch + 1) & 0xFFFFFFFF or 1
+        st = _lib.stream_ptr(stream)
+        _lib.check(self.lib.rs_peer_scatter_keys(ctypes.byref(self._ex), _lib.ptr(keys), nq, self.epoch, st),
+                   "rs_peer_scatter_keys")
+        q0, q1 = self.slice(nq)
+        D = torch.empty((q1 - q0, k), dtype=torch.float32, device=keys.device)
+        I = torch.empty((q1 - q0, k), dtype=torch.int64, device=keys.device)
+        _lib.check(self.lib.rs_peer_merge_topk(ctypes.byref(self._ex), nq, self.epoch, k, _lib.ptr(keep),
+                                               _lib.ptr(D), _lib.ptr(I), self.timeout_ms, st), "rs_peer_merge_topk")
+        return D, I
+
+    def error(self, clear: bool = False) -> int:
+        """1 if some merge timed out waiting for a peer (synchronous read)."""
+        out = ctypes.c_int32()
+        _lib.check(self.lib.rs_peer_error(ctypes.byref(self._ex), int(clear), ctypes.byref(out)))
+        return out.value
+
+    def close(self, barrier: bool = True) -> None:
+        if self._own is None:
+            return
+        torch.cuda.synchronize(self.device)
+        for p in self._opened:
+            self.lib.rs_peer_close(p)
+        self._opened = []
+        if barrier:  # no peer may still store into our region
+            dist.barrier(group=self.group)
+        self.lib.rs_peer_free(self._own)
+        self._own = None
+
+
 def sharded_retrieve_select(ops: ShardOps, queries, profiles, qlen, free_bytes, k: int, *, group=None,
-                            exchange: str = "all_to_all"):
+                            exchange: str = "all_to_all", peer: PeerExchange | None = None):
     """One batch through the sharded path on this rank.  All inputs are the
     full batch (replicated); returns (q0, q1, configs, D, I) for this rank's
     query slice.
@@ -72,12 +168,22 @@ def sharded_retrieve_select(ops: ShardOps, queries, profiles, qlen, free_bytes, 
     ``exchange="all_to_all"`` (default): each rank sends the keys of query
     slice r to rank r only (``all_to_all_single``, nq*k*8 bytes out per rank,
     and in: the P lists of its own slice).  ``"all_gather"``: every rank
-    receives every rank's full key matrix (P x more traffic)."""
+    receives every rank's full key matrix (P x more traffic).  ``"peer"``:
+    the same traffic as all_to_all through ``peer`` (a ``PeerExchange``),
+    stored by the library's kernels over NVLink, merged in the waiting
+    kernel."""
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     nq = queries.shape[0]
     keys = ops.search_keys(queries, k).contiguous()                     # [nq, k] local shard
     q0, q1 = shard_range(nq, rank, world)
+    if exchange == "peer":
+        if peer is None:
+            raise ValueError('exchange="peer" needs a PeerExchange')
+        spaces = ops.gate(profiles)
+        configs = ops.select(spaces[q0:q1], profiles[q0:q1], qlen[q0:q1], free_bytes[q0:q1])
+        D, I = peer.merge(keys, nq, k, keep=configs)
+        return q0, q1, configs, D, I
     if exchange == "all_to_all":
         sizes = [shard_range(nq, r, world)[1] - shard_range(nq, r, world)[0] for r in range(world)]
         recv = torch.empty(((q1 - q0) * world, k), dtype=keys.dtype, device=keys.device)  # source-rank-major

@@ -55,7 +55,7 @@ int main(void) {
          sizeof(rs_config), sizeof(rs_select_params), sizeof(rs_cost_model), sizeof(rs_gate_params),
          sizeof(rs_window), offsetof(rs_profile, confidence), sizeof(rs_call), sizeof(rs_admit_params),
          sizeof(rs_admit_info), sizeof(rs_admit_result));
-  printf("%zu\n", sizeof(rs_candidate));
+  printf("%zu %zu\n", sizeof(rs_candidate), sizeof(rs_peer_exchange));
   return 0;
 }
 """
@@ -71,7 +71,8 @@ int main(void) {
                      ctypes.sizeof(_lib.GateParamsC), _lib.WINDOW_DTYPE.itemsize,
                      _lib.PROFILE_DTYPE.fields["confidence"][1], _lib.CALL_DTYPE.itemsize,
                      ctypes.sizeof(_lib.AdmitParamsC), _lib.ADMIT_INFO_DTYPE.itemsize,
-                     _lib.ADMIT_RESULT_DTYPE.itemsize, _lib.CANDIDATE_DTYPE.itemsize]
+                     _lib.ADMIT_RESULT_DTYPE.itemsize, _lib.CANDIDATE_DTYPE.itemsize,
+                     ctypes.sizeof(_lib.PeerExchangeC)]
 
 
 def test_sass_contains_tcgen05_and_tma():

@@ -2,8 +2,11 @@
 slices) processes share cuda:0 over gloo (the pool gives one GPU per call;
 the measured configuration is NCCL, one GPU per rank, same code).  Each rank
 owns a corpus shard with global ids, runs the fused kernel, exchanges keys
-(all-to-all or all-gather), gates the batch, selects and merges its query
-slice; the concatenated result must equal the single-index pipeline."""
+(all-to-all, all-gather, or the library's peer-memory exchange through CUDA
+IPC mappings — here of the same device), gates the batch, selects and merges
+its query slice; the concatenated result must equal the single-index
+pipeline, for three consecutive batches with the peer exchange (both of its
+buffers and the epoch flags)."""
 
 import os
 import socket
@@ -55,18 +58,30 @@ def _worker(rank, world, port, exchange, q):
     ix = IndexFlatL2(D, capacity=r1 - r0, id_base=r0)
     ix.add(corpus[r0:r1].to(dev))
     params = batch.SelectParams(per_token_bytes=131072, chunk_size=1000, out_budget=10)
-    ops = rdist.gpu_ops(ix, params, batch.GateWindow(dev))
-    q0, q1, cfg, Dm, Im = rdist.sharded_retrieve_select(
-        ops, queries.to(dev), batch.to_device(prof, dev), torch.as_tensor(qlen, device=dev),
-        torch.as_tensor(free, device=dev), K, exchange=exchange)
+    peer = rdist.PeerExchange(NQ, K, device=dev) if exchange == "peer" else None
+    out = []
+    for it in range(_iters(exchange)):  # the peer exchange alternates its two buffers
+        ops = rdist.gpu_ops(ix, params, batch.GateWindow(dev))
+        q0, q1, cfg, Dm, Im = rdist.sharded_retrieve_select(
+            ops, queries.roll(it, 0).to(dev), batch.to_device(prof, dev), torch.as_tensor(qlen, device=dev),
+            torch.as_tensor(free, device=dev), K, exchange=exchange, peer=peer)
+        out.append((cfg.cpu().numpy(), Im.cpu().numpy()))
     torch.cuda.synchronize()
-    q.put((rank, q0, q1, cfg.cpu().numpy(), Im.cpu().numpy()))
+    if peer is not None:
+        assert peer.error() == 0
+        peer.close()
+    q.put((rank, q0, q1, out))
     ix.close()
     dist.destroy_process_group()
 
 
+def _iters(exchange):
+    return 3 if exchange == "peer" else 1
+
+
 @pytest.mark.timeout(600)
-@pytest.mark.parametrize("world,exchange", [(2, "all_to_all"), (3, "all_to_all"), (2, "all_gather")])
+@pytest.mark.parametrize("world,exchange", [(2, "all_to_all"), (3, "all_to_all"), (2, "all_gather"), (2, "peer"),
+                                            (3, "peer")])
 def test_multirank_sharded_path_equals_single_index(world, exchange):
     from paper_2412_10543_b200 import IndexFlatL2, batch
     from paper_2412_10543_b200.pipeline import RetrieveSelect
@@ -86,12 +101,14 @@ def test_multirank_sharded_path_equals_single_index(world, exchange):
     ix = IndexFlatL2(D, capacity=N)
     ix.add(corpus.to(dev))
     params = batch.SelectParams(per_token_bytes=131072, chunk_size=1000, out_budget=10)
-    ref = RetrieveSelect(ix, params).run(queries.to(dev), batch.to_device(prof, dev),
-                                         torch.as_tensor(qlen, device=dev), torch.as_tensor(free, device=dev))
-    torch.cuda.synchronize()
     assert [(r[1], r[2]) for r in res] == [(NQ * i // world, NQ * (i + 1) // world) for i in range(world)]
-    cfg = np.concatenate([r[3] for r in res])
-    Im = np.concatenate([r[4] for r in res])
-    np.testing.assert_array_equal(batch.from_device(torch.from_numpy(cfg), batch.CONFIG_DTYPE), ref.configs_np())
-    np.testing.assert_array_equal(Im, ref.chunk_ids.cpu().numpy())
+    for it in range(_iters(exchange)):
+        ref = RetrieveSelect(ix, params).run(queries.roll(it, 0).to(dev), batch.to_device(prof, dev),
+                                             torch.as_tensor(qlen, device=dev), torch.as_tensor(free, device=dev))
+        torch.cuda.synchronize()
+        cfg = np.concatenate([r[3][it][0] for r in res])
+        Im = np.concatenate([r[3][it][1] for r in res])
+        np.testing.assert_array_equal(batch.from_device(torch.from_numpy(cfg), batch.CONFIG_DTYPE),
+                                      ref.configs_np())
+        np.testing.assert_array_equal(Im, ref.chunk_ids.cpu().numpy())
     ix.close()
