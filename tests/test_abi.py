@@ -150,3 +150,20 @@ def test_parse_profiles_runs_on_the_host(lib):
     assert list(status) == [batch.RS_PARSE_OK, batch.RS_PARSE_UNPARSEABLE]
     assert recs[0]["pieces_required"] == 10 and clamped[0] == batch.RS_CLAMPED_PIECES
     assert recs[0]["confidence"] == 0.5 and list(lines[0]) == [0, 1, 2, 3]
+
+
+def test_peer_exchange_layout_and_argument_checks(lib):
+    """rs_peer_*: region size arithmetic and argument validation need no device
+    (the region header is 512 bytes, then two parity buffers of
+    [world][slice_cap][k] 8-byte keys)."""
+    nbytes = ctypes.c_uint64()
+    assert lib.rs_peer_region_bytes(8, 1024, 35, ctypes.byref(nbytes)) == _lib.RS_OK
+    assert nbytes.value == 512 + 2 * 8 * 1024 * 35 * 8
+    assert lib.rs_peer_region_bytes(_lib.PEER_MAX + 1, 1, 1, ctypes.byref(nbytes)) == _lib.RS_ERR_INVALID_ARG
+    ex = _lib.PeerExchangeC(2, 2, 35, 0, 16)  # rank == world
+    assert lib.rs_peer_scatter_keys(ctypes.byref(ex), None, 0, 1, None) == _lib.RS_ERR_INVALID_ARG
+    assert b"rank" in lib.rs_last_error()
+    ex = _lib.PeerExchangeC(0, 2, 35, 0, 16)  # regions not mapped
+    assert lib.rs_peer_merge_topk(ctypes.byref(ex), 32, 1, 35, None, None, None, 0, None) == _lib.RS_ERR_INVALID_ARG
+    assert b"region" in lib.rs_last_error()
+    assert lib.rs_peer_scatter_keys(None, None, 0, 1, None) == _lib.RS_ERR_INVALID_ARG
