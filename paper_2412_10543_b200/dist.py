@@ -129,7 +129,7 @@ class PeerExchange:
         this rank's slice -> (D [slice, k] fp32, I [slice, k] int64)."""
         if keys.dtype != torch.int64 or keys.shape != (nq, self.k_in) or not keys.is_contiguous():
             raise ValueError(f"keys must be a contiguous int64 [{nq}, {self.k_in}] tensor")
-        self.epoch = (self.epoch + 1) & 0xFFFFFFFF or 1
+        self.epoch = (self.epoch + 1) & 0xFFFFFFFF or 2  # skip 0 (initial flags), keep parity alternating
         st = _lib.stream_ptr(stream)
         _lib.check(self.lib.rs_peer_scatter_keys(ctypes.byref(self._ex), _lib.ptr(keys), nq, self.epoch, st),
                    "rs_peer_scatter_keys")
