@@ -59,6 +59,10 @@ constexpr int HB = BN / 2;      // corpus rows staged per CTA
 #ifndef RS_PAIR_STAGES_TF32
 #define RS_PAIR_STAGES_TF32 3
 #endif
+// corpus tiles prefetched into L2 ahead of the TMA loads (0 = off)
+#ifndef RS_PAIR_PREFETCH
+#define RS_PAIR_PREFETCH 0
+#endif
 constexpr int KREG = kTcMaxK;   // register top-k capacity (k <= 40)
 // candidate buffer per row; a warp flushes when one of its lanes holds more
 // than BUF - CHECK entries, so every flush batches many candidates per lane
@@ -422,6 +426,13 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
               } else {
                 tma_load_2d_pair(&tmc, full_leader, sa + C::OFF_B, kx, crow0, pol_c);
                 if (TF) tma_load_2d_pair(&tmcl, full_leader, sa + C::OFF_B + B_BYTES, kx, crow0, pol_c);
+              }
+              if (RS_PAIR_PREFETCH > 0 && j + RS_PAIR_PREFETCH < walk.ntiles) {
+                // the same box RS_PAIR_PREFETCH tiles ahead: the DRAM miss of the
+                // first unit to reach a tile no longer stalls the units in lockstep
+                const int32_t prow = int32_t(walk.c0(j + RS_PAIR_PREFETCH)) + int(half) * HB;
+                tma_prefetch_2d(&tmc, kx, prow);
+                if (TF && RS_TF32_STORED_LO) tma_prefetch_2d(&tmcl, kx, prow);
               }
             } else {
               // piece pp of this half's corpus rows, written into the same smem
