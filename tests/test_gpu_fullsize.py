@@ -1,0 +1,119 @@
+"""Retrieval parity at the BASELINE shapes themselves (cfg2: 10k x 1M x 768,
+cfg3: 10k x 2M x 1024, cfg4: 8,192 x 10M x 1024, bf16, k = 35), where the
+float64 oracle cannot scan the corpus in test time.  Checked instead:
+
+* every query (all of them): rows sorted by (distance, id), ids unique and
+  in range, and each returned distance equal to the float64 distance of the
+  returned id within the north-star tolerance (1e-3 of |q|^2 + |c|^2);
+* a 128-query sample: the exact top-k.  Candidates come from an fp32 torch
+  scan of the whole corpus (bf16 products are exact in fp32; the sum's
+  rounding, ~1e-6, is far inside the margin of k + 16 candidates), are
+  re-scored in float64 and ranked by (distance, id) — the oracle's rule — and
+  the kernel's result must match them under ``oracle.check_topk``'s tie rules.
+
+Synthetic data as in bench.py: unit-norm N(0, 1) rows, half the queries
+noisy neighbours normalize(c_j + 0.5 z / sqrt(d)) of corpus rows."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import retrieval_oracle as ro
+from paper_2412_10543_b200 import IndexFlatL2
+
+pytestmark = pytest.mark.gpu
+
+K, SAMPLE, MARGIN = 35, 128, 16
+
+
+def _corpus(n, d, seed, dev):
+    g = torch.Generator(device=dev).manual_seed(seed)
+    c = torch.empty(n, d, dtype=torch.bfloat16, device=dev)
+    for r0 in range(0, n, 1 << 20):
+        blk = torch.randn(min(1 << 20, n - r0), d, generator=g, device=dev)
+        c[r0:r0 + blk.shape[0]] = torch.nn.functional.normalize(blk, dim=1).bfloat16()
+    return c
+
+
+def _queries(c, nq, seed, dev):
+    g = torch.Generator(device=dev).manual_seed(seed + 1)
+    d = c.shape[1]
+    z = torch.randn(nq, d, generator=g, device=dev)
+    src = torch.randint(0, c.shape[0], (nq // 2,), generator=g, device=dev)
+    z[: nq // 2] = c[src].float() + 0.5 * z[: nq // 2] / d ** 0.5
+    return torch.nn.functional.normalize(z, dim=1).bfloat16()
+
+
+def _exact_f64(q, c, ids):
+    """float64 squared L2 of q[i] against c[ids[i, j]] -> [nq, m]."""
+    qd = q.double()
+    out = torch.empty(ids.shape, dtype=torch.float64, device=q.device)
+    for r0 in range(0, ids.shape[0], 1024):
+        rows = c[ids[r0:r0 + 1024].clamp_min(0)].double()            # [b, m, d]
+        qq = qd[r0:r0 + 1024, None, :]
+        out[r0:r0 + 1024] = ((rows - qq) ** 2).sum(-1)
+    return out
+
+
+def _reference_topk(qs, c, k):
+    """Exact (distance, id) top-k of the sample queries (see module doc)."""
+    qf = qs.float()
+    qn = (qf * qf).sum(1, keepdim=True)
+    best_d = torch.full((qs.shape[0], 0), float("inf"), device=qs.device)
+    best_i = torch.empty((qs.shape[0], 0), dtype=torch.int64, device=qs.device)
+    for r0 in range(0, c.shape[0], 1 << 21):
+        cb = c[r0:r0 + (1 << 21)].float()
+        dist = qn + (cb * cb).sum(1)[None] - 2.0 * (qf @ cb.T)
+        dd, ii = torch.topk(dist, k + MARGIN, dim=1, largest=False)
+        best_d = torch.cat([best_d, dd], 1)
+        best_i = torch.cat([best_i, ii + r0], 1)
+        best_d, sel = torch.topk(best_d, k + MARGIN, dim=1, largest=False)
+        best_i = torch.gather(best_i, 1, sel)
+    exact = _exact_f64(qs, c, best_i).cpu().numpy()
+    ids = best_i.cpu().numpy()
+    order = np.lexsort((ids, exact), axis=1)[:, :k]
+    return np.take_along_axis(exact, order, 1), np.take_along_axis(ids, order, 1)
+
+
+class _Rows:
+    """corpus[ids] -> float64 numpy rows (what check_topk indexes)."""
+
+    def __init__(self, c):
+        self.c = c
+
+    def __getitem__(self, ids):
+        return self.c[torch.as_tensor(ids, device=self.c.device)].double().cpu().numpy()
+
+
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("nq,n,d", [(10_000, 1_000_000, 768), (10_000, 2_000_000, 1024),
+                                    (8_192, 10_000_000, 1024)], ids=["cfg2", "cfg3", "cfg4"])
+def test_fullsize_retrieval(nq, n, d):
+    dev = torch.device("cuda", 0)
+    c = _corpus(n, d, 0, dev)
+    q = _queries(c, nq, 0, dev)
+    ix = IndexFlatL2(d, capacity=n)
+    ix.add(c)
+    D, I = ix.search(q, K)
+    torch.cuda.synchronize()
+    plan = ix.last_plan()
+    ix.close()
+    assert plan["algo"] == "tcgen05"
+    # all queries: order, uniqueness, range, distance of the returned id
+    assert bool((I >= 0).all() and (I < n).all())
+    assert bool((D[:, 1:] >= D[:, :-1]).all())
+    same = D[:, 1:] == D[:, :-1]
+    assert not bool((same & (I[:, 1:] <= I[:, :-1])).any()), "ties must go to the lower id"
+    srt = I.sort(1).values
+    assert not bool((srt[:, 1:] == srt[:, :-1]).any()), "duplicate ids"
+    true_d = _exact_f64(q, c, I)
+    scale = (q.double() ** 2).sum(1, keepdim=True) + _exact_f64(torch.zeros_like(q[:1]).expand(nq, d), c, I)
+    err = ((D.double() - true_d).abs() / scale).max().item()
+    assert err <= 1e-3, err
+    # a sample of queries against the exact top-k
+    rows = torch.linspace(0, nq - 1, SAMPLE, device=dev).long()
+    D_ref, I_ref = _reference_topk(q[rows], c, K)
+    res = ro.check_topk(D[rows].cpu().numpy(), I[rows].cpu().numpy(), q[rows].cpu(), _Rows(c), K, 1e-3,
+                        D_ref=D_ref, I_ref=I_ref)
+    assert not res["violations"], res["violations"][:5]
+    assert res["exact_rows"] >= 0.9 * SAMPLE, res
