@@ -739,7 +739,7 @@ int choose_algo(const rs_index* ix, int k) {
 }
 
 // small batches take the CTA pair's M = 128 tile: one tile, no padding rows
-bool pair_small(int64_t nq) { return nq <= rs::kSmallBatchMax && rs::kPairGroup == 1; }
+bool pair_small(int64_t nq) { return nq <= rs::kSmallBatchMax && rs::kPairGroup == 1 && rs::kPairEpiGroups == 1; }
 
 rs::SearchPlan make_plan(const rs_index* ix, int algo, int64_t nq, int64_t n, int k) {
   using namespace rs;

@@ -162,7 +162,6 @@ struct Cfg {
   static constexpr int STAGE_BYTES = NT * (A_BYTESv + B_BYTES);
   static constexpr int OFF_B = NT * A_BYTESv;  // stage layout: A hi | [A lo] | B hi | [B lo]
   static constexpr uint32_t IDESC = TF ? umma_idesc_tf32_f32(PMv, BN) : umma_idesc_bf16_f32(PMv, BN);
-  static_assert(!SM || EG == 1, "the M = 128 variant splits columns by lane quadrant, not by warp group");
   using Tail = SmemTailT<STAGES>;
   static constexpr size_t OFF_BUF = size_t(STAGES) * STAGE_BYTES;
   static constexpr size_t OFF_CN = OFF_BUF + size_t(BUF) * EPI_THREADS * 8;
@@ -762,6 +761,8 @@ int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap* tmql, cons
   RS_REQUIRE(!tf || !RS_TF32_STORED_LO || tmcl != nullptr, "tf32 path with stored residuals needs the corpus lo map");
   RS_REQUIRE(!tf || G == 1, "the tf32 path has no multicast (RS_PAIR_GROUP) variant");
   RS_REQUIRE(!small || G == 1, "the M = 128 variant has no multicast (RS_PAIR_GROUP) variant");
+  // (its epilogue splits columns by lane quadrant, not by warp group)
+  RS_REQUIRE(!small || EG == 1, "the M = 128 variant has one epilogue warp group");
   RS_REQUIRE(plan.lists_per_seg == (small ? 2 : kPairEpiGroups), "plan lists per segment do not match the kernel");
   RS_REQUIRE(plan.segments >= 1 && plan.segments <= kMaxSegments, "segments out of range (%d)", plan.segments);
   RS_CHECK_CUDA(cudaMemsetAsync(counter, 0, sizeof(int32_t) * (1 + plan.segments), st),
