@@ -398,6 +398,13 @@ int rs_peer_merge_topk(const rs_peer_exchange* ex, int64_t nq, uint32_t epoch, i
                        float* D, int64_t* I, int32_t timeout_ms, void* stream);
 /* Reads (and optionally clears) this rank's error word; synchronous. */
 int rs_peer_error(const rs_peer_exchange* ex, int32_t clear, int32_t* error);
+/* rs_index_search_keys fused with rs_peer_scatter_keys: the search's final
+ * k-way merge stores each query's key row straight into its slice owner's
+ * region and the same kernel raises the epoch flags (k must equal ex->k;
+ * searches whose final step is not that merge build the rows locally and
+ * scatter them).  Follow with rs_peer_merge_topk on every rank. */
+int rs_index_search_scatter(rs_index* index, const void* queries, int64_t nq, int32_t k, int64_t id_base,
+                            const rs_peer_exchange* ex, uint32_t epoch, void* stream);
 
 /* Squared L2 norms of n rows of `dtype` (fp32 accumulate). */
 int rs_row_norms(const void* x, int64_t n, int32_t dim, int32_t dtype, float* out, void* stream);

@@ -146,6 +146,7 @@ SIGNATURES = {
     "rs_peer_scatter_keys": (ctypes.c_int, [_PX, _P, _I64, ctypes.c_uint32, _P]),
     "rs_peer_merge_topk": (ctypes.c_int, [_PX, _I64, ctypes.c_uint32, _I32, _P, _P, _P, _I32, _P]),
     "rs_peer_error": (ctypes.c_int, [_PX, _I32, ctypes.POINTER(_I32)]),
+    "rs_index_search_scatter": (ctypes.c_int, [_P, _P, _I64, _I32, _I64, _PX, ctypes.c_uint32, _P]),
     "rs_launch_count": (ctypes.c_uint64, []),
     "rs_index_enable_timing": (ctypes.c_int, [_P, _I32]),
     "rs_index_kernel_times": (ctypes.c_int, [_P, _P, _I32, ctypes.POINTER(_I32)]),

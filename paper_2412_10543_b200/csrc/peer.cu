@@ -21,66 +21,18 @@
 namespace rs {
 namespace {
 
-constexpr size_t kCounterOff = 256;  // uint32, after flags[RS_PEER_MAX]
-constexpr size_t kErrorOff = 260;    // int32
-constexpr size_t kKeysOff = 512;
-
-__host__ __device__ inline uint32_t* region_flags(void* r) { return static_cast<uint32_t*>(r); }
-__host__ __device__ inline uint32_t* region_counter(void* r) {
-  return reinterpret_cast<uint32_t*>(static_cast<char*>(r) + kCounterOff);
-}
-__host__ __device__ inline int32_t* region_error(void* r) {
-  return reinterpret_cast<int32_t*>(static_cast<char*>(r) + kErrorOff);
-}
-__host__ __device__ inline uint64_t* region_keys(void* r) {
-  return reinterpret_cast<uint64_t*>(static_cast<char*>(r) + kKeysOff);
-}
-
-// first query row of rank o's slice (dist.shard_range)
-__device__ __forceinline__ int64_t slice_lo(int64_t nq, int o, int world) { return (int64_t(o) * nq) / world; }
-
 // One thread per key; consecutive threads walk a row, and rows of one owner
 // are contiguous at the destination, so the remote stores coalesce.
 __global__ void __launch_bounds__(256) peer_scatter_kernel(const uint64_t* __restrict__ keys, int64_t nq,
-                                                           rs_peer_exchange ex, uint32_t epoch) {
-  const int W = ex.world, k = ex.k;
-  const int64_t par = epoch & 1u;
+                                                           const __grid_constant__ rs_peer_exchange ex,
+                                                           uint32_t epoch) {
+  const int k = ex.k;
   const int64_t total = nq * k;
   for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
     const int64_t q = t / k;
-    const int j = int(t - q * k);
-    int o = int((q * W) / nq);
-    while (o + 1 < W && q >= slice_lo(nq, o + 1, W)) ++o;
-    while (q < slice_lo(nq, o, W)) --o;
-    uint64_t* dst = region_keys(ex.region[o]) + ((par * W + ex.rank) * ex.slice_cap + (q - slice_lo(nq, o, W))) * k + j;
-    *dst = keys[t];
+    peer_row(ex, nq, q, epoch)[t - q * k] = keys[t];
   }
-  // every thread's stores are ordered before the block's arrival; the last
-  // block then publishes the epoch to every owner (release, system scope)
-  __threadfence_system();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t* counter = region_counter(ex.region[ex.rank]);
-    const uint32_t prev = atomicAdd(counter, 1u);
-    if (prev == gridDim.x - 1) {
-      *counter = 0;  // every block has arrived; the next scatter is stream-ordered after this one
-      __threadfence_system();
-      for (int s = 0; s < W; ++s) {
-        uint32_t* f = region_flags(ex.region[s]) + ex.rank;
-        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(epoch) : "memory");
-      }
-    }
-  }
-}
-
-int check_exchange(const rs_peer_exchange* ex) {
-  RS_REQUIRE(ex != nullptr, "exchange is NULL");
-  RS_REQUIRE(ex->world >= 1 && ex->world <= RS_PEER_MAX, "world out of range (%d)", ex->world);
-  RS_REQUIRE(ex->rank >= 0 && ex->rank < ex->world, "rank out of range (%d)", ex->rank);
-  RS_REQUIRE(ex->k >= 1 && ex->k <= 255, "k out of range (%d)", ex->k);
-  RS_REQUIRE(ex->slice_cap >= 1, "slice_cap must be positive");
-  for (int r = 0; r < ex->world; ++r) RS_REQUIRE(ex->region[r] != nullptr, "region %d is NULL", r);
-  return RS_OK;
+  peer_signal(ex, epoch);
 }
 
 struct DevScope {
@@ -97,16 +49,36 @@ struct DevScope {
 };
 
 }  // namespace
+
+int check_peer_exchange(const rs_peer_exchange* ex) {
+  RS_REQUIRE(ex != nullptr, "exchange is NULL");
+  RS_REQUIRE(ex->world >= 1 && ex->world <= RS_PEER_MAX, "world out of range (%d)", ex->world);
+  RS_REQUIRE(ex->rank >= 0 && ex->rank < ex->world, "rank out of range (%d)", ex->rank);
+  RS_REQUIRE(ex->k >= 1 && ex->k <= 255, "k out of range (%d)", ex->k);
+  RS_REQUIRE(ex->slice_cap >= 1, "slice_cap must be positive");
+  for (int r = 0; r < ex->world; ++r) RS_REQUIRE(ex->region[r] != nullptr, "region %d is NULL", r);
+  return RS_OK;
+}
+
+int launch_peer_scatter(const rs_peer_exchange& ex, const uint64_t* keys, int64_t nq, uint32_t epoch,
+                        cudaStream_t st) {
+  // nq == 0 still launches one block: the flags must advance with the epoch
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(ceil_div(nq * ex.k, 256), 148 * 4));
+  peer_scatter_kernel<<<(unsigned)blocks, 256, 0, st>>>(keys, nq, ex, epoch);
+  RS_CHECK_LAUNCH("peer_scatter_kernel");
+  return RS_OK;
+}
+
 }  // namespace rs
 
 extern "C" int rs_peer_region_bytes(int32_t world, int64_t slice_cap, int32_t k, uint64_t* bytes) {
   RS_REQUIRE(world >= 1 && world <= RS_PEER_MAX && slice_cap >= 1 && k >= 1 && bytes, "bad arguments");
-  *bytes = rs::kKeysOff + 2ull * uint64_t(world) * uint64_t(slice_cap) * uint64_t(k) * 8ull;
+  *bytes = rs::kPeerKeysOff + 2ull * uint64_t(world) * uint64_t(slice_cap) * uint64_t(k) * 8ull;
   return RS_OK;
 }
 
 extern "C" int rs_peer_alloc(uint64_t bytes, int32_t device, void** region, void* ipc_handle) {
-  RS_REQUIRE(bytes >= rs::kKeysOff && region && ipc_handle, "bad arguments");
+  RS_REQUIRE(bytes >= rs::kPeerKeysOff && region && ipc_handle, "bad arguments");
   static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
   rs::DevScope g(device);
   void* p = nullptr;
@@ -150,20 +122,16 @@ extern "C" int rs_peer_free(void* region) {
 
 extern "C" int rs_peer_scatter_keys(const rs_peer_exchange* ex, const uint64_t* keys, int64_t nq, uint32_t epoch,
                                     void* stream) {
-  int rc = rs::check_exchange(ex);
+  int rc = rs::check_peer_exchange(ex);
   if (rc) return rc;
   RS_REQUIRE(nq >= 0 && (nq == 0 || keys), "bad arguments");
   RS_REQUIRE(rs::ceil_div(nq, ex->world) <= ex->slice_cap, "nq %lld exceeds world x slice_cap", (long long)nq);
-  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(rs::ceil_div(nq * ex->k, 256), 148 * 4));
-  // nq == 0 still launches one block: the flags must advance with the epoch
-  rs::peer_scatter_kernel<<<(unsigned)blocks, 256, 0, rs::as_stream(stream)>>>(keys, nq, *ex, epoch);
-  RS_CHECK_LAUNCH("peer_scatter_kernel");
-  return RS_OK;
+  return rs::launch_peer_scatter(*ex, keys, nq, epoch, rs::as_stream(stream));
 }
 
 extern "C" int rs_peer_merge_topk(const rs_peer_exchange* ex, int64_t nq, uint32_t epoch, int32_t k,
                                   const rs_config* cfg, float* D, int64_t* I, int32_t timeout_ms, void* stream) {
-  int rc = rs::check_exchange(ex);
+  int rc = rs::check_peer_exchange(ex);
   if (rc) return rc;
   RS_REQUIRE(nq >= 0 && k >= 1 && k <= 128 && timeout_ms >= 0, "bad arguments");
   RS_REQUIRE(rs::ceil_div(nq, ex->world) <= ex->slice_cap, "nq %lld exceeds world x slice_cap", (long long)nq);
@@ -172,21 +140,21 @@ extern "C" int rs_peer_merge_topk(const rs_peer_exchange* ex, int64_t nq, uint32
   RS_REQUIRE(D && I, "D/I are NULL");
   void* own = ex->region[ex->rank];
   rs::PeerWait pw;
-  pw.flags = rs::region_flags(own);
+  pw.flags = rs::peer_flags(own);
   pw.n = ex->world;
   pw.epoch = epoch;
-  pw.error = rs::region_error(own);
+  pw.error = rs::peer_error(own);
   pw.timeout_ns = uint64_t(timeout_ms ? timeout_ms : 60000) * 1000000ull;
-  const uint64_t* lists = rs::region_keys(own) + int64_t(epoch & 1u) * ex->world * ex->slice_cap * ex->k;
+  const uint64_t* lists = rs::peer_keys(own) + int64_t(epoch & 1u) * ex->world * ex->slice_cap * ex->k;
   return rs::launch_merge_wait(lists, q1 - q0, ex->world, ex->k, /*list_stride=*/ex->slice_cap * ex->k,
                                /*q_stride=*/ex->k, k, cfg, D, I, pw, rs::as_stream(stream));
 }
 
 extern "C" int rs_peer_error(const rs_peer_exchange* ex, int32_t clear, int32_t* error) {
-  int rc = rs::check_exchange(ex);
+  int rc = rs::check_peer_exchange(ex);
   if (rc) return rc;
   RS_REQUIRE(error, "error is NULL");
-  int32_t* e = rs::region_error(ex->region[ex->rank]);
+  int32_t* e = rs::peer_error(ex->region[ex->rank]);
   RS_CHECK_CUDA(cudaMemcpy(error, e, sizeof(int32_t), cudaMemcpyDeviceToHost), "read peer error");
   if (clear) RS_CHECK_CUDA(cudaMemset(e, 0, sizeof(int32_t)), "clear peer error");
   return RS_OK;

@@ -233,9 +233,20 @@ __global__ void __launch_bounds__(kMergeWarps * 32) merge_topk_kernel(
 // (distance bits, then the id among lanes tied on distance) and a ballot —
 // ids are unique, so the (distance, id) minimum is unique too.
 //
-// WAIT (the peer-exchange merge, peer.cu): the lists are written by other
-// GPUs over NVLink while the kernel starts, so each block first waits on the
-// sources' epoch flags and then reads the keys with ld.global.cv.
+// Modes.  kMergeWait (the owner's merge of the peer exchange, peer.cu): the
+// lists are written by other GPUs over NVLink while the kernel starts, so
+// each block first waits on the sources' epoch flags and then reads the keys
+// with ld.global.cv.  kMergeScatter (the last step of a sharded search): each
+// output row is stored straight into its slice owner's region (peer_row, over
+// NVLink for remote owners) and the grid signals the owners at the end — the
+// merge and the exchange are one kernel.
+constexpr int kMergePlain = 0, kMergeWait = 1, kMergeScatter = 2;
+
+struct PeerArgs {
+  PeerWait wait;
+  rs_peer_exchange ex;
+  uint32_t epoch;
+};
 template <bool WAIT>
 __device__ __forceinline__ uint64_t merge_key(const uint64_t* p) {
   if constexpr (WAIT) return __ldcv(reinterpret_cast<const unsigned long long*>(p));
@@ -265,15 +276,17 @@ __device__ __forceinline__ void peer_wait(const PeerWait& pw) {
   __syncthreads();
 }
 
-template <bool WAIT>
+template <int MODE>
 __global__ void __launch_bounds__(kMergeWarps * 32) merge_topk64_kernel(
     const uint64_t* keys, int64_t nq, int nlists, int k_in, int64_t list_stride, int64_t q_stride,
     int k, const rs_config* __restrict__ keep, float* __restrict__ D, int64_t* __restrict__ I,
-    uint64_t* __restrict__ keys_out, PeerWait pw) {
-  if constexpr (WAIT) peer_wait(pw);
+    uint64_t* __restrict__ keys_out, const __grid_constant__ PeerArgs pa) {
+  constexpr bool WAIT = MODE == kMergeWait;
+  if constexpr (WAIT) peer_wait(pa.wait);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int64_t q = int64_t(blockIdx.x) * kMergeWarps + w; q < nq; q += int64_t(gridDim.x) * kMergeWarps) {
     const uint64_t* base = keys + q * q_stride;
+    uint64_t* orow = MODE == kMergeScatter ? peer_row(pa.ex, nq, q, pa.epoch) : keys_out ? keys_out + q * k : nullptr;
     uint64_t cur[2], nxt[2];
     int head[2] = {0, 0};
 #pragma unroll
@@ -300,7 +313,7 @@ __global__ void __launch_bounds__(kMergeWarps * 32) merge_topk64_kernel(
       if (v == kEmptyKey) break;  // every list is exhausted
       const unsigned win = __ballot_sync(0xffffffffu, mine == v);
       if (lane == 0) {
-        if (keys_out) keys_out[q * k + j] = v;
+        if (orow) orow[j] = v;
         if (D) D[q * k + j] = key_dist(v);
         if (I) I[q * k + j] = int64_t(uint32_t(v));
       }
@@ -313,11 +326,12 @@ __global__ void __launch_bounds__(kMergeWarps * 32) merge_topk64_kernel(
       }
     }
     for (int jj = j + lane; jj < k; jj += 32) {  // padding past the limit / the lists
-      if (keys_out) keys_out[q * k + jj] = kEmptyKey;
+      if (orow) orow[jj] = kEmptyKey;
       if (D) D[q * k + jj] = __int_as_float(0x7f800000);
       if (I) I[q * k + jj] = -1;
     }
   }
+  if constexpr (MODE == kMergeScatter) peer_signal(pa.ex, pa.epoch);
 }
 
 __global__ void fill_empty_kernel(int64_t n, float* D, int64_t* I, uint64_t* keys) {
@@ -363,8 +377,8 @@ int launch_merge(const uint64_t* keys, int64_t nq, int nlists, int k_in, int64_t
   const size_t smem = size_t(kMergeWarps) * nlists;
   const int64_t blocks = std::min<int64_t>(ceil_div(nq, kMergeWarps), 65535);
   if (nlists <= 64) {
-    merge_topk64_kernel<false><<<(unsigned)blocks, kMergeWarps * 32, 0, st>>>(
-        keys, nq, nlists, k_in, list_stride, q_stride, k, keep, D, I, keys_out, PeerWait{});
+    merge_topk64_kernel<kMergePlain><<<(unsigned)blocks, kMergeWarps * 32, 0, st>>>(
+        keys, nq, nlists, k_in, list_stride, q_stride, k, keep, D, I, keys_out, PeerArgs{});
     RS_CHECK_LAUNCH("merge_topk64_kernel");
     return RS_OK;
   }
@@ -555,9 +569,25 @@ int launch_merge_wait(const uint64_t* keys, int64_t nq, int nlists, int k_in, in
   RS_REQUIRE(nlists >= 1 && nlists <= 64, "nlists out of range (%d)", nlists);
   RS_REQUIRE(k_in >= 1 && k_in <= 255, "k_in out of range (%d)", k_in);
   const int64_t blocks = std::min<int64_t>(ceil_div(nq, kMergeWarps), 65535);
-  merge_topk64_kernel<true><<<(unsigned)blocks, kMergeWarps * 32, 0, st>>>(keys, nq, nlists, k_in, list_stride,
-                                                                          q_stride, k, keep, D, I, nullptr, pw);
+  PeerArgs pa{};
+  pa.wait = pw;
+  merge_topk64_kernel<kMergeWait><<<(unsigned)blocks, kMergeWarps * 32, 0, st>>>(keys, nq, nlists, k_in, list_stride,
+                                                                                q_stride, k, keep, D, I, nullptr, pa);
   RS_CHECK_LAUNCH("merge_topk64_kernel<wait>");
+  return RS_OK;
+}
+
+int launch_merge_to_peers(const uint64_t* keys, int64_t nq, int nlists, int k_in, int64_t list_stride,
+                          int64_t q_stride, const rs_peer_exchange& ex, uint32_t epoch, cudaStream_t st) {
+  RS_REQUIRE(nlists >= 1 && nlists <= 64, "nlists out of range (%d)", nlists);
+  RS_REQUIRE(k_in >= 1 && k_in <= 255 && nq >= 1, "bad arguments");
+  const int64_t blocks = std::min<int64_t>(ceil_div(nq, kMergeWarps), 65535);
+  PeerArgs pa{};
+  pa.ex = ex;
+  pa.epoch = epoch;
+  merge_topk64_kernel<kMergeScatter><<<(unsigned)blocks, kMergeWarps * 32, 0, st>>>(
+      keys, nq, nlists, k_in, list_stride, q_stride, ex.k, nullptr, nullptr, nullptr, nullptr, pa);
+  RS_CHECK_LAUNCH("merge_topk64_kernel<scatter>");
   return RS_OK;
 }
 
@@ -678,6 +708,8 @@ struct rs_index {
   int64_t qnorm_cap = 0;
   uint64_t* part = nullptr;
   size_t part_cap = 0;  // bytes
+  uint64_t* skeys = nullptr;  // rs_index_search_scatter: local key rows when the merge cannot store to peers
+  size_t skeys_cap = 0;       // bytes
   rs::SearchPlan last;
   int32_t last_algo = 0;
   // optional per-search timing of the fused score kernel (event ring)
@@ -913,6 +945,7 @@ extern "C" int rs_index_destroy(rs_index* ix) {
   cudaFree(ix->qnorm);
   cudaFree(ix->qtau);
   cudaFree(ix->part);
+  cudaFree(ix->skeys);
   delete ix;
   return RS_OK;
 }
@@ -1001,17 +1034,30 @@ extern "C" int rs_index_last_plan(const rs_index* ix, int32_t* segments, int32_t
 }
 
 static int search_impl(rs_index* ix, const void* queries, int64_t nq, int32_t k, int64_t id_base,
-                       const rs_config* keep, float* D, int64_t* I, uint64_t* keys, void* stream) {
+                       const rs_config* keep, float* D, int64_t* I, uint64_t* keys, void* stream,
+                       const rs_peer_exchange* px = nullptr, uint32_t epoch = 0) {
   using namespace rs;
   int rc = check_search_args(ix, queries, nq, k, id_base);
   if (rc) return rc;
-  if (nq == 0) return RS_OK;
   DeviceGuard g(ix->device);
   cudaStream_t st = as_stream(stream);
+  if (px && nq > 0) {  // the key rows are built locally unless the final merge stores them to the peers
+    const size_t kb = size_t(nq) * k * sizeof(uint64_t);
+    if (kb > ix->skeys_cap) {
+      if (ix->skeys) cudaFree(ix->skeys);
+      ix->skeys = nullptr;
+      RS_CHECK_CUDA(cudaMalloc(&ix->skeys, kb), "cudaMalloc(scatter keys)");
+      ix->skeys_cap = kb;
+    }
+    keys = ix->skeys;
+  }
+  // after a local result: the peer scatter of its key rows (nq == 0 still signals)
+  auto finish = [&](int r) { return (r || !px) ? r : launch_peer_scatter(*px, keys, nq, epoch, st); };
+  if (nq == 0) return finish(RS_OK);
   if (ix->ntotal == 0) {
     fill_empty_kernel<<<(unsigned)std::min<int64_t>(ceil_div(nq * k, 256), 4096), 256, 0, st>>>(nq * k, D, I, keys);
     RS_CHECK_LAUNCH("fill_empty_kernel");
-    return RS_OK;
+    return finish(RS_OK);
   }
   SearchPlan plan;
   if (ix->dtype == RS_F32 && choose_algo(ix, k) == RS_ALGO_TCGEN05) {
@@ -1029,14 +1075,17 @@ static int search_impl(rs_index* ix, const void* queries, int64_t nq, int32_t k,
     rc = launch_merge(ix->part, nq, plan.lists(), kc, kc, int64_t(plan.lists()) * kc, kc, nullptr, nullptr, nullptr,
                       ix->cand, st);
     if (rc) return rc;
-    return launch_refine_fp32(ix->cand, ix->cand + size_t(nq) * kc, kc, static_cast<const float*>(queries), ix->qnorm,
-                              static_cast<const float*>(ix->data), ix->norms, nq, ix->dim, id_base, k, keep, D, I,
-                              keys, st);
+    return finish(launch_refine_fp32(ix->cand, ix->cand + size_t(nq) * kc, kc, static_cast<const float*>(queries),
+                                     ix->qnorm, static_cast<const float*>(ix->data), ix->norms, nq, ix->dim, id_base,
+                                     k, keep, D, I, keys, st));
   }
   rc = run_partial(ix, queries, nq, k, id_base, st, &plan);
   if (rc) return rc;
-  return launch_merge(ix->part, nq, plan.lists(), k, /*list_stride=*/k, /*q_stride=*/int64_t(plan.lists()) * k, k,
-                      keep, D, I, keys, st);
+  if (px && plan.lists() <= 64)  // the merge and the exchange in one kernel
+    return launch_merge_to_peers(ix->part, nq, plan.lists(), k, /*list_stride=*/k,
+                                 /*q_stride=*/int64_t(plan.lists()) * k, *px, epoch, st);
+  return finish(launch_merge(ix->part, nq, plan.lists(), k, /*list_stride=*/k, /*q_stride=*/int64_t(plan.lists()) * k,
+                             k, keep, D, I, keys, st));
 }
 
 extern "C" int rs_index_search(rs_index* ix, const void* queries, int64_t nq, int32_t k, int64_t id_base,
@@ -1049,6 +1098,16 @@ extern "C" int rs_index_search_keys(rs_index* ix, const void* queries, int64_t n
                                     uint64_t* keys, void* stream) {
   RS_REQUIRE(nq == 0 || keys != nullptr, "keys is NULL");
   return search_impl(ix, queries, nq, k, id_base, nullptr, nullptr, nullptr, keys, stream);
+}
+
+extern "C" int rs_index_search_scatter(rs_index* ix, const void* queries, int64_t nq, int32_t k, int64_t id_base,
+                                       const rs_peer_exchange* ex, uint32_t epoch, void* stream) {
+  int rc = rs::check_peer_exchange(ex);
+  if (rc) return rc;
+  RS_REQUIRE(ex->k == k, "k (%d) must equal the exchange's k (%d)", k, ex->k);
+  RS_REQUIRE(nq >= 0 && rs::ceil_div(nq, ex->world) <= ex->slice_cap, "nq %lld exceeds world x slice_cap",
+             (long long)nq);
+  return search_impl(ix, queries, nq, k, id_base, nullptr, nullptr, nullptr, nullptr, stream, ex, epoch);
 }
 
 extern "C" int rs_merge_topk(const uint64_t* keys, int64_t nq, int32_t nlists, int32_t k_in, int64_t list_stride,

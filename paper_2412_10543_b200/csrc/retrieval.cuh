@@ -39,6 +39,64 @@ struct PeerWait {
 int launch_merge_wait(const uint64_t* keys, int64_t nq, int nlists, int k_in, int64_t list_stride, int64_t q_stride,
                       int k, const rs_config* keep, float* D, int64_t* I, const PeerWait& pw, cudaStream_t st);
 
+// ---- peer-exchange regions (peer.cu; layout documented in ragsched_b200.h) ----
+constexpr size_t kPeerCounterOff = 256;  // uint32, after flags[RS_PEER_MAX]
+constexpr size_t kPeerErrorOff = 260;    // int32
+constexpr size_t kPeerKeysOff = 512;
+__host__ __device__ inline uint32_t* peer_flags(void* r) { return static_cast<uint32_t*>(r); }
+__host__ __device__ inline uint32_t* peer_counter(void* r) {
+  return reinterpret_cast<uint32_t*>(static_cast<char*>(r) + kPeerCounterOff);
+}
+__host__ __device__ inline int32_t* peer_error(void* r) {
+  return reinterpret_cast<int32_t*>(static_cast<char*>(r) + kPeerErrorOff);
+}
+__host__ __device__ inline uint64_t* peer_keys(void* r) {
+  return reinterpret_cast<uint64_t*>(static_cast<char*>(r) + kPeerKeysOff);
+}
+
+// first query row of rank o's slice of an nq batch (dist.shard_range)
+__host__ __device__ inline int64_t peer_slice_lo(int64_t nq, int o, int world) { return (int64_t(o) * nq) / world; }
+
+// Where query q's key row (this rank's shard list) goes: the owner's region,
+// list (epoch parity, source ex.rank), row q - slice_lo(owner).
+__device__ __forceinline__ uint64_t* peer_row(const rs_peer_exchange& ex, int64_t nq, int64_t q, uint32_t epoch) {
+  const int W = ex.world;
+  int o = int((q * W) / nq);
+  while (o + 1 < W && q >= peer_slice_lo(nq, o + 1, W)) ++o;
+  while (q < peer_slice_lo(nq, o, W)) --o;
+  const int64_t par = epoch & 1u;
+  return peer_keys(ex.region[o]) + ((par * W + ex.rank) * ex.slice_cap + (q - peer_slice_lo(nq, o, W))) * ex.k;
+}
+
+// Block epilogue of a kernel that stored key rows with peer_row: every
+// thread's stores are ordered before its block's arrival; the last block of
+// the grid raises flags[rank] = epoch in every region (release, system
+// scope) and resets the arrival counter.  All threads of every block call it.
+__device__ __forceinline__ void peer_signal(const rs_peer_exchange& ex, uint32_t epoch) {
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t* counter = peer_counter(ex.region[ex.rank]);
+    const uint32_t prev = atomicAdd(counter, 1u);
+    if (prev == gridDim.x - 1) {
+      *counter = 0;  // every block has arrived; the next exchange is stream-ordered after this one
+      __threadfence_system();
+      for (int s = 0; s < ex.world; ++s) {
+        uint32_t* f = peer_flags(ex.region[s]) + ex.rank;
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(epoch) : "memory");
+      }
+    }
+  }
+}
+
+int check_peer_exchange(const rs_peer_exchange* ex);
+// the scatter kernel: key rows [nq, ex.k] -> owners' regions, then the signal
+int launch_peer_scatter(const rs_peer_exchange& ex, const uint64_t* keys, int64_t nq, uint32_t epoch, cudaStream_t st);
+// the K2 merge of a search whose output rows go straight to the owners'
+// regions (nlists <= 64, k == ex.k), then the signal
+int launch_merge_to_peers(const uint64_t* keys, int64_t nq, int nlists, int k_in, int64_t list_stride,
+                          int64_t q_stride, const rs_peer_exchange& ex, uint32_t epoch, cudaStream_t st);
+
 // upper bound of SearchPlan::segments (plan_search never exceeds it)
 constexpr int kMaxSegments = 4096;
 

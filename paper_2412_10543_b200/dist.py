@@ -48,6 +48,8 @@ class ShardOps:
     gate: Callable             # (profiles) -> spaces (whole batch, in order)
     select: Callable           # (spaces, profiles, qlen, free) -> configs (query slice)
     merge: Callable            # (gathered_slice, nlists, k, list_stride, nq_slice, configs) -> (D, I)
+    # (queries, k, peer, epoch) -> None: search whose final merge stores the key rows to the slice owners
+    search_scatter: Callable | None = None
 
 
 def gpu_ops(index, pipeline_params, window, *, threshold=0.90, default_space=None, cost=None) -> ShardOps:
@@ -68,7 +70,10 @@ def gpu_ops(index, pipeline_params, window, *, threshold=0.90, default_space=Non
     def merge(keys_slice, nlists, k, list_stride, nq, configs):
         return merge_topk(keys_slice, nlists, k, list_stride, k, keep=configs, nq=nq)
 
-    return ShardOps(search_keys, gate, select, merge)
+    def search_scatter(q, k, peer, epoch):
+        index.search_scatter(q, k, peer, epoch)
+
+    return ShardOps(search_keys, gate, select, merge, search_scatter)
 
 
 class PeerExchange:
@@ -124,21 +129,39 @@ class PeerExchange:
     def slice(self, nq: int) -> tuple[int, int]:
         return shard_range(nq, self.rank, self.world)
 
-    def merge(self, keys: torch.Tensor, nq: int, k: int, keep: torch.Tensor | None = None, stream=None):
-        """Scatter ``keys`` [nq, k_in] (this rank's shard, global ids) and merge
-        this rank's slice -> (D [slice, k] fp32, I [slice, k] int64)."""
+    @property
+    def exchange_struct(self) -> _lib.PeerExchangeC:
+        return self._ex
+
+    def begin(self) -> int:
+        """Next epoch (one per exchanged batch)."""
+        self.epoch = (self.epoch + 1) & 0xFFFFFFFF or 2  # skip 0 (initial flags), keep parity alternating
+        return self.epoch
+
+    def scatter(self, keys: torch.Tensor, nq: int, epoch: int, stream=None) -> None:
+        """Store ``keys`` [nq, k_in] (this rank's shard, global ids) into the
+        slice owners' regions and signal ``epoch``."""
         if keys.dtype != torch.int64 or keys.shape != (nq, self.k_in) or not keys.is_contiguous():
             raise ValueError(f"keys must be a contiguous int64 [{nq}, {self.k_in}] tensor")
-        self.epoch = (self.epoch + 1) & 0xFFFFFFFF or 2  # skip 0 (initial flags), keep parity alternating
-        st = _lib.stream_ptr(stream)
-        _lib.check(self.lib.rs_peer_scatter_keys(ctypes.byref(self._ex), _lib.ptr(keys), nq, self.epoch, st),
-                   "rs_peer_scatter_keys")
+        _lib.check(self.lib.rs_peer_scatter_keys(ctypes.byref(self._ex), _lib.ptr(keys), nq, epoch,
+                                                 _lib.stream_ptr(stream)), "rs_peer_scatter_keys")
+
+    def merge_slice(self, nq: int, k: int, epoch: int, keep: torch.Tensor | None = None, stream=None):
+        """Wait for every source's rows of ``epoch`` and merge this rank's slice
+        of the nq batch -> (D [slice, k] fp32, I [slice, k] int64)."""
         q0, q1 = self.slice(nq)
-        D = torch.empty((q1 - q0, k), dtype=torch.float32, device=keys.device)
-        I = torch.empty((q1 - q0, k), dtype=torch.int64, device=keys.device)
-        _lib.check(self.lib.rs_peer_merge_topk(ctypes.byref(self._ex), nq, self.epoch, k, _lib.ptr(keep),
-                                               _lib.ptr(D), _lib.ptr(I), self.timeout_ms, st), "rs_peer_merge_topk")
+        D = torch.empty((q1 - q0, k), dtype=torch.float32, device=self.device)
+        I = torch.empty((q1 - q0, k), dtype=torch.int64, device=self.device)
+        _lib.check(self.lib.rs_peer_merge_topk(ctypes.byref(self._ex), nq, epoch, k, _lib.ptr(keep), _lib.ptr(D),
+                                               _lib.ptr(I), self.timeout_ms, _lib.stream_ptr(stream)),
+                   "rs_peer_merge_topk")
         return D, I
+
+    def merge(self, keys: torch.Tensor, nq: int, k: int, keep: torch.Tensor | None = None, stream=None):
+        """``scatter`` + ``merge_slice`` of one batch."""
+        epoch = self.begin()
+        self.scatter(keys, nq, epoch, stream)
+        return self.merge_slice(nq, k, epoch, keep, stream)
 
     def error(self, clear: bool = False) -> int:
         """1 if some merge timed out waiting for a peer (synchronous read)."""
@@ -175,15 +198,20 @@ def sharded_retrieve_select(ops: ShardOps, queries, profiles, qlen, free_bytes, 
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     nq = queries.shape[0]
-    keys = ops.search_keys(queries, k).contiguous()                     # [nq, k] local shard
     q0, q1 = shard_range(nq, rank, world)
     if exchange == "peer":
         if peer is None:
             raise ValueError('exchange="peer" needs a PeerExchange')
+        epoch = peer.begin()
+        if ops.search_scatter is not None:   # the search's final merge stores to the owners
+            ops.search_scatter(queries, k, peer, epoch)
+        else:
+            peer.scatter(ops.search_keys(queries, k).contiguous(), nq, epoch)
         spaces = ops.gate(profiles)
         configs = ops.select(spaces[q0:q1], profiles[q0:q1], qlen[q0:q1], free_bytes[q0:q1])
-        D, I = peer.merge(keys, nq, k, keep=configs)
+        D, I = peer.merge_slice(nq, k, epoch, keep=configs)
         return q0, q1, configs, D, I
+    keys = ops.search_keys(queries, k).contiguous()                     # [nq, k] local shard
     if exchange == "all_to_all":
         sizes = [shard_range(nq, r, world)[1] - shard_range(nq, r, world)[0] for r in range(world)]
         recv = torch.empty(((q1 - q0) * world, k), dtype=keys.dtype, device=keys.device)  # source-rank-major

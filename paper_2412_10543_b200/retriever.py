@@ -116,6 +116,15 @@ class IndexFlatL2:
                                                   _lib.ptr(keys), _lib.stream_ptr(stream)), "rs_index_search_keys")
         return keys
 
+    def search_scatter(self, x: torch.Tensor, k: int, peer, epoch: int, *, stream=None) -> None:
+        """``search_keys`` whose final merge stores each query's key row into
+        its slice owner's peer region and signals ``epoch`` (``dist.PeerExchange``);
+        the owners collect with ``PeerExchange.merge_slice``."""
+        q = self._dev_tensor(x)
+        _lib.check(self._lib.rs_index_search_scatter(self._h, _lib.ptr(q), q.shape[0], int(k), self.id_base,
+                                                     ctypes.byref(peer.exchange_struct), int(epoch),
+                                                     _lib.stream_ptr(stream)), "rs_index_search_scatter")
+
     def last_plan(self) -> dict:
         s, q, c, a = (ctypes.c_int32() for _ in range(4))
         _lib.check(self._lib.rs_index_last_plan(self._h, ctypes.byref(s), ctypes.byref(q), ctypes.byref(c),

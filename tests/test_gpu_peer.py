@@ -61,3 +61,32 @@ def test_world1_exchange_is_a_copy_and_timeout_is_reported(group):
     with pytest.raises(ValueError):
         px.merge(keys.to(dev), 300, 35)  # exceeds the region's slice capacity
     px.close()
+
+
+@pytest.mark.parametrize("dtype,n", [(torch.bfloat16, 20_000), (torch.bfloat16, 200), (torch.float32, 5_000),
+                                     (torch.bfloat16, 0)])
+def test_world1_search_scatter_equals_search(group, dtype, n):
+    """rs_index_search_scatter: the fused merge-to-peers (bf16, one or many
+    segments), the local-rows-then-scatter path (3xTF32 re-rank, empty index)
+    and the owner's merge give the plain search's result."""
+    from paper_2412_10543_b200 import IndexFlatL2
+    from paper_2412_10543_b200 import dist as rdist
+
+    dev = torch.device("cuda", 0)
+    g = torch.Generator().manual_seed(n)
+    c = torch.nn.functional.normalize(torch.randn(n, 256, generator=g), dim=1).to(dtype)
+    q = torch.nn.functional.normalize(torch.randn(77, 256, generator=g), dim=1).to(dtype).to(dev)
+    ix = IndexFlatL2(256, dtype=dtype, capacity=max(n, 1), id_base=1000)
+    if n:
+        ix.add(c.to(dev))
+    px = rdist.PeerExchange(77, 35, device=dev)
+    for _ in range(3):
+        epoch = px.begin()
+        ix.search_scatter(q, 35, px, epoch)
+        D, I = px.merge_slice(77, 35, epoch)
+        D0, I0 = ix.search(q, 35)
+        torch.cuda.synchronize()
+        assert torch.equal(I, I0) and torch.equal(D, D0)
+    assert px.error() == 0
+    px.close()
+    ix.close()
