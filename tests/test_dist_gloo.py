@@ -97,6 +97,32 @@ class Sliceable:
         return (self.pr[s], self.conf[s])
 
 
+class GlooPeer:
+    """The PeerExchange protocol (begin / scatter / merge_slice) over gloo on
+    CPU: the scatter's row routing is an all-to-all of the query slices, the
+    owner's merge the oracle merge.  Exercises dist.py's "peer" branch, with
+    and without a fused search_scatter op."""
+
+    def __init__(self, world, k, merge):
+        self.world, self.k, self.merge, self.epoch, self.pending = world, k, merge, 0, {}
+
+    def begin(self):
+        self.epoch += 1
+        return self.epoch
+
+    def scatter(self, keys, nq, epoch):
+        sizes = [rdist.shard_range(nq, r, self.world)[1] - rdist.shard_range(nq, r, self.world)[0]
+                 for r in range(self.world)]
+        mine = sizes[dist.get_rank()]
+        recv = torch.empty((mine * self.world, self.k), dtype=torch.int64)
+        dist.all_to_all_single(recv, keys, output_split_sizes=[mine] * self.world, input_split_sizes=sizes)
+        self.pending[epoch] = (recv.reshape(-1), mine)
+
+    def merge_slice(self, nq, k, epoch, keep=None):
+        flat, mine = self.pending.pop(epoch)
+        return self.merge(flat, self.world, k, mine * k, mine, keep)
+
+
 def worker(rank, world, port, out_q, exchange="all_to_all"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -104,10 +130,15 @@ def worker(rank, world, port, out_q, exchange="all_to_all"):
     ops = oracle_ops(rank, world, corpus)
     # gate takes the whole batch; select/merge take the rank's slice
     ops_gate = ops.gate
-    ops = rdist.ShardOps(ops.search_keys, lambda p: ops_gate((p.pr, p.conf)), ops.select, ops.merge)
+    fused = None
+    if exchange == "peer_fused":
+        def fused(q, k, peer, epoch):
+            peer.scatter(ops.search_keys(q, k), q.shape[0], epoch)
+    ops = rdist.ShardOps(ops.search_keys, lambda p: ops_gate((p.pr, p.conf)), ops.select, ops.merge, fused)
     profiles = Sliceable(prof, conf)
+    peer = GlooPeer(world, K, ops.merge) if exchange.startswith("peer") else None
     q0, q1, cfg, Dm, Im = rdist.sharded_retrieve_select(ops, torch.from_numpy(queries), profiles, qlen, free, K,
-                                                        exchange=exchange)
+                                                        exchange="peer" if peer else exchange, peer=peer)
     out_q.put((rank, q0, q1, cfg, Dm, Im))
     dist.destroy_process_group()
 
@@ -129,7 +160,7 @@ def test_shard_range_partitions_exactly():
 
 
 @pytest.mark.timeout(300)
-@pytest.mark.parametrize("exchange", ["all_to_all", "all_gather"])
+@pytest.mark.parametrize("exchange", ["all_to_all", "all_gather", "peer", "peer_fused"])
 def test_two_rank_gloo_matches_single_process(exchange):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
