@@ -29,7 +29,12 @@ def _port():
     return p
 
 
-def _inputs():
+def _inputs(nq=None):
+    out = _all_inputs()
+    return out if nq is None else (out[0], out[1][:nq], out[2][:nq], out[3][:nq], out[4][:nq])
+
+
+def _all_inputs():
     g = torch.Generator().manual_seed(9)
     corpus = torch.nn.functional.normalize(torch.randn(N, D, generator=g), dim=1).bfloat16()
     queries = torch.nn.functional.normalize(torch.randn(NQ, D, generator=g), dim=1).bfloat16()
@@ -43,7 +48,7 @@ def _inputs():
     return corpus, queries, prof, qlen, free
 
 
-def _worker(rank, world, port, exchange, q):
+def _worker(rank, world, port, exchange, q, nq):
     import torch.distributed as dist
 
     from paper_2412_10543_b200 import IndexFlatL2, batch
@@ -53,12 +58,12 @@ def _worker(rank, world, port, exchange, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)
     dev = torch.device("cuda", 0)
-    corpus, queries, prof, qlen, free = _inputs()
+    corpus, queries, prof, qlen, free = _inputs(nq)
     r0, r1 = rdist.shard_range(N, rank, world)
     ix = IndexFlatL2(D, capacity=r1 - r0, id_base=r0)
     ix.add(corpus[r0:r1].to(dev))
     params = batch.SelectParams(per_token_bytes=131072, chunk_size=1000, out_budget=10)
-    peer = rdist.PeerExchange(NQ, K, device=dev) if exchange == "peer" else None
+    peer = rdist.PeerExchange(nq, K, device=dev) if exchange == "peer" else None
     out = []
     for it in range(_iters(exchange)):  # the peer exchange alternates its two buffers
         ops = rdist.gpu_ops(ix, params, batch.GateWindow(dev))
@@ -80,28 +85,28 @@ def _iters(exchange):
 
 
 @pytest.mark.timeout(600)
-@pytest.mark.parametrize("world,exchange", [(2, "all_to_all"), (3, "all_to_all"), (2, "all_gather"), (2, "peer"),
-                                            (3, "peer")])
-def test_multirank_sharded_path_equals_single_index(world, exchange):
+@pytest.mark.parametrize("world,exchange,nq", [(2, "all_to_all", NQ), (3, "all_to_all", NQ), (2, "all_gather", NQ),
+                                               (2, "peer", NQ), (3, "peer", NQ), (3, "peer", 2)])
+def test_multirank_sharded_path_equals_single_index(world, exchange, nq):
     from paper_2412_10543_b200 import IndexFlatL2, batch
     from paper_2412_10543_b200.pipeline import RetrieveSelect
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, exchange, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, exchange, q, nq)) for r in range(world)]
     for p in procs:
         p.start()
     res = sorted([q.get(timeout=500) for _ in range(world)], key=lambda t: t[0])
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    corpus, queries, prof, qlen, free = _inputs()
+    corpus, queries, prof, qlen, free = _inputs(nq)
     dev = torch.device("cuda", 0)
     ix = IndexFlatL2(D, capacity=N)
     ix.add(corpus.to(dev))
     params = batch.SelectParams(per_token_bytes=131072, chunk_size=1000, out_budget=10)
-    assert [(r[1], r[2]) for r in res] == [(NQ * i // world, NQ * (i + 1) // world) for i in range(world)]
+    assert [(r[1], r[2]) for r in res] == [(nq * i // world, nq * (i + 1) // world) for i in range(world)]
     for it in range(_iters(exchange)):
         ref = RetrieveSelect(ix, params).run(queries.roll(it, 0).to(dev), batch.to_device(prof, dev),
                                              torch.as_tensor(qlen, device=dev), torch.as_tensor(free, device=dev))

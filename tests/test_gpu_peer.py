@@ -39,6 +39,10 @@ def test_world1_exchange_is_a_copy_and_timeout_is_reported(group):
         D, I = px.merge(keys.to(dev), nq, 35)
         np.testing.assert_array_equal(I.cpu().numpy(), ids)
         np.testing.assert_array_equal(D.cpu().numpy(), d)
+    # fewer outputs than list entries: the k smallest
+    keys, d, ids = _sorted_keys(50, 35, 5)
+    D, I = px.merge(keys.to(dev), 50, 10)
+    np.testing.assert_array_equal(I.cpu().numpy(), ids[:, :10])
     # the join: only the first num_chunks of selected queries survive
     keys, d, ids = _sorted_keys(4, 35, 7)
     cfg = np.zeros(4, dtype=_lib.CONFIG_DTYPE)
