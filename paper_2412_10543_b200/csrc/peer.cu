@@ -136,8 +136,9 @@ extern "C" int rs_peer_merge_topk(const rs_peer_exchange* ex, int64_t nq, uint32
   RS_REQUIRE(nq >= 0 && k >= 1 && k <= 128 && timeout_ms >= 0, "bad arguments");
   RS_REQUIRE(rs::ceil_div(nq, ex->world) <= ex->slice_cap, "nq %lld exceeds world x slice_cap", (long long)nq);
   const int64_t q0 = (int64_t(ex->rank) * nq) / ex->world, q1 = (int64_t(ex->rank + 1) * nq) / ex->world;
-  if (q1 == q0) return RS_OK;
-  RS_REQUIRE(D && I, "D/I are NULL");
+  // an empty slice still waits: the next exchange may reuse a parity buffer
+  // only after every rank's merge of this one has seen all sources arrive
+  RS_REQUIRE(q1 == q0 || (D && I), "D/I are NULL");
   void* own = ex->region[ex->rank];
   rs::PeerWait pw;
   pw.flags = rs::peer_flags(own);

@@ -568,7 +568,8 @@ int launch_merge_wait(const uint64_t* keys, int64_t nq, int nlists, int k_in, in
                       int k, const rs_config* keep, float* D, int64_t* I, const PeerWait& pw, cudaStream_t st) {
   RS_REQUIRE(nlists >= 1 && nlists <= 64, "nlists out of range (%d)", nlists);
   RS_REQUIRE(k_in >= 1 && k_in <= 255, "k_in out of range (%d)", k_in);
-  const int64_t blocks = std::min<int64_t>(ceil_div(nq, kMergeWarps), 65535);
+  // nq == 0: one block that only waits (keeps the exchange's epoch chain)
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(ceil_div(nq, kMergeWarps), 65535));
   PeerArgs pa{};
   pa.wait = pw;
   merge_topk64_kernel<kMergeWait><<<(unsigned)blocks, kMergeWarps * 32, 0, st>>>(keys, nq, nlists, k_in, list_stride,
