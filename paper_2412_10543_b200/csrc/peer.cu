@@ -35,18 +35,6 @@ __global__ void __launch_bounds__(256) peer_scatter_kernel(const uint64_t* __res
   peer_signal(ex, epoch);
 }
 
-struct DevScope {
-  int prev = -1;
-  explicit DevScope(int dev) {
-    cudaGetDevice(&prev);
-    if (prev != dev) cudaSetDevice(dev);
-  }
-  ~DevScope() {
-    int cur = -1;
-    cudaGetDevice(&cur);
-    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
-  }
-};
 
 }  // namespace
 
@@ -80,7 +68,7 @@ extern "C" int rs_peer_region_bytes(int32_t world, int64_t slice_cap, int32_t k,
 extern "C" int rs_peer_alloc(uint64_t bytes, int32_t device, void** region, void* ipc_handle) {
   RS_REQUIRE(bytes >= rs::kPeerKeysOff && region && ipc_handle, "bad arguments");
   static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
-  rs::DevScope g(device);
+  rs::DeviceGuard g(device);
   void* p = nullptr;
   RS_CHECK_CUDA(cudaMalloc(&p, bytes), "cudaMalloc(peer region)");
   cudaError_t e = cudaMemset(p, 0, bytes);
@@ -99,7 +87,7 @@ extern "C" int rs_peer_alloc(uint64_t bytes, int32_t device, void** region, void
 
 extern "C" int rs_peer_open(const void* ipc_handle, int32_t device, void** region) {
   RS_REQUIRE(ipc_handle && region, "bad arguments");
-  rs::DevScope g(device);
+  rs::DeviceGuard g(device);
   cudaIpcMemHandle_t h;
   memcpy(&h, ipc_handle, sizeof(h));
   void* p = nullptr;

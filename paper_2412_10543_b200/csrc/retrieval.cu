@@ -690,6 +690,8 @@ SearchPlan plan_search(int64_t nq, int64_t n, int bq, int bn, int ctas_capacity,
 }  // namespace rs
 
 // ============================ rs_index =========================================
+using rs::DeviceGuard;
+
 struct rs_index {
   int32_t dim = 0, dtype = 0, device = 0, algo = RS_ALGO_AUTO;
   int32_t walk_bias = 0;  // test hook (rs_index_set_walk_bias)
@@ -747,19 +749,6 @@ int ensure_ws(rs_index* ix, int64_t nq, size_t part_bytes) {
   }
   return RS_OK;
 }
-
-struct DeviceGuard {
-  int prev = -1;
-  explicit DeviceGuard(int dev) {
-    cudaGetDevice(&prev);
-    if (prev != dev) cudaSetDevice(dev);
-  }
-  ~DeviceGuard() {
-    int cur = -1;
-    cudaGetDevice(&cur);
-    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
-  }
-};
 
 // Concrete kernel for a search: the CTA-pair tcgen05 kernel (default; bf16,
 // or 3xTF32 for an fp32 corpus), the single-CTA tcgen05 kernel on request
