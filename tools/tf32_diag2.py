@@ -6,7 +6,6 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from tests.test_gpu_retrieval import make_data, run_search  # noqa: E402
-from oracle import retrieval_oracle as ro  # noqa: E402
 
 for (nq, n, d, k) in [(129, 257, 768, 35), (128, 256, 768, 35), (129, 256, 768, 35), (128, 257, 768, 35), (64, 257, 768, 35), (129, 257, 128, 35)]:
     q, c = make_data(nq, n, d, torch.float32, seed=9 + nq)
