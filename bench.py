@@ -527,8 +527,9 @@ def main():
     roof["peak_source"] = f"{peak_src}, " + (
         ("sustained" if sustained else "burst") + (" bf16 / 2 (tf32)" if tf32 else " bf16")
         if roof["bound"] == "tensor" else "copy")
+    # the committed capture of this exact workload (not of an overridden shape)
     prof_path = os.path.join(ROOT, "profiles", f"ncu_{args.workload}_n{world}.json")
-    if os.path.exists(prof_path):
+    if os.path.exists(prof_path) and not (args.queries or args.corpus_rows):
         try:
             pj = json.load(open(prof_path))
             roof["traffic"] = pj.get("dram_bytes_per_launch")
