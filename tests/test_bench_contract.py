@@ -1,11 +1,14 @@
-"""bench.py's JSON-line contract, checked on the CPU through the reference arm
+"""bench.py's JSON-line contract: on the CPU through the reference arm
 of the config-only workload (cfg5: the C port of best fit + fallback on a
-bounded sample), which needs no GPU."""
+bounded sample, no GPU needed), and on the GPU through our arm (cfg4 on a
+small corpus, cfg5)."""
 
 import json
 import os
 import subprocess
 import sys
+
+import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -35,3 +38,29 @@ def test_help_lists_every_workload_and_exchange():
     for w in ("cfg1", "cfg2", "cfg3", "cfg4", "cfg5"):
         assert w in r.stdout
     assert "all_to_all" in r.stdout and "peer" in r.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("workload", ["cfg4", "cfg5"])
+def test_our_arm_prints_one_contract_line_on_the_gpu(workload):
+    """The measured arm's line (small corpus override for cfg4): every key the
+    driver reads, a tensor/HBM roofline, NVML clocks, launches of our kernels."""
+    extra = ["--corpus-rows", "300000"] if workload == "cfg4" else []
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--workload", workload, "--steps", "3",
+                        "--warmup", "3", "--no-cpu-baseline", *extra], capture_output=True, text=True, timeout=800,
+                       cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "gpu_launches", "clocks"):
+        assert key in d, key
+    assert d["value"] > 0 and d["gpu_launches"] > 0 and d["n_gpus"] == 1
+    roof = d["roofline"]
+    assert roof["bound"] in ("hbm", "tensor") and roof["achieved"] > 0 and roof["peak"] > 0
+    assert abs(roof["frac"] - roof["achieved"] / roof["peak"]) < 1e-9
+    e2e = d["e2e"]
+    assert e2e["value"] > 0 and e2e["h2d_bytes_per_step"] > 0 and e2e["d2h_bytes_per_step"] > 0
+    assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
