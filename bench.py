@@ -1,6 +1,7 @@
 """Benchmark of the METIS per-query hot path: retrieval + config selection.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg4] [--impl ours|reference]
+                    [--data iso|clustered|doc_contiguous]
 
 One step = one batch of the workload's queries through the whole path:
 confidence gate + Algorithm-1 pruning, best-fit / fallback selection with the
@@ -9,11 +10,32 @@ the join (each query's chunk ids truncated to its chosen ``num_chunks``).
 For N > 1 (``torchrun``, one process per GPU, NCCL) the corpus is sharded
 across the GPUs (strong scaling: the workload is fixed), each rank's top-k
 lists reach the owners of its query slices through the library's peer-memory
-exchange (CUDA IPC over NVLink: a scatter kernel stores them into the owners'
-regions, the owner's merge kernel waits on epoch flags; ``--exchange
-all_to_all`` uses NCCL instead), and the config stage is sharded by query.
+exchange (CUDA IPC over NVLink: the search's final merge stores them into the
+owners' regions, the owner's merge kernel waits on epoch flags; ``--exchange
+all_to_all|all_gather`` uses NCCL instead), and the config stage is sharded by
+query.
 
-Prints ONE JSON line (rank 0).  Inputs are synthetic (seeded), larger than L2.
+Inputs, identical in both arms:
+* corpus and queries from ``tools/synth.py`` — a counter-hash generator that
+  is bit-identical on the GPU (torch) and on the host (``oracle/csrc/synth.c``);
+* profiles, query lengths and free KV bytes from
+  ``tests/golden/workload_<cfg>.npz`` (made by running the reference's
+  TruthDistribution + mock_estimate; the file also holds the reference's own
+  decisions, checked bit for bit before timing).
+
+The CPU side (``--impl reference``, and the ``cpu_baseline`` leg of our arm)
+runs on the host cores: retrieval of a fixed 128-query sample of the same
+queries against the FULL corpus (FAISS flat-L2 decomposition with torch's
+BLAS, all threads; ``oracle/retrieval_oracle.py``), plus the config path of
+ALL the step's queries through the AS-SHIPPED reference package
+(``baseline/_ref``: gate_profile in order, then best_fit_select ->
+fallback_config under ``multiprocessing.Pool``).  Its ``ms_per_step`` is the
+time actually measured for that step; ``value`` is queries/s of the path,
+1 / (retrieval s per query + config s per query).  Our arm checks its own
+outputs on the same 128 queries against the exact (float64) top-k in the
+same run (``parity``).
+
+Prints ONE JSON line (rank 0).  Inputs are larger than L2.
 """
 
 from __future__ import annotations
@@ -33,80 +55,71 @@ sys.path.insert(0, ROOT)
 
 METRIC = "queries/sec retrieval+config-select at 1/2/4/8 B200; % HBM/tensor roofline"
 
-# SURVEY.md §8(d) / BASELINE.json configs
-LENGTHS = {  # workload.py:53-58 (input range, output range); out_budget = top of output range
-    "single_hop_qa": ((400, 2000), (5, 10)),
-    "multihop_qa": ((1000, 5000), (5, 20)),
-    "doc_level_qa": ((4000, 10000), (20, 40)),
-    "summarization_qa": ((4000, 12000), (20, 60)),
-}
 WORKLOADS = {
     "cfg1": dict(desc="reference CPU workload: 1,000 queries, 100k x 768 fp32, k<=35, 3 methods",
-                 nq=1000, n=100_000, d=768, dtype="fp32", truth="default", lengths="single_hop_qa", chunk=1000),
+                 nq=1000, n=100_000, d=768, dtype="fp32"),
     "cfg2": dict(desc="SQuAD-shaped: 10k queries, 1M x 768 bf16, stuff/map_rerank pruned space",
-                 nq=10_000, n=1_000_000, d=768, dtype="bf16", truth="squad", lengths="single_hop_qa", chunk=1000),
+                 nq=10_000, n=1_000_000, d=768, dtype="bf16"),
     "cfg3": dict(desc="MuSiQue-shaped: 10k queries, 2M x 1024 bf16, full map_reduce interlen sweep",
-                 nq=10_000, n=2_000_000, d=1024, dtype="bf16", truth="musique", lengths="multihop_qa", chunk=1000),
+                 nq=10_000, n=2_000_000, d=1024, dtype="bf16"),
     "cfg4": dict(desc="QMSUM/FinSec-shaped long-doc: 8,192 queries, 10M x 1024 bf16 corpus sharded over the GPUs",
-                 nq=8192, n=10_000_000, d=1024, dtype="bf16", truth="default", lengths="doc_level_qa", chunk=1024),
+                 nq=8192, n=10_000_000, d=1024, dtype="bf16"),
+    # config path only (no retrieval): the scheduler burst, queries sharded over the GPUs
+    "cfg5": dict(desc="scheduler burst: 100k queries x the full 700-candidate space (best fit + fallback "
+                      "+ plan delay), free KV = 16 GiB - U[0, 16 GiB]",
+                 nq=100_000, n=0, d=0, dtype="int64", config_only=True),
 }
-# config path only (no retrieval): the scheduler burst, queries sharded over the GPUs
-WORKLOADS["cfg5"] = dict(desc="scheduler burst: 100k queries x the full 700-candidate space (best fit + fallback "
-                              "+ plan delay), free KV = 16 GiB - U[0, 16 GiB]",
-                         nq=100_000, n=0, d=0, dtype="int64", config_only=True, chunk=1000)
-K = 35  # DEFAULT_MAX_CHUNKS: the largest num_chunks any selected config can ask for
-BLOCK = 262_144  # corpus generation block (rows); block b is seeded independently
+K = 35            # DEFAULT_MAX_CHUNKS: the largest num_chunks any selected config can ask for
+SEED = 0          # corpus and query seed (tools/synth.py)
+SAMPLE_Q = 128    # CPU side: retrieval queries per step (a fixed subset of the step's queries)
+MARGIN = 16       # CPU scan keeps k + MARGIN candidates for the float64 re-rank
+CFG5_SAMPLE = 20_000  # CPU side of cfg5: queries per step
+RTOL = {"bf16": 1e-3, "fp32": 1e-5}  # north star: retrieval distance tolerance relative to the distance
 
 
-# ---------------------------------------------------------------------------------
-# synthetic workload (host side, deterministic)
-
-def make_profiles(cfg, nq, seed):
-    """Profiles per SURVEY §8(d): TruthDistribution sampling (workload.py:61-81),
-    profile_from_truth embedding (profiler.py:166-176) and ~5% low-confidence
-    corrupted profiles (the default mock noise, profiler.py:99-106, 257-309)."""
-    rng = np.random.default_rng(seed)
-    if cfg["truth"] == "musique":
-        joint = np.ones(nq, bool)
-        cx = np.ones(nq, bool)
-        pieces = rng.integers(1, 11, nq)
-        lo = np.full(nq, 30)
-        hi = np.full(nq, 200)
-    else:
-        pc_j, pc_s = (0.0, 0.0) if cfg["truth"] == "squad" else (0.6, 0.1)
-        joint = rng.random(nq) < 0.5
-        cx = rng.random(nq) < np.where(joint, pc_j, pc_s)
-        pieces = np.where(joint, rng.integers(2, 11, nq), rng.integers(1, 4, nq))
-        lo = rng.integers(60, 181, nq)
-        hi = np.minimum(200, lo + 60)
-    conf = np.full(nq, 0.99)
-    noisy = rng.random(nq) < 0.049
-    conf[noisy] = np.round(rng.uniform(0.55, 0.88, noisy.sum()), 4)
-    flip = noisy & (rng.random(nq) < 0.5)
-    joint = np.where(flip, ~joint, joint)
-    pieces = np.where(noisy & ~flip, np.clip(pieces + rng.choice([-1, 1], nq), 1, 10), pieces)
-    (qlo, qhi), (_, out_budget) = LENGTHS[cfg["lengths"]]
-    qlen = rng.integers(qlo, qhi + 1, nq).astype(np.int32)
-    # free KV bytes ~ U[0, 2 x the largest candidate of the query's mapped space] (A2 mixture)
-    per_tok, C, T, O = 131072, cfg["chunk"], 64, out_budget
-    buf = lambda t: (102 * t.astype(np.int64) * per_tok + 99) // 100  # noqa: E731
-    n_hi = np.minimum(3 * pieces, 35)
-    q = qlen.astype(np.int64)
-    b_rr = n_hi * buf(q + C + T + O)
-    b_st = buf(q + n_hi * C + T + O)
-    b_mr = n_hi * buf(q + C + T + hi) + buf(q + n_hi * hi + T + O)
-    maxb = np.where(~joint, b_rr, np.where(cx, np.maximum(b_st, b_mr), b_st))
-    free = (rng.random(nq) * 2 * maxb).astype(np.int64)
-    return dict(cx=cx, joint=joint, pieces=pieces, lo=lo, hi=hi, conf=conf, qlen=qlen, free=free,
-                out_budget=out_budget)
+def sample_index(nq: int, m: int = SAMPLE_Q) -> np.ndarray:
+    """The fixed CPU-side query subset: evenly spread, alternating noisy
+    neighbours (even ids) and random queries (odd ids)."""
+    if nq <= m:
+        return np.arange(nq)
+    i = np.arange(m)
+    return i * (nq // m) + (i % 2)
 
 
-def corpus_block_torch(b, d, seed, device):
-    import torch
+def workload_cfg(args) -> dict:
+    cfg = dict(WORKLOADS[args.workload])
+    if args.corpus_rows:
+        cfg["n"] = args.corpus_rows
+    if args.queries:
+        cfg["nq"] = args.queries
+        cfg["desc"] += f" [queries per step overridden: {args.queries}]"
+    return cfg
 
-    g = torch.Generator(device=device).manual_seed(seed * 1_000_003 + b)
-    x = torch.randn(BLOCK, d, generator=g, device=device)
-    return torch.nn.functional.normalize(x, dim=1)
+
+def config_dict(args, cfg: dict, world: int) -> dict:
+    """The workload description — IDENTICAL in both arms (same_config)."""
+    if cfg.get("config_only"):
+        return {"workload": f"{args.workload}: {cfg['desc']}", "queries_per_step": cfg["nq"],
+                "candidates_per_query": 700, "profiles": f"tests/golden/workload_{args.workload}.npz",
+                "parallelism": f"query-sharded x{world}, no collective"}
+    return {"workload": f"{args.workload}: {cfg['desc']}", "queries_per_step": cfg["nq"],
+            "corpus_rows": cfg["n"], "dim": cfg["d"], "corpus_dtype": cfg["dtype"], "k": K,
+            "data": args.data, "seed": SEED,
+            "profiles": f"tests/golden/workload_{args.workload}.npz (reference TruthDistribution + mock_estimate)",
+            "parallelism": f"corpus-sharded x{world}, query-sharded config stage",
+            "l2": "inputs larger than L2 (corpus shard >> 126 MB), no flush"}
+
+
+def load_workload(args, cfg):
+    from tools import workload as wl
+
+    w = wl.load(args.workload)
+    if cfg["nq"] != len(w["qlen"]):  # --queries override: tile the fixture (its decisions no longer apply)
+        idx = np.arange(cfg["nq"]) % len(w["qlen"])
+        w = {k: (v[idx] if isinstance(v, np.ndarray) and v.ndim and len(v) == len(w["qlen"]) else v)
+             for k, v in w.items()}
+        w["overridden"] = True
+    return w
 
 
 # ---------------------------------------------------------------------------------
@@ -123,8 +136,7 @@ def measured_peaks():
 
 class ClockSampler:
     """SM clocks and clock-event (throttle) reasons sampled through NVML every
-    few milliseconds during the timed region (short regions still get
-    samples; nvidia-smi -lms is the fallback when pynvml is unavailable)."""
+    few milliseconds during the timed region."""
 
     NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
@@ -137,7 +149,7 @@ class ClockSampler:
             nv.nvmlInit()
             self.nv = nv
             self.h = []
-            for g in self.gpus:  # skip indices this node does not have
+            for g in self.gpus:
                 try:
                     self.h.append(nv.nvmlDeviceGetHandleByIndex(g))
                 except Exception:
@@ -168,7 +180,7 @@ class ClockSampler:
             self.t = threading.Thread(target=self._poll, daemon=True)
             self.t.start()
 
-    def stop(self, gpus=None):
+    def stop(self):
         if self.nv is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"], "samples": 0}
         self.stop_ev.set()
@@ -181,110 +193,227 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------------
-# CPU baseline: the oracle port (FAISS-style fp32 BLAS search + C config path)
+# CPU side (the reference arm and our arm's cpu_baseline leg; the only places
+# bench.py touches oracle/, never inside our timed region)
 
-def cpu_sample(cfg, prof, seed, n_rows=262_144, n_q=128, threads=None):
-    """Time a bounded sample of the workload on the host cores and extrapolate
-    to the full workload.  Returns (queries/s, sample description, cores)."""
-    import torch
+class HostCorpus:
+    """The corpus on the host as float32 [n, d] (bf16-valued for a bf16
+    corpus), built by oracle/csrc/synth.c — bit-identical to the rows the GPU
+    arm generates with tools/synth.py — plus precomputed squared norms (the
+    GPU index also computes them at ``add``)."""
 
-    from oracle import c_oracle
-    from oracle import config_oracle as co
+    def __init__(self, cfg, seed, threads):
+        import torch
+
+        from oracle import synth_host
+
+        n, d = cfg["n"], cfg["d"]
+        t0 = time.perf_counter()
+        self.x = np.empty((n, d), dtype=np.float32)
+        self.norms = np.empty(n, dtype=np.float32)
+        blk = 1 << 20
+        for a in range(0, n, blk):
+            b = min(n, a + blk)
+            synth_host.corpus_rows(a, b, d, seed, cfg["dtype"] == "bf16", out=self.x[a:b], nthreads=threads)
+            t = torch.from_numpy(self.x[a:b])
+            self.norms[a:b] = (t * t).sum(1).numpy()
+        self.gen_s = time.perf_counter() - t0
+
+    def __getitem__(self, ids):
+        return self.x[ids]
+
+
+def cpu_retrieve(host: HostCorpus, q_f32: np.ndarray, k: int):
+    """Timed FAISS-style search on all host threads -> (D, I, seconds)."""
     from oracle import retrieval_oracle as ro
 
-    d, n_full, nq = cfg["d"], cfg["n"], cfg["nq"]
-    cores = threads or os.cpu_count()
+    t0 = time.perf_counter()
+    D, I = ro.search_torch_cpu(q_f32, host.x, host.norms, k)
+    return D, I, time.perf_counter() - t0
+
+
+class CpuConfigPath:
+    """The config path of a whole step on the host: the AS-SHIPPED reference
+    (``baseline/_ref``, oracle/refpath.py) — gate_profile in order, then
+    best_fit_select -> fallback_config under multiprocessing.Pool(cores).
+    Falls back to the C restatement (and says so) if the reference is not
+    installed."""
+
+    def __init__(self, w: dict, cores: int, limit: int | None = None):
+        self.cores = cores
+        self.n = len(w["qlen"]) if limit is None else min(limit, len(w["qlen"]))
+        self.w = w
+        try:
+            from oracle import refpath
+
+            rs = refpath.import_ragsched()
+            sub = {k: (v[:self.n] if isinstance(v, np.ndarray) and v.ndim and len(v) == len(w["qlen"]) else v)
+                   for k, v in w.items()}
+            self.batch = refpath.Batch(rs, sub)
+            self.batch.gate()
+            self.pool = refpath.PoolSelect(self.batch, cores)
+            self.kind = "reference"
+            self.source = "ragsched " + refpath.source_of(rs)
+        except ImportError as e:
+            self.batch, self.pool, self.kind = None, None, "port"
+            self.source = f"C restatement (oracle/csrc/oracle_select.c): {str(e)[:100]}"
+
+    def step(self):
+        """One step's config path -> (decisions int64 [n, 5], seconds)."""
+        t0 = time.perf_counter()
+        if self.batch is not None:
+            self.batch.gate()
+            out = self.pool.run(0, self.n)
+        else:
+            from oracle import c_oracle
+            from oracle import config_oracle as co
+            from tools import workload as wl
+
+            w = self.w
+            if wl.full_space(w):
+                spaces = np.tile(w["fixed_space"].astype(np.int32), (self.n, 1))
+            else:
+                spaces, _, _ = c_oracle.gate_batch(wl.profiles_int5(w)[:self.n], w["conf"][:self.n])
+            p = co.SelectParams(chunk_size=w["chunk_size"], out_budget=w["out_budget"])
+            cfg, b, st = c_oracle.select_batch(spaces, w["joint"][:self.n], w["qlen"][:self.n],
+                                               w["free"][:self.n], p, nthreads=self.cores)
+            out = np.concatenate([cfg.astype(np.int64), st[:, None].astype(np.int64), b[:, None]], 1)
+        return out, time.perf_counter() - t0
+
+    def single_thread_us(self, m: int) -> float | None:
+        """As shipped, one thread: microseconds per query (gate + select) over m queries."""
+        if self.batch is None:
+            return None
+        m = min(m, self.n)
+        t0 = time.perf_counter()
+        self.batch.gate()
+        self.batch.select_range(0, m)
+        return 1e6 * (time.perf_counter() - t0) / m if m else None
+
+    def close(self):
+        if self.pool is not None:
+            self.pool.close()
+
+
+def cpu_side(cfg, w, queries_host, cores, steps=1):
+    """Build the host corpus, then run ``steps`` CPU steps.  Returns a dict
+    with per-step timings and the last step's retrieval candidates."""
+    import torch
+
     torch.set_num_threads(cores)
-    n_rows = min(n_rows, n_full)
-    g = torch.Generator().manual_seed(seed)
-    c = torch.nn.functional.normalize(torch.randn(n_rows, d, generator=g), dim=1)
-    qv = torch.nn.functional.normalize(torch.randn(n_q, d, generator=g), dim=1)
-    if cfg["dtype"] == "bf16":
-        c, qv = c.bfloat16().float(), qv.bfloat16().float()
-    c, qv = c.numpy(), qv.numpy()
-    cn = np.einsum("ij,ij->i", c, c)
-    t0 = time.perf_counter()
-    ro.search_blas_fp32(qv, c, K, corpus_norms=cn)
-    t_ret = time.perf_counter() - t0
-    # config path for the whole batch: gate (serial) + select (all threads)
-    p = co.SelectParams(chunk_size=cfg["chunk"], out_budget=prof["out_budget"])
-    pr = np.stack([prof["cx"], prof["joint"], prof["pieces"], prof["lo"], prof["hi"]], 1).astype(np.int32)
-    t0 = time.perf_counter()
-    spaces, fb, _ = c_oracle.gate_batch(pr, prof["conf"])
-    c_oracle.select_batch(spaces, prof["joint"], prof["qlen"], prof["free"], p, nthreads=cores)
-    t_sel = time.perf_counter() - t0
-    per_query = t_ret / n_q * (n_full / n_rows) + t_sel / nq
-    desc = (f"{n_q} queries x {n_rows} rows x {d} fp32 BLAS exact search (extrapolated x{n_full / n_rows:.1f} "
-            f"to {n_full} rows) + gate/select of all {nq} queries (C port)")
-    return 1.0 / per_query, desc, cores, per_query
+    host = HostCorpus(cfg, SEED, cores)
+    idx = sample_index(cfg["nq"])
+    qs = queries_host[idx].float().numpy()
+    cp = CpuConfigPath(w, cores)
+    st_us = cp.single_thread_us(min(2000, cp.n))
+    t_ret, t_cfg, D = [], [], None
+    for _ in range(steps):
+        D, I, tr = cpu_retrieve(host, qs, K + MARGIN)
+        dec, tc = cp.step()
+        t_ret.append(tr)
+        t_cfg.append(tc)
+    cp.close()
+    return dict(host=host, idx=idx, qs=qs, cand_I=I, t_ret=t_ret, t_cfg=t_cfg, decisions=dec, cfg_kind=cp.kind,
+                cfg_source=cp.source, cfg_single_thread_us=st_us, gen_s=host.gen_s, cores=cores)
 
 
-def cfg5_inputs(n, seed):
-    """cfg5: every query gets the full space {RR, ST, MR} x [1, 35]
-    x [30, 200] (700 candidates at the default granularity); single-hop
-    lengths; free KV bytes 16 GiB - U[0, 16 GiB] (regime ii)."""
-    rng = np.random.default_rng(seed)
-    joint = rng.integers(0, 2, n)
-    return dict(cx=rng.integers(0, 2, n), joint=joint, pieces=rng.integers(1, 11, n), lo=np.full(n, 30),
-                hi=np.full(n, 200), conf=np.where(rng.random(n) < 0.05, 0.6, 0.99),
-                qlen=rng.integers(400, 2001, n).astype(np.int32),
-                free=(16 * 1024**3 - rng.integers(0, 16 * 1024**3, n)).astype(np.int64), out_budget=10)
+def cpu_value(cs, nq):
+    """queries/s of the path from measured step times: 1 / (retrieval s per
+    query over the sample + config s per query over the whole batch)."""
+    per_q = [tr / len(cs["idx"]) + tc / nq for tr, tc in zip(cs["t_ret"], cs["t_cfg"])]
+    return len(per_q) / sum(per_q)
 
 
-def cfg5_cpu_sample(prof, n_sample=20_000, threads=None):
-    """The C port of best_fit_select -> fallback_config (the reference's
-    sort-then-reverse-scan) over a bounded sample, all host threads."""
-    from oracle import c_oracle
-    from oracle import config_oracle as co
-
-    cores = threads or os.cpu_count()
-    p = co.SelectParams(chunk_size=1000, out_budget=prof["out_budget"])
-    m = min(n_sample, len(prof["qlen"]))
-    spaces = np.tile(np.array([[7, 1, 35, 30, 200]], dtype=np.int32), (m, 1))
-    t0 = time.perf_counter()
-    c_oracle.select_batch(spaces, prof["joint"][:m], prof["qlen"][:m], prof["free"][:m], p, nthreads=cores)
-    dt = time.perf_counter() - t0
-    return m / dt, f"best-fit + fallback of {m} full-space queries (C port, no delays)", cores, dt / m
+def cpu_sample_desc(cfg, cs):
+    return (f"{len(cs['idx'])} of the step's queries (fixed subset) x the full {cfg['n']}-row corpus: fp32 "
+            f"flat-L2 (torch BLAS, {cs['cores']} threads, k+{MARGIN} candidates) + the config path of all "
+            f"{cfg['nq']} queries ({'as-shipped reference, gate in order + Pool select' if cs['cfg_kind'] == 'reference' else 'C restatement'}); "
+            "no extrapolation: value = 1 / (retrieval s/query + config s/query)")
 
 
 def run_reference(args, cfg, rank):
-    """--impl reference: the CPU port of the reference path on the host cores."""
+    """--impl reference: the reference's CPU path on the host cores (see module doc)."""
     if rank != 0:
         return
+    cores = os.cpu_count()
+    base = {"metric": METRIC, "unit": "queries/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "data": "synthetic",
+            "impl": "reference", "config": config_dict(args, cfg, args.gpus)}
+    if args.data != "iso":
+        print(json.dumps(dict(base, unavailable="the CPU arm generates only the iso corpus family "
+                                                "(tools/synth.py; the mixture families are GPU-generated)")))
+        return
+    w = load_workload(args, cfg)
     if cfg.get("config_only"):
-        prof = cfg5_inputs(cfg["nq"], args.seed)
-        per_q = [cfg5_cpu_sample(prof)[3] for _ in range(args.warmup + args.steps)][args.warmup:]
-        value = len(per_q) / sum(per_q)
-        _, desc, cores, _ = cfg5_cpu_sample(prof, n_sample=1)
-        line = {
-            "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1e3 * cfg["nq"] / value, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": f"{args.workload}: {cfg['desc']}"},
-            "cpu_baseline": {"value": value, "unit": "queries/s", "cores": cores, "kind": "port",
-                             "sample": "best-fit + fallback of 20000 full-space queries per step (C port)"},
-            "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        }
+        cp = CpuConfigPath(w, cores, limit=CFG5_SAMPLE)
+        st_us = cp.single_thread_us(1000)
+        times = [cp.step()[1] for _ in range(args.warmup + args.steps)][args.warmup:]
+        cp.close()
+        value = cp.n * len(times) / sum(times)
+        line = dict(base, value=value, ms_per_step=1e3 * statistics.mean(times), dtype="int64",
+                    cpu_baseline={"value": value, "unit": "queries/s", "cores": cores, "kind": cp.kind,
+                                  "sample": f"best-fit + fallback of the first {cp.n} fixture queries per step "
+                                            f"({cp.source}, multiprocessing.Pool({cores}))",
+                                  "single_thread_us_per_query": st_us},
+                    e2e={"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0})
         print(json.dumps(line), flush=True)
         return
-    prof = make_profiles(cfg, cfg["nq"], args.seed)
-    times = []
-    desc = cores = None
-    for i in range(args.warmup + args.steps):
-        v, desc, cores, per_q = cpu_sample(cfg, prof, args.seed + i)
-        if i >= args.warmup:
-            times.append(per_q * cfg["nq"])
-    total = sum(times)
-    value = cfg["nq"] * len(times) / total
-    line = {
-        "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
-        "config": {"workload": f"{args.workload}: {cfg['desc']}", "k": K},
-        "cpu_baseline": {"value": value, "unit": "queries/s", "cores": cores, "kind": "port", "sample": desc},
-        "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
+    import torch
+
+    from tools import synth
+
+    tdtype = torch.bfloat16 if cfg["dtype"] == "bf16" else torch.float32
+    queries = synth.make_queries(cfg["nq"], cfg["n"], cfg["d"], SEED, tdtype, args.data)
+    cs = cpu_side(cfg, w, queries, cores, steps=args.warmup + args.steps)
+    cs["t_ret"], cs["t_cfg"] = cs["t_ret"][args.warmup:], cs["t_cfg"][args.warmup:]
+    value = cpu_value(cs, cfg["nq"])
+    ms = 1e3 * statistics.mean(a + b for a, b in zip(cs["t_ret"], cs["t_cfg"]))
+    line = dict(base, value=value, ms_per_step=ms, dtype="f32",
+                cpu_baseline={"value": value, "unit": "queries/s", "cores": cores, "kind": "port",
+                              "sample": cpu_sample_desc(cfg, cs), "config_path": cs["cfg_source"],
+                              "retrieval_ms_per_step": 1e3 * statistics.mean(cs["t_ret"]),
+                              "config_ms_per_step": 1e3 * statistics.mean(cs["t_cfg"]),
+                              "config_single_thread_us_per_query": cs["cfg_single_thread_us"],
+                              "corpus_build_s": cs["gen_s"]},
+                e2e={"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0})
     print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------------
+# parity of our arm on the same inputs (checked before the timed region)
+
+def config_parity(w, configs_np, q0, q1):
+    """Our decisions for queries [q0, q1) vs the reference's (fixture)."""
+    if w.get("overridden"):
+        return None
+    e = w["exp_select"][q0:q1]
+    bad = ((configs_np["status"] != e[:, 3]) | (configs_np["method"] != e[:, 0]) |
+           (configs_np["num_chunks"] != e[:, 1]) | (configs_np["interlen"] != e[:, 2]) |
+           (configs_np["kv_bytes"] != e[:, 4]))
+    return {"checked": int(q1 - q0), "mismatches": int(bad.sum()), "against": "reference decisions (fixture)"}
+
+
+def retrieval_parity(cfg, cs, D_full, I_full):
+    from oracle import retrieval_oracle as ro
+
+    idx = cs["idx"]
+    qs = cs["qs"]
+    D_ref, I_ref = ro.exact_topk(qs, cs["host"], cs["cand_I"], K)
+    res = ro.check_topk_rel(D_full[idx], I_full[idx], qs, cs["host"], D_ref, I_ref, RTOL[cfg["dtype"]])
+    return {"sample_queries": len(idx), "exact_id_rows": res["exact_rows"], "violations": len(res["violations"]),
+            "first_violations": [list(map(str, v)) for v in res["violations"][:3]],
+            "max_rel_err": res["max_rel_err"], "max_abs_err": res["max_abs_err"], "rtol": RTOL[cfg["dtype"]],
+            "against": "float64 exact top-k of the CPU scan's candidates (same corpus, generated on the host)"}
+
+
+def join_ok(configs_np, D_join, I_join, D_full, I_full):
+    """The join: each query's ids are the first num_chunks of
+    its full top-k (status best-fit/fallback), nothing for MustQueue."""
+    nc = np.where(configs_np["status"] <= 1, configs_np["num_chunks"], 0).astype(np.int64)
+    cols = np.arange(I_full.shape[1])[None, :]
+    keep = cols < nc[:, None]
+    return bool(np.array_equal(np.where(keep, I_full, -1), I_join) and
+                np.array_equal(np.where(keep, D_full, np.inf), D_join))
 
 
 # ---------------------------------------------------------------------------------
@@ -297,7 +426,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg4", choices=sorted(WORKLOADS))
-    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--data", default="iso", choices=["iso", "clustered", "doc_contiguous"],
+                    help="corpus family (tools/synth.py); iso = SURVEY §8(d)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--exchange", default="peer", choices=["peer", "all_to_all", "all_gather"],
@@ -307,12 +437,7 @@ def main():
     ap.add_argument("--queries", type=int, default=None,
                     help="override the queries per step (e.g. 128: the HBM-bound small-batch regime)")
     args = ap.parse_args()
-    cfg = dict(WORKLOADS[args.workload])
-    if args.corpus_rows:
-        cfg["n"] = args.corpus_rows
-    if args.queries:
-        cfg["nq"] = args.queries
-        cfg["desc"] += f" [queries per step overridden: {args.queries}]"
+    cfg = workload_cfg(args)
     rank = int(os.environ.get("RANK", "0"))
     if args.impl == "reference":
         return run_reference(args, cfg, rank)
@@ -324,6 +449,7 @@ def main():
     from paper_2412_10543_b200 import dist as rdist
     from paper_2412_10543_b200.pipeline import RetrieveSelect
     from paper_2412_10543_b200.retriever import IndexFlatL2
+    from tools import synth
 
     # RS_BENCH_BACKEND / RS_BENCH_DEVICE: plumbing checks only (e.g. two ranks
     # sharing one GPU over gloo); the measured configuration is NCCL, one GPU per rank
@@ -331,80 +457,74 @@ def main():
     local = int(os.environ.get("RS_BENCH_DEVICE", os.environ.get("LOCAL_RANK", rank)))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    w = load_workload(args, cfg)
     if cfg.get("config_only"):
-        return run_cfg5(args, cfg, rank, world, dev)
+        return run_cfg5(args, cfg, w, rank, world, dev)
     nq, n, d = cfg["nq"], cfg["n"], cfg["d"]
     tdtype = torch.bfloat16 if cfg["dtype"] == "bf16" else torch.float32
     esize = 2 if cfg["dtype"] == "bf16" else 4
 
-    # ---- corpus shard (global rows [r0, r1), ids r0..) ----
+    # ---- corpus shard (global rows [r0, r1), ids r0..), generated on the device ----
     r0, r1 = rdist.shard_range(n, rank, world)
     index = IndexFlatL2(d, dtype=tdtype, capacity=r1 - r0, device=dev, id_base=r0)
-    qloc0, qloc1 = rdist.shard_range(nq, rank, world)
-    nql = qloc1 - qloc0
-    grng = torch.Generator(device=dev).manual_seed(args.seed + 17 * rank + 1)
-    src = torch.randint(r0, r1, (nql,), generator=grng, device=dev)  # neighbour sources (local rows)
-    q_local = torch.nn.functional.normalize(torch.randn(nql, d, generator=grng, device=dev), dim=1)
-    is_nb = torch.arange(nql, device=dev) % 2 == 0
-    for b in range(r0 // BLOCK, (r1 - 1) // BLOCK + 1):
-        blk = corpus_block_torch(b, d, args.seed, dev)
-        lo, hi = max(r0, b * BLOCK), min(r1, (b + 1) * BLOCK)
-        rows = blk[lo - b * BLOCK: hi - b * BLOCK]
-        index.add(rows.to(tdtype))
-        m = is_nb & (src >= lo) & (src < hi)
-        if m.any():  # noisy neighbours normalize(c_j + 0.5 z)
-            q_local[m] = torch.nn.functional.normalize(
-                blk[src[m] - b * BLOCK] + 0.5 * q_local[m] / d ** 0.5, dim=1)
-        del blk, rows
-    torch.cuda.synchronize()
-    if world > 1:
-        # slices may differ by one row: gather equal padded blocks, then trim
-        sizes = [rdist.shard_range(nq, r, world)[1] - rdist.shard_range(nq, r, world)[0] for r in range(world)]
-        pad = torch.zeros(max(sizes), d, device=dev)
-        pad[:nql] = q_local
-        parts = [torch.empty(max(sizes), d, device=dev) for _ in range(world)]
-        dist.all_gather(parts, pad)
-        queries = torch.cat([p_[:sz] for p_, sz in zip(parts, sizes)]).to(tdtype)
-    else:
-        queries = q_local.to(tdtype)
+    for a in range(r0, r1, 1 << 20):
+        index.add(synth.corpus_rows(a, min(r1, a + (1 << 20)), d, SEED, tdtype, dev, args.data))
+    queries_host = synth.make_queries(nq, n, d, SEED, tdtype, args.data)  # identical on every rank
+    queries = queries_host.to(dev)
 
-    prof = make_profiles(cfg, nq, args.seed + 1)
-    prof_np = batch.profiles_from_arrays(prof["cx"], prof["joint"], prof["pieces"], prof["lo"], prof["hi"],
-                                         prof["conf"])
+    prof_np = batch.profiles_from_arrays(w["cx"], w["joint"], w["pieces"], w["s_lo"], w["s_hi"], w["conf"])
     profiles = batch.to_device(prof_np, dev)
-    qlen = torch.as_tensor(prof["qlen"], device=dev)
-    free = torch.as_tensor(prof["free"], device=dev)
-    params = batch.SelectParams(per_token_bytes=131072, chunk_size=cfg["chunk"], out_budget=prof["out_budget"])
+    qlen = torch.as_tensor(w["qlen"], device=dev)
+    free = torch.as_tensor(w["free"], device=dev)
+    params = batch.SelectParams(per_token_bytes=131072, chunk_size=w["chunk_size"], out_budget=w["out_budget"])
     cost = batch.CostModel()
     index.reserve(nq, K)
+    torch.cuda.synchronize()
 
+    parity = {}
     exchange_used = None
     if world == 1:
+        # parity batch: a fresh pipeline (fresh gate window, as the fixture's reference run)
+        chk = RetrieveSelect(index, params, k=K, cost=cost).run(queries, profiles, qlen, free)
+        D_full, I_full = index.search(queries, K)
+        cfg_np = chk.configs_np()
+        parity["config_decisions"] = config_parity(w, cfg_np, 0, nq)
+        parity["join_prefix"] = join_ok(cfg_np, chk.distances.cpu().numpy(), chk.chunk_ids.cpu().numpy(),
+                                        D_full.cpu().numpy(), I_full.cpu().numpy())
+        D_full, I_full = D_full.cpu().numpy(), I_full.cpu().numpy()
         pipe = RetrieveSelect(index, params, k=K, cost=cost)
 
         def step():
             return pipe.run(queries, profiles, qlen, free)
     else:
-        window = batch.GateWindow(dev)
-        ops = rdist.gpu_ops(index, params, window, cost=cost)
-        exchange, peer = args.exchange, None
+        ops = rdist.gpu_ops(index, params, batch.GateWindow(dev), cost=cost)
+        exchange, peer, exchange_note = args.exchange, None, None
         if exchange == "peer":
             try:
-                peer = rdist.PeerExchange(nq, K, device=dev)
+                peer = rdist.PeerExchange(nq, K, device=dev, timeout_ms=60_000)
             except RuntimeError as e:  # e.g. no CUDA IPC between the ranks' containers: NCCL instead, reported
-                exchange_note = f"all_to_all (peer exchange unavailable: {str(e)[:120]})"
-                exchange = "all_to_all"
+                exchange_note = f"all_gather (peer exchange unavailable: {str(e)[:120]})"
+                exchange = "all_gather"
+        # the first batch through NCCL (fresh window) and through the chosen
+        # exchange must agree, and both must match the reference decisions
+        a = rdist.sharded_retrieve_select(rdist.gpu_ops(index, params, batch.GateWindow(dev), cost=cost), queries,
+                                          profiles, qlen, free, K, exchange="all_gather")
+        q0, q1 = a[0], a[1]
+        cp_ = config_parity(w, batch.from_device(a[2], _lib.CONFIG_DTYPE), q0, q1)
+        bad = torch.tensor([float(cp_["mismatches"]) if cp_ else 0.0], device=dev)
+        dist.all_reduce(bad, op=dist.ReduceOp.SUM)
+        parity["config_decisions"] = {"checked": nq, "mismatches": int(bad.item()),
+                                      "against": "reference decisions (fixture)"} if cp_ else None
         if peer is not None:
-            # the first batch through both exchanges must agree before the peer path is timed
-            a = rdist.sharded_retrieve_select(ops, queries, profiles, qlen, free, K, exchange="all_to_all")
-            b = rdist.sharded_retrieve_select(ops, queries, profiles, qlen, free, K, exchange="peer", peer=peer)
-            bad = torch.tensor([float(not (torch.equal(a[3], b[3]) and torch.equal(a[4], b[4])) or peer.error())],
-                               device=dev)
-            dist.all_reduce(bad, op=dist.ReduceOp.MAX)
-            if bad.item():
-                exchange_note = "all_to_all (peer exchange disagreed with NCCL on the check batch: disabled)"
-                exchange, peer = "all_to_all", None
-        exchange_used = exchange_note if exchange != args.exchange else exchange
+            b = rdist.sharded_retrieve_select(rdist.gpu_ops(index, params, batch.GateWindow(dev), cost=cost),
+                                              queries, profiles, qlen, free, K, exchange="peer", peer=peer)
+            diff = torch.tensor([float(not (torch.equal(a[3], b[3]) and torch.equal(a[4], b[4])) or peer.error())],
+                                device=dev)
+            dist.all_reduce(diff, op=dist.ReduceOp.MAX)
+            if diff.item():
+                exchange_note = "all_gather (peer exchange disagreed with NCCL on the check batch: disabled)"
+                exchange, peer = "all_gather", None
+        exchange_used = exchange_note or exchange
 
         def step():
             return rdist.sharded_retrieve_select(ops, queries, profiles, qlen, free, K, exchange=exchange, peer=peer)
@@ -413,16 +533,10 @@ def main():
         if world > 1:
             dist.barrier()
 
-    def max_over_ranks(x):
+    def reduce(x, op):
         t = torch.tensor([x], dtype=torch.float64, device=dev)
         if world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
-    def sum_over_ranks(x):
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+            dist.all_reduce(t, op=op)
         return float(t.item())
 
     # ---- device-resident timing ----
@@ -452,46 +566,24 @@ def main():
     ms = ev0.elapsed_time(ev1)
     kt = index.kernel_times_ms()
     index.enable_timing(False)
-    clk = clocks.stop(gpus=list(range(world))) if rank == 0 else None
-    ms_max = max_over_ranks(ms)
-    launches_total = int(sum_over_ranks(launches))
-    kernel_ms = max_over_ranks(statistics.mean(kt) if kt else float("nan"))
+    clk = clocks.stop() if rank == 0 else None
+    ms_max = reduce(ms, dist.ReduceOp.MAX if world > 1 else None)
+    launches_total = int(reduce(launches, dist.ReduceOp.SUM if world > 1 else None))
+    kernel_ms = reduce(statistics.mean(kt) if kt else float("nan"), dist.ReduceOp.MAX if world > 1 else None)
     value = nq * args.steps / (ms_max / 1e3)
+    if world > 1 and exchange == "peer":
+        # a flag-wait timeout inside the timed region would merge stale rows: fail the line
+        perr = reduce(float(peer.error()), dist.ReduceOp.MAX)
+        parity["peer_exchange_timeouts"] = int(perr)
 
     # ---- end-to-end through the public API with pinned host buffers ----
     e2e = None
     if not args.no_e2e:
-        q_host = queries.cpu().pin_memory()
-        p_host = profiles.cpu().pin_memory()
-        ql_host, fr_host = qlen.cpu().pin_memory(), free.cpu().pin_memory()
-        outbufs = {}
-
-        def e2e_step():
-            if world == 1:
-                return pipe.run_host(q_host, p_host, ql_host, fr_host, pinned_out=outbufs)
-            qd, pd = q_host.to(dev, non_blocking=True), p_host.to(dev, non_blocking=True)
-            qld, frd = ql_host.to(dev, non_blocking=True), fr_host.to(dev, non_blocking=True)
-            q0, q1, cfgs, D, I = rdist.sharded_retrieve_select(ops, qd, pd, qld, frd, K, exchange=exchange,
-                                                               peer=peer)
-            out = (cfgs.cpu(), I.cpu())
-            torch.cuda.synchronize()
-            return out
-
-        for _ in range(max(1, args.warmup // 2)):
-            e2e_step()
-        barrier()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            e2e_step()
-        torch.cuda.synchronize()
-        barrier()
-        e2e_s = max_over_ranks(time.perf_counter() - t0)
-        h2d = q_host.numel() * q_host.element_size() + p_host.numel() + 4 * nq + 8 * nq
-        nq_slice = nq if world == 1 else (qloc1 - qloc0)
-        d2h = nq_slice * 16 + nq_slice * K * 8
-        e2e = {"value": nq * args.steps / e2e_s, "unit": "queries/s", "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h)}
+        e2e = run_e2e(args, world, rank, dev, nq, queries, profiles, qlen, free,
+                      pipe if world == 1 else None,
+                      (lambda qd, pd, qld, frd: rdist.sharded_retrieve_select(
+                          ops, qd, pd, qld, frd, K, exchange=exchange, peer=peer)) if world > 1 else None,
+                      barrier, reduce, dist)
 
     # ---- roofline of the dominant kernel (fused score + top-k) ----
     hbm, tf_burst, tf_sust, peak_src = measured_peaks()
@@ -500,12 +592,9 @@ def main():
     bytes_alg = n_shard * d * esize + 4 * n_shard + nq * d * esize + nq * K * 12
     algo = index.last_plan()["algo"]
     tf32 = cfg["dtype"] != "bf16" and algo == "tcgen05"
-    # the fp32 corpus runs as 3xTF32 on the tensor cores: 3 tf32 MMAs per
-    # product at half the bf16 rate (peak derived from the measured bf16 one)
     tc_flops = 3.0 * flops if tf32 else flops
-    # a timed region longer than ~100 ms runs into the power cap (measured:
-    # cfg3's 330 ms region median 1545 MHz): the sustained peak; shorter ones
-    # run at burst clocks (MEASURED_PEAKS: best-of-10 burst vs a 4 s run)
+    # a timed region longer than ~100 ms runs into the power cap: the sustained
+    # peak; shorter ones run at burst clocks (MEASURED_PEAKS: best-of-10 burst vs a 4 s run)
     sustained = ms_max > 100.0
     tf_ref = tf_sust if sustained else tf_burst
     tc_peak = tf_ref / 2.0 if tf32 else tf_ref
@@ -520,6 +609,9 @@ def main():
         roof = {"bound": "hbm", "achieved": bytes_alg / (kernel_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s"}
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["traffic"] = None
+    roof["algorithmic"] = {"flops_per_launch": flops, "bytes_per_launch": bytes_alg,
+                           "per_unit": f"2*N*d = {2 * n_shard * d:.4g} flop per query; corpus N*d*{esize}+4N bytes "
+                                       "per launch + d*e + k*12 bytes per query"}
     roof["kernel"] = {"tcgen05": "score_topk_pair_kernel", "tcgen05_1sm": "score_topk_tc_kernel"}.get(
         algo, "score_topk_simt_kernel")
     roof["kernel_ms"] = kernel_ms
@@ -527,42 +619,118 @@ def main():
     roof["peak_source"] = f"{peak_src}, " + (
         ("sustained" if sustained else "burst") + (" bf16 / 2 (tf32)" if tf32 else " bf16")
         if roof["bound"] == "tensor" else "copy")
-    # the committed capture of this exact workload (not of an overridden shape)
     prof_path = os.path.join(ROOT, "profiles", f"ncu_{args.workload}_n{world}.json")
-    if os.path.exists(prof_path) and not (args.queries or args.corpus_rows):
+    if os.path.exists(prof_path) and not (args.queries or args.corpus_rows) and args.data == "iso":
         try:
             pj = json.load(open(prof_path))
             roof["traffic"] = pj.get("dram_bytes_per_launch")
-            if pj.get("tensor_pipe_pct") is not None:  # same kernel's tensor pipe activity in that capture
+            if pj.get("tensor_pipe_pct") is not None:
                 roof["tensor_pipe_active_ncu"] = round(pj["tensor_pipe_pct"] / 100.0, 4)
         except Exception:
             pass
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, desc, cores, _ = cpu_sample(cfg, prof, args.seed)
-        cpu = {"value": v, "unit": "queries/s", "cores": cores, "kind": "port", "sample": desc}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.data == "iso":
+        cores = os.cpu_count()
+        cs = cpu_side(cfg, w, queries_host, cores)
+        parity["retrieval"] = retrieval_parity(cfg, cs, D_full, I_full)
+        cpu = {"value": cpu_value(cs, nq), "unit": "queries/s", "cores": cores, "kind": "port",
+               "sample": cpu_sample_desc(cfg, cs), "config_path": cs["cfg_source"],
+               "ms_measured": 1e3 * (cs["t_ret"][0] + cs["t_cfg"][0]),
+               "config_single_thread_us_per_query": cs["cfg_single_thread_us"]}
+    elif rank == 0 and world == 1 and args.data != "iso":
+        parity["retrieval"] = gpu_side_parity(cfg, index, queries, D_full, I_full, args.data, dev)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic",
-            "config": {"workload": f"{args.workload}: {cfg['desc']}", "queries_per_step": nq, "corpus_rows": n,
-                       "dim": d, "k": K, "corpus_shard_rows": n_shard,
-                       "parallelism": f"corpus-sharded x{world}, query-sharded config stage",
-                       "exchange": exchange_used,
-                       "l2": "inputs larger than L2 (corpus shard >> 126 MB), no flush"},
+            "config": config_dict(args, cfg, world), "exchange": exchange_used,
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_total,
-            "clocks": clk, "plan": index.last_plan(),
+            "clocks": clk, "parity": parity, "plan": index.last_plan(),
         }
         print(json.dumps(line), flush=True)
     index.close()
     if world > 1:
+        if exchange == "peer":
+            peer.close()
         dist.destroy_process_group()
 
 
-def run_cfg5(args, cfg, rank, world, dev):
+def gpu_side_parity(cfg, index, queries, D_full, I_full, data, dev):
+    """Parity for the GPU-generated data families: the CPU scan runs over the
+    rows read back from the index's own corpus (same bytes)."""
+    import torch
+
+    from oracle import retrieval_oracle as ro
+
+    from tools import synth
+
+    idx = sample_index(cfg["nq"])
+    qs = queries[torch.as_tensor(idx, device=dev)].float().cpu().numpy()
+    tdtype = torch.bfloat16 if cfg["dtype"] == "bf16" else torch.float32
+    n, d = cfg["n"], cfg["d"]
+    host_rows = np.empty((n, d), dtype=np.float32)
+    for a in range(0, n, 1 << 20):
+        b = min(n, a + (1 << 20))
+        host_rows[a:b] = synth.corpus_rows(a, b, d, SEED, tdtype, dev, data).float().cpu().numpy()
+    norms = (torch.from_numpy(host_rows) ** 2).sum(1).numpy()
+    _, cand = ro.search_torch_cpu(qs, host_rows, norms, K + MARGIN)
+    D_ref, I_ref = ro.exact_topk(qs, host_rows, cand, K)
+    res = ro.check_topk_rel(D_full[idx], I_full[idx], qs, host_rows, D_ref, I_ref, RTOL[cfg["dtype"]])
+    return {"sample_queries": len(idx), "exact_id_rows": res["exact_rows"], "violations": len(res["violations"]),
+            "max_rel_err": res["max_rel_err"], "rtol": RTOL[cfg["dtype"]],
+            "against": f"float64 exact top-k ({data} corpus copied from the generator on the device)"}
+
+
+def run_e2e(args, world, rank, dev, nq, queries, profiles, qlen, free, pipe, sharded, barrier, reduce, dist):
+    """The same metric through the public API with pinned HOST inputs and
+    outputs: every step copies its inputs H2D and its configs + joined chunk
+    ids D2H inside the timed region."""
+    import torch
+
+    q_host = queries.cpu().pin_memory()
+    p_host = profiles.cpu().pin_memory()
+    ql_host, fr_host = qlen.cpu().pin_memory(), free.cpu().pin_memory()
+    if world == 1:
+        stream = pipe.host_stream(q_host, p_host, ql_host, fr_host)
+
+        def run(steps):
+            return stream.run(steps)
+    else:
+        def run(steps):
+            for _ in range(steps):
+                qd, pd = q_host.to(dev, non_blocking=True), p_host.to(dev, non_blocking=True)
+                qld, frd = ql_host.to(dev, non_blocking=True), fr_host.to(dev, non_blocking=True)
+                _, _, cfgs, _, I = sharded(qd, pd, qld, frd)
+                cfgs.cpu(), I.cpu()
+            torch.cuda.synchronize()
+
+    run(max(1, args.warmup // 2))
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    run(args.steps)
+    torch.cuda.synchronize()
+    barrier()
+    e2e_s = reduce(time.perf_counter() - t0, dist.ReduceOp.MAX if world > 1 else None)
+    h2d = q_host.numel() * q_host.element_size() + p_host.numel() + 4 * nq + 8 * nq
+    nq_slice = nq if world == 1 else (dist_slice(nq, rank, world))
+    d2h = nq_slice * 16 + nq_slice * K * 8
+    return {"value": nq * args.steps / e2e_s, "unit": "queries/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "overlap": "H2D of step i+1 and D2H of step i-1 on copy streams"
+            if world == 1 else "none"}
+
+
+def dist_slice(nq, rank, world):
+    from paper_2412_10543_b200 import dist as rdist
+
+    a, b = rdist.shard_range(nq, rank, world)
+    return b - a
+
+
+def run_cfg5(args, cfg, w, rank, world, dev):
     """cfg5: the config path alone (select_kernel: best fit + fallback + plan
     delay over the 700-candidate grid), queries sharded over the ranks with no
     collective on the data path."""
@@ -571,22 +739,23 @@ def run_cfg5(args, cfg, rank, world, dev):
 
     from paper_2412_10543_b200 import _lib, batch
     from paper_2412_10543_b200 import dist as rdist
+    from paper_2412_10543_b200.pipeline import SelectHostStream
 
     n = cfg["nq"]
     q0, q1 = rdist.shard_range(n, rank, world)
-    prof = cfg5_inputs(n, args.seed)
+    m = q1 - q0
     sl = slice(q0, q1)
-    sp_np = batch.spaces_from_arrays(np.full(q1 - q0, 7), np.full(q1 - q0, 1), np.full(q1 - q0, 35),
-                                     np.full(q1 - q0, 30), np.full(q1 - q0, 200))
-    pr_np = batch.profiles_from_arrays(prof["cx"][sl], prof["joint"][sl], prof["pieces"][sl], prof["lo"][sl],
-                                       prof["hi"][sl], prof["conf"][sl])
+    fs = [int(x) for x in w["fixed_space"]]
+    sp_np = batch.spaces_from_arrays(*(np.full(m, v) for v in fs))
+    pr_np = batch.profiles_from_arrays(w["cx"][sl], w["joint"][sl], w["pieces"][sl], w["s_lo"][sl], w["s_hi"][sl],
+                                       w["conf"][sl])
     spaces, profiles = batch.to_device(sp_np, dev), batch.to_device(pr_np, dev)
-    qlen = torch.as_tensor(prof["qlen"][sl], device=dev)
-    free = torch.as_tensor(prof["free"][sl], device=dev)
-    params = batch.SelectParams(per_token_bytes=131072, chunk_size=cfg["chunk"], out_budget=prof["out_budget"])
+    qlen = torch.as_tensor(w["qlen"][sl], device=dev)
+    free = torch.as_tensor(w["free"][sl], device=dev)
+    params = batch.SelectParams(per_token_bytes=131072, chunk_size=w["chunk_size"], out_budget=w["out_budget"])
     cost = batch.CostModel()
-    out = torch.empty((q1 - q0, 16), dtype=torch.uint8, device=dev)
-    delay = torch.empty(q1 - q0, dtype=torch.float64, device=dev)
+    out = torch.empty((m, 16), dtype=torch.uint8, device=dev)
+    delay = torch.empty(m, dtype=torch.float64, device=dev)
 
     def step():
         batch.select(spaces, profiles, qlen, free, params, cost=cost, out=out, delay=delay)
@@ -601,6 +770,11 @@ def run_cfg5(args, cfg, rank, world, dev):
             dist.all_reduce(t, op=op)
         return float(t.item())
 
+    step()
+    cp_ = config_parity(w, batch.from_device(out, _lib.CONFIG_DTYPE), q0, q1)
+    mism = reduce(float(cp_["mismatches"]) if cp_ else 0.0, dist.ReduceOp.SUM if world > 1 else None)
+    parity = {"config_decisions": {"checked": n, "mismatches": int(mism),
+                                   "against": "reference decisions (fixture)"} if cp_ else None}
     for _ in range(args.warmup):
         step()
     # a step is ~0.2 ms: time `reps` batches per reported step so the region is well above launch noise
@@ -622,7 +796,7 @@ def run_cfg5(args, cfg, rank, world, dev):
     torch.cuda.synchronize()
     barrier()
     launches = reduce(_lib.launch_count() - l0, dist.ReduceOp.SUM if world > 1 else None)
-    clk = clocks.stop(gpus=list(range(world))) if rank == 0 else None
+    clk = clocks.stop() if rank == 0 else None
     ms_max = reduce(ev0.elapsed_time(ev1), dist.ReduceOp.MAX if world > 1 else None)
     ms_step = ms_max / (args.steps * reps)
     value = n / (ms_step / 1e3)
@@ -630,31 +804,22 @@ def run_cfg5(args, cfg, rank, world, dev):
     e2e = None
     if not args.no_e2e:
         hs = [t.cpu().pin_memory() for t in (spaces, profiles, qlen, free)]
-        out_h = torch.empty(out.shape, dtype=out.dtype).pin_memory()
-        del_h = torch.empty(delay.shape, dtype=delay.dtype).pin_memory()
-
-        def e2e_step():
-            sd, pd, qd, fd = (h.to(dev, non_blocking=True) for h in hs)
-            batch.select(sd, pd, qd, fd, params, cost=cost, out=out, delay=delay)
-            out_h.copy_(out, non_blocking=True)
-            del_h.copy_(delay, non_blocking=True)
-            torch.cuda.synchronize()
-
-        for _ in range(3):
-            e2e_step()
+        st = SelectHostStream(hs, params, cost=cost, device=dev)
+        st.run(3)
         barrier()
+        torch.cuda.synchronize()
         t0 = time.perf_counter()
-        for _ in range(args.steps * reps):
-            e2e_step()
+        st.run(args.steps * reps)
         barrier()
         e2e_s = reduce(time.perf_counter() - t0, dist.ReduceOp.MAX if world > 1 else None) / (args.steps * reps)
         e2e = {"value": n / e2e_s, "unit": "queries/s",
                "h2d_bytes_per_step": int(sum(h.numel() * h.element_size() for h in hs)) * world,
-               "d2h_bytes_per_step": int(out_h.numel() + del_h.numel() * 8) * world}
+               "d2h_bytes_per_step": int(m * 16 + m * 8) * world,
+               "overlap": "H2D of batch i+1 and D2H of batch i-1 on copy streams"}
 
     hbm, _, _, peak_src = measured_peaks()
     per_q_bytes = 16 + 16 + 4 + 8 + 16 + 8  # space, profile, qlen, free in; config, delay out
-    achieved = (q1 - q0) * per_q_bytes / (ms_step * 1e-3) / 1e9
+    achieved = m * per_q_bytes / (ms_step * 1e-3) / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
             "traffic": None, "kernel": "select_kernel", "kernel_ms": ms_step, "kernel_share_of_step": 1.0,
             "peak_source": f"{peak_src}, copy",
@@ -663,19 +828,24 @@ def run_cfg5(args, cfg, rank, world, dev):
             "candidate_evals_per_s": n * 700 / (ms_step * 1e-3)}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, desc, cores, _ = cfg5_cpu_sample(prof)
-        cpu = {"value": v, "unit": "queries/s", "cores": cores, "kind": "port", "sample": desc}
+        cores = os.cpu_count()
+        cp = CpuConfigPath(w, cores, limit=CFG5_SAMPLE)
+        _, t = cp.step()
+        st_us = cp.single_thread_us(1000)
+        cp.close()
+        cpu = {"value": cp.n / t, "unit": "queries/s", "cores": cores, "kind": cp.kind,
+               "sample": f"best-fit + fallback of the first {cp.n} fixture queries ({cp.source}, "
+                         f"multiprocessing.Pool({cores}))", "single_thread_us_per_query": st_us}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-            "config": {"workload": f"{args.workload}: {cfg['desc']}", "queries_per_step": n,
-                       "candidates_per_query": 700, "parallelism": f"query-sharded x{world}, no collective",
-                       "timing": f"{reps} batches per reported step (a batch is ~0.2 ms)",
-                       "l2": "inputs (6.8 MB) fit in L2: the kernel is ALU-bound, not memory-bound"},
+            "config": config_dict(args, cfg, world),
+            "timing": f"{reps} batches per reported step (a batch is ~0.2 ms); inputs (6.8 MB) fit in L2: "
+                      "the kernel is ALU-bound",
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-            "clocks": clk,
+            "clocks": clk, "parity": parity,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -22,8 +22,10 @@ class _Params(ctypes.Structure):
 
 
 def build(force: bool = False) -> str:
-    src = os.path.join(_HERE, "csrc", "oracle_select.c")
-    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(src):
+    srcs = [os.path.join(_HERE, "csrc", f) for f in ("oracle_select.c", "synth.c")]
+    outs = [_SO, os.path.join(_HERE, "_build", "libsynth.so")]
+    if force or any(not os.path.exists(o) for o in outs) or \
+            max(os.path.getmtime(s) for s in srcs) > min(os.path.getmtime(o) for o in outs):
         subprocess.check_call(["make", "-s", "-C", _HERE])
     return _SO
 

@@ -178,3 +178,99 @@ def check_topk(D_gpu, I_gpu, queries, corpus, k, rtol, *, D_ref=None, I_ref=None
                 viol.append((r, f"id mismatch at {j} outside tie tolerance"))
                 break
     return {"rows": q.shape[0], "exact_rows": exact_rows, "violations": viol}
+
+
+def search_torch_cpu(queries: np.ndarray, corpus: np.ndarray, corpus_norms: np.ndarray, k: int, *,
+                     block: int = 16384):
+    """FAISS-style flat-L2 on the CPU with torch's BLAS on all host threads
+    (the ``exhaustive_L2sqr_blas`` decomposition: ``|q|^2 + |c|^2 - 2 q.c`` per
+    corpus block, then a running per-query top-k).  The timed CPU baseline /
+    reference-arm retrieval; fp32 arithmetic, so ties and near-ties come back
+    in arbitrary order (``exact_topk`` re-ranks the candidates in float64).
+    The corpus norms are precomputed (as the GPU index does at ``add``)."""
+    import torch
+
+    q = torch.from_numpy(np.ascontiguousarray(queries, dtype=np.float32))
+    qn = (q * q).sum(1, keepdim=True)
+    n = corpus.shape[0]
+    kk = min(k, n)
+    bestD = torch.full((q.shape[0], 0), float("inf"))
+    bestI = torch.zeros((q.shape[0], 0), dtype=torch.int64)
+    for s in range(0, n, block):
+        c = torch.from_numpy(corpus[s:s + block])
+        base = qn + torch.from_numpy(corpus_norms[s:s + block])[None, :]
+        d = torch.addmm(base, q, c.T, beta=1.0, alpha=-2.0).clamp_(min=0.0)
+        dd, ii = torch.topk(d, min(kk, d.shape[1]), dim=1, largest=False, sorted=False)
+        bestD = torch.cat([bestD, dd], 1)
+        bestI = torch.cat([bestI, ii + s], 1)
+        if bestD.shape[1] > 4 * kk:
+            bestD, sel = torch.topk(bestD, kk, dim=1, largest=False, sorted=False)
+            bestI = torch.gather(bestI, 1, sel)
+    bestD, sel = torch.topk(bestD, kk, dim=1, largest=False, sorted=True)
+    bestI = torch.gather(bestI, 1, sel)
+    return bestD.numpy(), bestI.numpy()
+
+
+def exact_topk(queries, corpus, cand_ids: np.ndarray, k: int):
+    """Float64 re-score of candidate ids per query, ordered by (distance, id):
+    the exact top-k whenever the true top-k is among the candidates (a
+    fp32 scan with a margin of extra candidates guarantees that outside
+    near-ties far below the tolerance)."""
+    q = _as_f64(queries)
+    nq = q.shape[0]
+    D = np.full((nq, k), np.inf)
+    I = np.full((nq, k), -1, dtype=np.int64)
+    for r in range(nq):
+        ids = np.unique(cand_ids[r][cand_ids[r] >= 0])
+        c = _as_f64(corpus[ids])
+        d = ((c - q[r]) ** 2).sum(1)
+        o = np.lexsort((ids, d))[:k]
+        D[r, :len(o)] = d[o]
+        I[r, :len(o)] = ids[o]
+    return D, I
+
+
+def check_topk_rel(D_gpu, I_gpu, queries, corpus, D_ref, I_ref, rtol: float, atol_scale: float = 1e-6):
+    """Parity of a GPU result against the exact (float64) top-k, tolerance
+    RELATIVE TO THE DISTANCE (north star: 1e-3 for bf16, 1e-5 for fp32):
+    ``|D - D_true| <= rtol * D_true + atol_scale * (|q|^2 + |c|^2)``; the
+    second term is the cancellation floor of the ``|q|^2 + |c|^2 - 2 q.c``
+    form (FAISS's too) and only matters for (near-)duplicates, D ~ 0.
+
+    Rules: (1) each returned distance within tolerance of the float64
+    distance of the returned id; (2) rank by rank within tolerance of the
+    exact distance; (3) so ids may differ only inside tolerance-ties.
+    Returns rows, exact-id rows, violations, and the max relative error
+    ``|D - D_true| / D_true`` over entries with D_true >= 1e-3."""
+    q = _as_f64(queries)
+    D_gpu = np.asarray(D_gpu, dtype=np.float64)
+    I_gpu = np.asarray(I_gpu, dtype=np.int64)
+    qn = np.einsum("ij,ij->i", q, q)
+    viol, exact_rows, max_rel, max_abs = [], 0, 0.0, 0.0
+    for r in range(q.shape[0]):
+        exact_rows += int(np.array_equal(I_gpu[r], I_ref[r]))
+        valid = I_ref[r] >= 0
+        if not np.array_equal(I_gpu[r] >= 0, valid):
+            viol.append((r, "padding mismatch"))
+            continue
+        ids = I_gpu[r][valid]
+        if len(np.unique(ids)) != len(ids):
+            viol.append((r, "duplicate ids"))
+            continue
+        c = _as_f64(corpus[ids]) if len(ids) else np.zeros((0, q.shape[1]))
+        true_d = ((c - q[r]) ** 2).sum(1)
+        tol = rtol * true_d + atol_scale * (qn[r] + np.einsum("ij,ij->i", c, c))
+        err = np.abs(D_gpu[r][valid] - true_d)
+        big = true_d >= 1e-3
+        if big.any():
+            max_rel = max(max_rel, float((err[big] / true_d[big]).max()))
+        if len(err):
+            max_abs = max(max_abs, float(err.max()))
+        if np.any(err > tol):
+            viol.append((r, "distance off"))
+            continue
+        tol_ref = rtol * D_ref[r][valid] + atol_scale * (qn[r] + np.einsum("ij,ij->i", c, c))
+        if np.any(np.abs(true_d - D_ref[r][valid]) > np.maximum(tol, tol_ref)):
+            viol.append((r, "rank distance off"))
+    return {"rows": int(q.shape[0]), "exact_rows": exact_rows, "violations": viol,
+            "max_rel_err": max_rel, "max_abs_err": max_abs}

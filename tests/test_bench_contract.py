@@ -25,7 +25,7 @@ def test_reference_arm_prints_one_contract_line():
         assert key in d, key
     assert d["impl"] == "reference" and d["value"] > 0 and d["higher_is_better"] is True
     assert d["steps"] == 2 and d["warmup"] == 1 and d["vs_baseline"] is None
-    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
+    assert d["cpu_baseline"]["kind"] in ("reference", "port") and d["cpu_baseline"]["cores"] >= 1
     assert d["cpu_baseline"]["value"] == d["value"]
     assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
     assert d["config"]["workload"].startswith("cfg5")
@@ -64,3 +64,41 @@ def test_our_arm_prints_one_contract_line_on_the_gpu(workload):
     e2e = d["e2e"]
     assert e2e["value"] > 0 and e2e["h2d_bytes_per_step"] > 0 and e2e["d2h_bytes_per_step"] > 0
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
+
+
+def test_reference_arm_retrieval_workload_is_measured_not_extrapolated():
+    """cfg1 through the reference arm: 128 queries x the full corpus + the
+    as-shipped config path per step; ms_per_step is the measured step time and
+    the config dict is the one our arm prints."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--workload", "cfg1",
+                        "--steps", "2", "--warmup", "1"], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][0])
+    cb = d["cpu_baseline"]
+    assert abs(d["ms_per_step"] - cb["retrieval_ms_per_step"] - cb["config_ms_per_step"]) < 1e-6 * d["ms_per_step"]
+    assert "extrapolat" not in cb["sample"].replace("no extrapolation", "")
+    sys.path.insert(0, ROOT)
+    import bench
+
+    class A:
+        workload, data, corpus_rows, queries = "cfg1", "iso", None, None
+    assert d["config"] == bench.config_dict(A, bench.workload_cfg(A), 1)
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(900)
+def test_our_arm_parity_block_on_a_small_corpus():
+    """Our arm with the CPU leg on a 300k-row corpus: the config decisions
+    equal the reference's, the join is the top-k prefix, and the 128 sampled
+    queries match the float64 exact top-k within the north-star tolerance."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--workload", "cfg4", "--steps", "3",
+                        "--warmup", "3", "--corpus-rows", "300000", "--no-e2e"], capture_output=True, text=True,
+                       timeout=800, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][0])
+    p = d["parity"]
+    assert p["config_decisions"]["mismatches"] == 0 and p["config_decisions"]["checked"] == 8192
+    assert p["join_prefix"] is True
+    assert p["retrieval"]["violations"] == 0 and p["retrieval"]["sample_queries"] == 128
+    assert p["retrieval"]["max_rel_err"] < 1e-3
+    assert d["cpu_baseline"]["value"] > 0 and d["cpu_baseline"]["cores"] >= 1
