@@ -14,6 +14,7 @@ kernel of ``libragsched_b200.so``:
 from __future__ import annotations
 
 import ctypes
+import functools
 from dataclasses import dataclass
 
 import numpy as np
@@ -87,9 +88,25 @@ def pack_profiles(profiles) -> np.ndarray:
     """QueryProfile-like objects -> structured array of rs_profile."""
     a = np.zeros(len(profiles), dtype=PROFILE_DTYPE)
     for i, p in enumerate(profiles):
-        a[i] = (bool(p.complexity_high), bool(p.needs_joint_reasoning), int(p.pieces_required),
-                int(p.summary_len_range.low), int(p.summary_len_range.high), float(p.confidence))
+        a[i] = profile_tuple(p)
     return a
+
+
+def profile_tuple(p) -> tuple:
+    """QueryProfile-like -> one rs_profile record as a tuple."""
+    return (bool(p.complexity_high), bool(p.needs_joint_reasoning), int(p.pieces_required),
+            int(p.summary_len_range.low), int(p.summary_len_range.high), float(p.confidence))
+
+
+@functools.lru_cache(maxsize=256)
+def params_c(params: SelectParams) -> _lib.SelectParamsC:
+    """The (cached) C struct of a SelectParams (scalar calls reuse it)."""
+    return params.c()
+
+
+@functools.lru_cache(maxsize=64)
+def cost_c(cost: CostModel) -> _lib.CostModelC:
+    return cost.c()
 
 
 def profiles_from_arrays(complexity_high, joint, pieces, summary_lo, summary_hi, confidence) -> np.ndarray:

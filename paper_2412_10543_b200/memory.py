@@ -16,6 +16,7 @@ import torch
 
 from . import _lib
 from . import batch as _b
+from . import scalar as _scalar
 from .types import DEFAULT_MAX_CHUNKS, ContextOverflow, InvalidChunkCount
 from .types import DEFAULT_TEMPLATE_TOKENS, SynthesisMethod, method_bit
 
@@ -38,12 +39,8 @@ def plan_bytes(query_token_len: int, cfg, chunk_size: int, per_token_bytes: int,
     il = cfg.intermediate_length
     if m == method_bit(SynthesisMethod.MAP_REDUCE) and (il is None or il <= 0):
         raise ValueError("map_reduce config requires a positive intermediate_length")
-    dev = _b.default_device()
     params = _b.SelectParams(int(per_token_bytes), int(chunk_size), int(out_budget), int(template_tokens))
-    t = lambda v, dt: torch.tensor([v], dtype=dt, device=dev)  # noqa: E731
-    out = _b.plan_bytes_batch(t(m, torch.uint8), t(int(cfg.num_chunks), torch.int32), t(int(il or 0), torch.int32),
-                              t(int(query_token_len), torch.int32), params)
-    return int(out.item())
+    return _scalar.plan_bytes_one(m, int(cfg.num_chunks), int(il or 0), int(query_token_len), _b.params_c(params))
 
 
 # -- per-call expansion (memory.py:29-67, :89-150) -----------------------------

@@ -10,12 +10,15 @@ one launch sequence.
 
 from __future__ import annotations
 
+import functools
 from collections import deque
 from dataclasses import dataclass
 
 import numpy as np
 
+from . import _lib
 from . import batch as _b
+from . import scalar as _scalar
 from .mapping import PrunedConfigSpace, hull_of_spaces
 from .types import DEFAULT_MAX_CHUNKS, IntRange, SynthesisMethod
 
@@ -62,27 +65,26 @@ def _window_spaces(window) -> list:
 
 def _gate_one(profile, window_spaces, *, threshold, default_space, max_chunks, space_cls=None,
               method_enum=None, range_cls=None):
-    """Run the gate kernel on one profile.  threshold=None means "always
-    accept" (plain map_profile).  Returns (space, used_fallback)."""
-    import torch
-
-    dev = _b.default_device()
+    """Run the gate kernel on one profile (scalar fast path, scalar.py).
+    threshold=None means "always accept" (plain map_profile).  Returns
+    (space, used_fallback)."""
     space_cls = space_cls or PrunedConfigSpace
     method_enum = method_enum or SynthesisMethod
     range_cls = range_cls or IntRange
-    rec = _b.pack_profiles([profile])
-    thr = float(threshold) if threshold is not None else 1.0
+    prof = _b.profile_tuple(profile)
     if threshold is None:
-        rec["confidence"] = 1.0
-    window = _b.GateWindow(dev, window_spaces)
-    out = _b.prune_gate(_b.to_device(rec, dev), window, threshold=thr,
-                        default_space=default_space if default_space is not None else DEFAULT_FALLBACK_SPACE,
-                        max_chunks=max_chunks)
-    r = _b.from_device(out, _b.SPACE_DTYPE)[0]
-    torch.cuda.current_stream().synchronize()
+        prof = prof[:5] + (1.0,)
+    ds = _b.space_record(default_space if default_space is not None else DEFAULT_FALLBACK_SPACE)
+    gp = _gate_params(float(threshold) if threshold is not None else 1.0, ds, int(max_chunks))
+    r = _scalar.gate_one(prof, [_b.space_record(s) for s in window_spaces], gp)
     if int(r["gate_fallback"]) and default_space is not None and not window_spaces:
         return default_space, True  # `window.hull() or default_space` returns the object itself
     return _b.unpack_space(r, space_cls=space_cls, method_enum=method_enum, range_cls=range_cls), bool(r["gate_fallback"])
+
+
+@functools.lru_cache(maxsize=64)
+def _gate_params(threshold: float, ds: tuple, max_chunks: int):
+    return _lib.GateParamsC(threshold, _lib.SpaceC(ds[0], ds[1], ds[2], ds[3], ds[4], 1, 0), max_chunks, 0)
 
 
 def gate_profile(out, window, threshold: float = GATE_THRESHOLD, *, default_space=DEFAULT_FALLBACK_SPACE,

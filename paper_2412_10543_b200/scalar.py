@@ -1,0 +1,132 @@
+"""One-query calls of the C ABI at the lowest latency the GPU allows.
+
+The reference-facing scalar functions (``best_fit_select``,
+``fallback_config``, ``gate_profile`` / ``map_profile``, ``plan_bytes``,
+``call_latency``) get one query per call.  A batch API round trip (allocate
+device tensors, copy each argument H2D, launch, copy D2H) costs several
+synchronous copies per call; here the arguments and results live in ONE
+pinned host block that the kernels read and write directly (pinned host
+memory is device-accessible under unified addressing), so a call is: fill
+the block from Python, one launch on a private stream, one stream
+synchronize, read the block.  Same kernels, same results as the batch path.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import CONFIG_DTYPE, PROFILE_DTYPE, SPACE_DTYPE, WINDOW_DTYPE
+
+# byte offsets inside the pinned block
+_SPACE, _PROFILE, _QLEN, _FREE, _CONFIG, _WINDOW, _OUTSPACE = 0, 16, 32, 40, 48, 64, 240
+_LAT_IN, _LAT_OUT, _PB_IN, _PB_OUT = 256, 280, 288, 312
+_BLOCK = 512
+
+
+class _Ctx:
+    def __init__(self, device: int):
+        self.device = device
+        self.lib = _lib.lib_for_device(device)
+        with torch.cuda.device(device):
+            self.stream = torch.cuda.Stream(device=device)
+            self.block = torch.zeros(_BLOCK, dtype=torch.uint8, pin_memory=True)
+            self.ws = torch.empty(max(int(self.lib.rs_prune_gate_workspace_size(1)), 1), dtype=torch.uint8,
+                                  device=torch.device("cuda", device))
+        self.base = int(self.block.data_ptr())
+        self.buf = self.block.numpy()
+        v = lambda off, dt, n=1: self.buf[off:off + dt.itemsize * n].view(dt)  # noqa: E731
+        self.space = v(_SPACE, SPACE_DTYPE)
+        self.profile = v(_PROFILE, PROFILE_DTYPE)
+        self.qlen = v(_QLEN, np.dtype("<i4"))
+        self.free = v(_FREE, np.dtype("<i8"))
+        self.config = v(_CONFIG, CONFIG_DTYPE)
+        self.window = v(_WINDOW, WINDOW_DTYPE)
+        self.outspace = v(_OUTSPACE, SPACE_DTYPE)
+        self.lat_in = v(_LAT_IN, np.dtype("<i8"), 3)
+        self.lat_out = v(_LAT_OUT, np.dtype("<f8"))
+        self.pb_in = v(_PB_IN, np.dtype("<i4"), 4)   # method, num_chunks, interlen, qlen
+        self.pb_out = v(_PB_OUT, np.dtype("<i8"))
+        self.sptr = int(self.stream.cuda_stream)
+
+    def p(self, off: int) -> int:
+        return self.base + off
+
+    def sync(self):
+        self.stream.synchronize()
+
+
+_ctx: dict[int, _Ctx] = {}
+_lock = threading.Lock()
+
+
+def ctx() -> _Ctx:
+    if not torch.cuda.is_available():
+        raise _lib.LibraryUnavailable("no CUDA device: paper_2412_10543_b200 runs only on a B200 (no CPU fallback)")
+    dev = torch.cuda.current_device()
+    c = _ctx.get(dev)
+    if c is None:
+        with _lock:
+            c = _ctx.get(dev) or _Ctx(dev)
+            _ctx[dev] = c
+    return c
+
+
+def select_one(space: tuple | None, profile: tuple | None, qlen: int, free_bytes: int,
+               params: _lib.SelectParamsC) -> np.void:
+    """rs_select for one query.  ``space`` = (methods, n_lo, n_hi, il_lo,
+    il_hi) or None (no candidates: straight to the fallback); ``profile`` =
+    an rs_profile tuple or None.  Returns the rs_config record (a copy)."""
+    c = ctx()
+    with _lock:
+        c.space[0] = (*space, 0, 0) if space is not None else (0, 0, 0, 0, 0, 0, 0)
+        if profile is not None:
+            c.profile[0] = profile
+        c.qlen[0] = qlen
+        c.free[0] = free_bytes
+        _lib.check(c.lib.rs_select(c.p(_SPACE), c.p(_PROFILE) if profile is not None else 0, c.p(_QLEN),
+                                   c.p(_FREE), 1, ctypes.byref(params), None, 0, 0, c.p(_CONFIG), c.sptr),
+                   "rs_select")
+        c.sync()
+        return c.config[0].copy()
+
+
+def gate_one(profile: tuple, window_spaces: list, gate_params: _lib.GateParamsC) -> np.void:
+    """rs_prune_gate for one profile against a window of <= 10 space tuples.
+    Returns the rs_space record (a copy; ``gate_fallback`` set on fallback)."""
+    c = ctx()
+    with _lock:
+        c.profile[0] = profile
+        w = c.window[0]
+        n = len(window_spaces)
+        for i, s in enumerate(window_spaces):
+            w["spaces"][i] = (*s, 0, 0)
+        w["len"] = n
+        _lib.check(c.lib.rs_prune_gate(c.p(_PROFILE), 1, ctypes.byref(gate_params), c.p(_WINDOW), c.p(_OUTSPACE),
+                                       int(c.ws.data_ptr()), c.ws.numel(), c.sptr), "rs_prune_gate")
+        c.sync()
+        return c.outspace[0].copy()
+
+
+def call_latency_one(prompt_tokens: int, max_output_tokens: int, concurrent: int, cost: _lib.CostModelC) -> float:
+    c = ctx()
+    with _lock:
+        c.lat_in[:] = (prompt_tokens, max_output_tokens, concurrent)
+        _lib.check(c.lib.rs_call_latency(c.p(_LAT_IN), c.p(_LAT_IN + 8), c.p(_LAT_IN + 16), 1, ctypes.byref(cost),
+                                         c.p(_LAT_OUT), c.sptr), "rs_call_latency")
+        c.sync()
+        return float(c.lat_out[0])
+
+
+def plan_bytes_one(method: int, num_chunks: int, interlen: int, qlen: int, params: _lib.SelectParamsC) -> int:
+    c = ctx()
+    with _lock:
+        c.pb_in[:] = (method, num_chunks, interlen, qlen)
+        _lib.check(c.lib.rs_plan_bytes(c.p(_PB_IN), c.p(_PB_IN + 4), c.p(_PB_IN + 8), c.p(_PB_IN + 12), 1,
+                                       ctypes.byref(params), c.p(_PB_OUT), c.sptr), "rs_plan_bytes")
+        c.sync()
+        return int(c.pb_out[0])

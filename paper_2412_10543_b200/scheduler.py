@@ -16,6 +16,7 @@ import torch
 
 from . import _lib
 from . import batch as _b
+from . import scalar as _scalar
 from . import memory as _mem
 from ._lib import SPACE_DTYPE
 from .mapping import EnumGranularity
@@ -33,14 +34,13 @@ class SchedulingImpossible(RuntimeError):
     """scheduler.py:41."""
 
 
-def _run_select(space_rec, profile, q, free_bytes, params, config_cls, method_enum):
-    dev = _b.default_device()
-    spaces = _b.to_device(space_rec, dev)
-    prof = _b.to_device(_b.pack_profiles([profile]), dev) if profile is not None else None
-    qlen = torch.tensor([int(q.query_token_len)], dtype=torch.int32, device=dev)
-    free = torch.tensor([int(free_bytes)], dtype=torch.int64, device=dev)
-    out, _ = _b.select(spaces, prof, qlen, free, params)
-    return _b.unpack_config(_b.from_device(out, _b.CONFIG_DTYPE)[0], config_cls=config_cls, method_enum=method_enum)
+def _run_select(space, profile, q, free_bytes, params, config_cls, method_enum):
+    """One query through ``rs_select`` (scalar fast path: pinned, device-mapped
+    arguments; see scalar.py)."""
+    rec = _scalar.select_one(_b.space_record(space) if space is not None else None,
+                             _b.profile_tuple(profile) if profile is not None else None,
+                             int(q.query_token_len), int(free_bytes), _b.params_c(params))
+    return _b.unpack_config(rec, config_cls=config_cls, method_enum=method_enum)
 
 
 def best_fit_select(space, q, free_bytes: int, *, model, meta, out_budget: int,
@@ -51,7 +51,7 @@ def best_fit_select(space, q, free_bytes: int, *, model, meta, out_budget: int,
     fits."""
     params = _b.SelectParams.from_model(model, meta, out_budget, template_tokens, DEFAULT_MAX_CHUNKS, granularity,
                                         allow_fallback=False)
-    return _run_select(_b.pack_spaces([space]), None, q, free_bytes, params, config_cls, method_enum)
+    return _run_select(space, None, q, free_bytes, params, config_cls, method_enum)
 
 
 def fallback_config(profile, q, free_bytes: int, *, model, meta, out_budget: int,
@@ -61,8 +61,8 @@ def fallback_config(profile, q, free_bytes: int, *, model, meta, out_budget: int
     the largest fitting stuff (joint); never map_reduce; None = MustQueue."""
     params = _b.SelectParams.from_model(model, meta, out_budget, template_tokens, max_chunks, None,
                                         allow_fallback=True)
-    empty = np.zeros(1, dtype=SPACE_DTYPE)  # no candidates: the kernel goes straight to the fallback
-    return _run_select(empty, profile, q, free_bytes, params, config_cls, method_enum)
+    # no candidates: the kernel goes straight to the fallback
+    return _run_select(None, profile, q, free_bytes, params, config_cls, method_enum)
 
 
 # -- the stateful scheduler (scheduler.py:33-469) -------------------------------

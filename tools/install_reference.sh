@@ -12,4 +12,8 @@ cp -r "$SRC"/. "$TMP"/
 python -m pip install --quiet --no-index --no-build-isolation --no-deps --find-links /opt/wheelhouse \
     --target "$ROOT/baseline/_ref" --upgrade "$TMP"
 rm -rf "$TMP"
-echo "installed ragsched into $ROOT/baseline/_ref"
+# the reference's own test suite, run on the GPU box with the drop-in active
+# (tests/test_gpu_reference_sim.py); git-ignored like the install itself
+rm -rf "$ROOT/baseline/_ref_tests"
+cp -r "$SRC/tests" "$ROOT/baseline/_ref_tests"
+echo "installed ragsched into $ROOT/baseline/_ref (tests in baseline/_ref_tests)"
