@@ -879,7 +879,7 @@ extern "C" int rs_index_create(int32_t dim, int32_t dtype, int64_t capacity, int
     if (e == cudaSuccess) e = cudaMalloc(&ix->norms, sizeof(float) * (capacity + rs::kTcBN));
     if (e == cudaSuccess) e = cudaMalloc(&ix->norm_max, sizeof(float));
     if (e == cudaSuccess) e = cudaMalloc(&ix->sched_counter, sizeof(int32_t) * (1 + rs::kMaxSegments));
-    if (e == cudaSuccess && dtype == RS_F32 && RS_TF32_STORED_LO)
+    if (e == cudaSuccess && dtype == RS_F32 && RS_TF32_STORED_LO && dim % 4 == 0)
       e = cudaMalloc(&ix->lo, size_t(capacity) * dim * sizeof(float));
     if (e == cudaSuccess) e = cudaMalloc(&ix->cmin, sizeof(float) * (rs::ceil_div(capacity, 256) * 8 + 8));
     if (e == cudaSuccess) e = cudaMemset(ix->norm_max, 0, sizeof(float));
@@ -958,7 +958,7 @@ extern "C" int rs_index_add(rs_index* ix, const void* emb, int64_t n, void* stre
   if (rc) return rc;
   rc = rs::launch_chunk_min(ix->norms, ix->ntotal, ix->ntotal + n, ix->cmin, st);
   if (rc) return rc;
-  if (ix->dtype == RS_F32 && RS_TF32_STORED_LO) {  // 3xTF32 residuals of the new rows
+  if (ix->lo != nullptr) {  // 3xTF32 residuals of the new rows (fp32, dim % 4 == 0: the tcgen05 path exists)
     const size_t off = size_t(ix->ntotal) * ix->dim;
     rc = rs::launch_tf32_lo(static_cast<const float*>(ix->data) + off, n * ix->dim, ix->lo + off, st);
     if (rc) return rc;
@@ -1009,8 +1009,11 @@ extern "C" int rs_index_reserve(rs_index* ix, int64_t nq_max, int32_t k) {
   RS_REQUIRE(ix != nullptr && nq_max >= 0 && k >= 1, "bad arguments");
   DeviceGuard g(ix->device);
   // worst case over the expected corpus size (capacity)
-  const SearchPlan plan = make_plan(ix, choose_algo(ix, k), nq_max, std::max<int64_t>(ix->capacity, 1), k);
-  return ensure_ws(ix, nq_max, size_t(nq_max) * plan.lists() * k * sizeof(uint64_t));
+  const int algo = choose_algo(ix, k);
+  // the fp32 tensor-core search keeps k + kRefineExtra candidates per list
+  const int kk = (ix->dtype == RS_F32 && algo == RS_ALGO_TCGEN05) ? k + kRefineExtra : k;
+  const SearchPlan plan = make_plan(ix, algo, nq_max, std::max<int64_t>(ix->capacity, 1), kk);
+  return ensure_ws(ix, nq_max, size_t(nq_max) * plan.lists() * kk * sizeof(uint64_t));
 }
 
 extern "C" int rs_index_last_plan(const rs_index* ix, int32_t* segments, int32_t* qtiles, int32_t* ctas,
@@ -1052,7 +1055,7 @@ static int search_impl(rs_index* ix, const void* queries, int64_t nq, int32_t k,
   SearchPlan plan;
   if (ix->dtype == RS_F32 && choose_algo(ix, k) == RS_ALGO_TCGEN05) {
     // 3xTF32 candidates (kc per query) -> exact fp32 re-rank to k
-    const int kc = std::min(k + kRefineExtra, kTcMaxK);
+    const int kc = k + kRefineExtra;  // <= kTcMaxK + kRefineExtra: the tf32 lists' capacity
     rc = run_partial(ix, queries, nq, kc, id_base, st, &plan);
     if (rc) return rc;
     const size_t cb = 2 * size_t(nq) * kc * sizeof(uint64_t);  // merged candidates + their exact keys

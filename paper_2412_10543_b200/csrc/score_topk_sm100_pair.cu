@@ -63,7 +63,11 @@ constexpr int HB = BN / 2;      // corpus rows staged per CTA
 #ifndef RS_PAIR_PREFETCH
 #define RS_PAIR_PREFETCH 0
 #endif
-constexpr int KREG = kTcMaxK;   // register top-k capacity (k <= 40)
+constexpr int KREG = kTcMaxK;   // register top-k capacity, bf16 (k <= 40)
+// tf32 path: the candidate pass keeps k + kRefineExtra rows for the exact
+// re-rank, so its lists hold up to kTcMaxK + kRefineExtra (every k <= 40 keeps
+// its 8 spare candidates)
+constexpr int KREG_TF32 = kTcMaxK + kRefineExtra;
 // candidate buffer per row; a warp flushes when one of its lanes holds more
 // than BUF - CHECK entries, so every flush batches many candidates per lane
 constexpr int BUF = RS_PAIR_BUF;
@@ -168,9 +172,9 @@ struct Cfg {
   static constexpr size_t OFF_TAIL = OFF_CN + 2 * BN * sizeof(float);
   static constexpr size_t SMEM_BYTES = OFF_TAIL + sizeof(Tail);
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
+  static constexpr int KR = TF ? KREG_TF32 : KREG;  // register top-k capacity
+  using TopK = RegTopK<KR, EPI_THREADS, BUF>;
 };
-
-using TopK = RegTopK<KREG, EPI_THREADS, BUF>;
 
 struct Params {
   const float* qn;
@@ -565,7 +569,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     const int row = SM ? (ew & 1) * 32 + lane : ew * 32 + lane;
     const int tcol0 = SM ? eg * SLICE : 0;  // tile column held at this accumulator's TMEM column 0
     const int et = (warp - EPI_WARP0) * 32 + lane;
-    TopK rt;
+    typename C::TopK rt;
     rt.k = p.k;
     rt.wbase = smem_u32(smem + C::OFF_BUF) + uint32_t(et) * 8u;
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tail->tempty[0]), pair_leader);
@@ -632,9 +636,9 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           return;
 #endif
           if (base + EPI_COLS <= valid)
-            epi_chunk32b<KREG, EPI_THREADS, BUF, CHECK, true>(rt, r, cn_t + base, id0 + base, EPI_COLS, thr);
+            epi_chunk32b<C::KR, EPI_THREADS, BUF, CHECK, true>(rt, r, cn_t + base, id0 + base, EPI_COLS, thr);
           else
-            epi_chunk32b<KREG, EPI_THREADS, BUF, CHECK, false>(rt, r, cn_t + base, id0 + base, valid - base, thr);
+            epi_chunk32b<C::KR, EPI_THREADS, BUF, CHECK, false>(rt, r, cn_t + base, id0 + base, valid - base, thr);
         };
 #if RS_PAIR_EPI_PAIRED
         // two 32-column loads in flight per wait (4 waits per 256-column tile)

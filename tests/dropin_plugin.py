@@ -21,7 +21,7 @@ def pytest_configure(config):
     from paper_2412_10543_b200 import dropin
 
     INSTALLED["originals"] = dropin.install(ragsched)
-    config.stash_dropin = True
+    print(f"GPU drop-in active: ragsched from {os.path.dirname(ragsched.__file__)}", flush=True)
 
 
 def pytest_report_header(config):
