@@ -207,6 +207,99 @@ __global__ void __launch_bounds__(kBlock) gate_hull_kernel(int64_t n, GateWs ws,
   }
 }
 
+// Batches of <= kBlock queries (and the scalar drop-in, n = 1): the four
+// steps above in ONE block and one launch — accept flags, the block-wide
+// exclusive scan of the accepted ranks, the compaction and the hulls all in
+// shared memory.
+__global__ void __launch_bounds__(kBlock) gate_small_kernel(const rs_profile* __restrict__ prof, int n, double thr,
+                                                            int max_chunks, rs_space dflt,
+                                                            rs_space* __restrict__ out,
+                                                            rs_window* __restrict__ window_io) {
+  __shared__ rs_space s_sp[kBlock];   // accepted spaces by batch index
+  __shared__ int32_t s_acc_idx[kBlock];
+  __shared__ int32_t warp_cnt[32];
+  __shared__ int32_t s_total;
+  __shared__ rs_window carry;
+  const int i = threadIdx.x;
+  const int lane = i & 31, wid = i >> 5;
+  if (i == 0) carry = *window_io;
+  int acc = 0;
+  if (i < n) {
+    const rs_profile p = prof[i];
+    acc = p.confidence >= thr;  // profiler.py:481, IEEE double compare
+    if (acc) {
+      const rs_space sp = map_profile(p, max_chunks);
+      s_sp[i] = sp;
+      out[i] = sp;
+    }
+  }
+  const unsigned bal = __ballot_sync(0xffffffffu, acc);
+  if (lane == 0) warp_cnt[wid] = __popc(bal);
+  __syncthreads();
+  if (wid == 0) {
+    const int32_t w = warp_cnt[lane];
+    int32_t x = w;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, x, off);
+      if (lane >= off) x += y;
+    }
+    warp_cnt[lane] = x - w;  // exclusive over warps
+    if (lane == 31) s_total = x;
+  }
+  __syncthreads();
+  const int32_t rank = warp_cnt[wid] + __popc(bal & ((1u << lane) - 1u));
+  if (acc) s_acc_idx[rank] = i;
+  __syncthreads();
+  const int32_t total_acc = s_total;
+  const int32_t w0 = carry.len;
+  auto entry = [&](int32_t t) -> const rs_space& { return t < w0 ? carry.spaces[t] : s_sp[s_acc_idx[t - w0]]; };
+  if (i < n && !acc) {
+    const int32_t end = w0 + rank;
+    const int32_t beg = end > RS_WINDOW_CAPACITY ? end - RS_WINDOW_CAPACITY : 0;
+    rs_space s;
+    if (end == 0) {
+      s = dflt;  // `window.hull() or default_space` (profiler.py:485)
+    } else {
+      const rs_space& f = entry(beg);
+      int m = 0, lo = f.num_chunks_lo, hi = f.num_chunks_hi, a = -1, b = -1;
+      for (int32_t t = beg; t < end; ++t) {
+        const rs_space& e = entry(t);
+        m |= e.methods;
+        lo = min(lo, (int)e.num_chunks_lo);
+        hi = max(hi, (int)e.num_chunks_hi);
+        if (e.methods & RS_MAP_REDUCE) {
+          a = a < 0 ? e.interlen_lo : min(a, (int)e.interlen_lo);
+          b = b < 0 ? e.interlen_hi : max(b, (int)e.interlen_hi);
+        }
+      }
+      s = rs_space{};
+      s.methods = (uint16_t)m;
+      s.num_chunks_lo = (uint16_t)lo;
+      s.num_chunks_hi = (uint16_t)hi;
+      if (m & RS_MAP_REDUCE) {  // mapping.py:196-199
+        s.interlen_lo = (uint16_t)(a < 0 ? 30 : a);
+        s.interlen_hi = (uint16_t)(a < 0 ? 200 : b);
+      }
+    }
+    s.gate_fallback = 1;
+    s.reserved = 0;
+    out[i] = s;
+  }
+  if (i == 0) {
+    const int32_t total = w0 + total_acc;
+    const int32_t beg = total > RS_WINDOW_CAPACITY ? total - RS_WINDOW_CAPACITY : 0;
+    rs_window w{};
+    for (int32_t t = beg; t < total; ++t) {
+      rs_space e = entry(t);
+      e.gate_fallback = 0;
+      w.spaces[t - beg] = e;
+    }
+    w.len = total - beg;
+    *window_io = w;
+  }
+}
+
 }  // namespace
 }  // namespace rs
 
@@ -229,6 +322,14 @@ extern "C" int rs_prune_gate(const rs_profile* profiles, int64_t n, const rs_gat
   const size_t need = ws_layout(n, (char*)workspace, &ws);
   RS_REQUIRE(workspace_bytes >= need, "workspace too small (%zu < %zu)", workspace_bytes, need);
   cudaStream_t st = as_stream(stream);
+  rs_space dflt = params->default_space;
+  dflt.gate_fallback = 1;
+  if (n <= kBlock) {  // one block, one launch
+    gate_small_kernel<<<1, kBlock, 0, st>>>(profiles, int(n), params->threshold, params->max_chunks, dflt,
+                                            spaces_out, window_io);
+    RS_CHECK_LAUNCH("gate_small_kernel");
+    return RS_OK;
+  }
   const int64_t nb = ceil_div(n, kBlock);
   gate_map_kernel<<<(unsigned)nb, kBlock, 0, st>>>(profiles, n, params->threshold, params->max_chunks,
                                                   spaces_out, ws);
@@ -237,8 +338,6 @@ extern "C" int rs_prune_gate(const rs_profile* profiles, int64_t n, const rs_gat
   RS_CHECK_LAUNCH("gate_scan_kernel");
   gate_rank_kernel<<<(unsigned)nb, kBlock, 0, st>>>(n, ws);
   RS_CHECK_LAUNCH("gate_rank_kernel");
-  rs_space dflt = params->default_space;
-  dflt.gate_fallback = 1;
   gate_hull_kernel<<<(unsigned)nb, kBlock, 0, st>>>(n, ws, dflt, spaces_out, window_io);
   RS_CHECK_LAUNCH("gate_hull_kernel");
   return RS_OK;

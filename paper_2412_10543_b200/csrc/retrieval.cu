@@ -782,9 +782,11 @@ rs::SearchPlan make_plan(const rs_index* ix, int algo, int64_t nq, int64_t n, in
 
 // partial lists for (queries x this shard) -> part; returns the plan
 int run_partial(rs_index* ix, const void* queries, int64_t nq, int k, int64_t id_base, cudaStream_t st,
-                rs::SearchPlan* plan_out) {
+                rs::SearchPlan* plan_out, int algo_for_k = -1) {
   using namespace rs;
-  const int algo = choose_algo(ix, k);
+  // algo_for_k: the user's k when this pass keeps more candidates than k (the
+  // fp32 re-rank pass), so the kernel choice follows the user's k
+  const int algo = choose_algo(ix, algo_for_k >= 0 ? algo_for_k : k);
   RS_REQUIRE(!((ix->algo == RS_ALGO_TCGEN05 || ix->algo == RS_ALGO_TCGEN05_1SM) && algo == RS_ALGO_SIMT),
              "tcgen05 path needs 16-byte rows (bf16 dim %% 8, fp32 dim %% 4) and k <= %d", kTcMaxK);
   RS_REQUIRE(!(ix->algo == RS_ALGO_TCGEN05_1SM && ix->dtype != RS_BF16), "the single-CTA tcgen05 kernel is bf16-only");
@@ -1056,7 +1058,7 @@ static int search_impl(rs_index* ix, const void* queries, int64_t nq, int32_t k,
   if (ix->dtype == RS_F32 && choose_algo(ix, k) == RS_ALGO_TCGEN05) {
     // 3xTF32 candidates (kc per query) -> exact fp32 re-rank to k
     const int kc = k + kRefineExtra;  // <= kTcMaxK + kRefineExtra: the tf32 lists' capacity
-    rc = run_partial(ix, queries, nq, kc, id_base, st, &plan);
+    rc = run_partial(ix, queries, nq, kc, id_base, st, &plan, k);
     if (rc) return rc;
     const size_t cb = 2 * size_t(nq) * kc * sizeof(uint64_t);  // merged candidates + their exact keys
     if (cb > ix->cand_cap) {

@@ -764,6 +764,8 @@ int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap* tmql, cons
   const bool tf = tmql != nullptr;
   RS_REQUIRE(!tf || !RS_TF32_STORED_LO || tmcl != nullptr, "tf32 path with stored residuals needs the corpus lo map");
   RS_REQUIRE(!tf || G == 1, "the tf32 path has no multicast (RS_PAIR_GROUP) variant");
+  RS_REQUIRE(k >= 1 && k <= (tf ? KREG_TF32 : KREG), "k (%d) exceeds the register top-k capacity (%d)", k,
+             tf ? KREG_TF32 : KREG);
   RS_REQUIRE(!small || G == 1, "the M = 128 variant has no multicast (RS_PAIR_GROUP) variant");
   // (its epilogue splits columns by lane quadrant, not by warp group)
   RS_REQUIRE(!small || EG == 1, "the M = 128 variant has one epilogue warp group");

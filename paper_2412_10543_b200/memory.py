@@ -101,12 +101,16 @@ PLAN_ERRORS = {
 
 def plans_from_device(offsets, calls, totals, status, *, call_cls=LlmCall, plan_cls=CallPlan,
                       kind_enum=CallKind) -> list:
-    """Host objects of an ``rs_plan_calls`` result: one CallPlan per query, or
-    the RS_PLAN_* status (int) where the reference raises."""
-    off = offsets.cpu().numpy()
+    """Host objects of an ``rs_plan_calls`` result (device tensors): one
+    CallPlan per query, or the RS_PLAN_* status (int) where the reference raises."""
     rec = _b.from_device(calls, _lib.CALL_DTYPE) if calls.numel() else np.zeros(0, _lib.CALL_DTYPE)
-    tot = totals.cpu().numpy()
-    st = status.cpu().numpy()
+    return plans_from_host(offsets.cpu().numpy(), rec, totals.cpu().numpy(), status.cpu().numpy(),
+                           call_cls=call_cls, plan_cls=plan_cls, kind_enum=kind_enum)
+
+
+def plans_from_host(off, rec, tot, st, *, call_cls=LlmCall, plan_cls=CallPlan, kind_enum=CallKind) -> list:
+    """``plans_from_device`` over host arrays (offsets [n+1], rs_call records,
+    totals [n], status [n])."""
     kinds = [kind_enum(v) for v in _lib.CALL_KINDS]
     out = []
     for i in range(len(st)):
@@ -115,7 +119,7 @@ def plans_from_device(offsets, calls, totals, status, *, call_cls=LlmCall, plan_
             continue
         cs = []
         mappers = frozenset()
-        for r in rec[off[i]:off[i + 1]]:
+        for r in rec[int(off[i]):int(off[i + 1])]:
             kind = kinds[int(r["kind"])]
             if kind.value == "reducer":
                 deps = mappers
@@ -129,7 +133,31 @@ def plans_from_device(offsets, calls, totals, status, *, call_cls=LlmCall, plan_
     return out
 
 
-def raise_plan_error(code: int, cfg, *, max_chunks: int, max_context_tokens: int):
+def context_overflow_message(qlen: int, cfg, chunk_size: int, template_tokens: int, out_budget: int,
+                             max_context_tokens: int) -> str:
+    """The message of the reference's first failing ``_check_context``
+    (memory.py:81-86, :117-145) for this config."""
+    C, T, O, ctx = chunk_size, template_tokens, out_budget, max_context_tokens
+    n, m = cfg.num_chunks, cfg.synthesis_method.value
+    if m == "stuff":
+        checks = [("stuff call", qlen + n * C + T, O)]
+    elif m == "map_rerank":
+        checks = [("rerank call", qlen + C + T, O)]
+    else:
+        il = cfg.intermediate_length
+        checks = [("mapper call", qlen + C + T, il), ("reducer call", qlen + n * il + T, O)]
+    for label, prompt, out in checks:
+        if prompt + out > ctx:
+            return f"{label} needs {prompt + out} tokens, context window is {ctx}"
+    return "context window exceeded"
+
+
+def raise_plan_error(code: int, cfg, *, max_chunks: int, max_context_tokens: int, qlen: int = 0,
+                     chunk_size: int = 0, template_tokens: int = DEFAULT_TEMPLATE_TOKENS, out_budget: int = 0):
+    """Raise the reference's exception (and message) for an RS_PLAN_* status."""
+    if code == _lib.RS_PLAN_CONTEXT_OVERFLOW:
+        raise ContextOverflow(context_overflow_message(qlen, cfg, chunk_size, template_tokens, out_budget,
+                                                       max_context_tokens))
     exc, fmt = PLAN_ERRORS[code]
     desc = cfg.describe() if hasattr(cfg, "describe") else str(cfg)
     raise exc(fmt.format(n=getattr(cfg, "num_chunks", "?"), mc=max_chunks, cfg=desc, ctx=max_context_tokens))
@@ -140,6 +168,9 @@ def plan_calls(q, cfg, meta, model, out_budget: int, *, template_tokens: int = D
     """memory.py:89-150 on the GPU (``rs_plan_calls``): the config's LLM calls
     with their KV bytes.  Raises InvalidChunkCount / ContextOverflow /
     ValueError exactly where the reference does."""
+    # the reference's check order (memory.py:108-111): chunk count, then out_budget
+    if not 1 <= int(cfg.num_chunks) <= max_chunks:
+        raise InvalidChunkCount(f"num_chunks {cfg.num_chunks} outside [1, {max_chunks}]")
     if out_budget <= 0:
         raise ValueError("out_budget must be positive")
     dev = _b.default_device()
@@ -154,7 +185,7 @@ def plan_calls(q, cfg, meta, model, out_budget: int, *, template_tokens: int = D
     res = _b.plan_calls(_b.to_device(rec, dev), qlen, params, int(model.max_context_tokens))
     plan = plans_from_device(*res, call_cls=call_cls, plan_cls=plan_cls, kind_enum=kind_enum)[0]
     if isinstance(plan, int):
-        if int(cfg.num_chunks) < 1 or int(cfg.num_chunks) > max_chunks:
-            plan = _lib.RS_PLAN_INVALID_CHUNKS
-        raise_plan_error(plan, cfg, max_chunks=max_chunks, max_context_tokens=model.max_context_tokens)
+        raise_plan_error(plan, cfg, max_chunks=max_chunks, max_context_tokens=model.max_context_tokens,
+                         qlen=int(q.query_token_len), chunk_size=int(meta.chunk_size),
+                         template_tokens=int(template_tokens), out_budget=int(out_budget))
     return plan

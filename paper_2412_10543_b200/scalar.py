@@ -130,3 +130,80 @@ def plan_bytes_one(method: int, num_chunks: int, interlen: int, qlen: int, param
                                        ctypes.byref(params), c.p(_PB_OUT), c.sptr), "rs_plan_bytes")
         c.sync()
         return int(c.pb_out[0])
+
+
+class AdmitArena:
+    """Pinned, device-mapped buffers of one Scheduler's admission launches
+    (``rs_admit_fifo`` over a chunk of the waiting queue, then
+    ``rs_plan_calls`` over the admitted configs): the kernels read the packed
+    queue entries and write their results straight into host memory, so a
+    chunk costs two launch + synchronize round trips and no copies."""
+
+    def __init__(self, cap: int = 32, calls_per_plan: int = 36):
+        self.c = ctx()
+        self.cap = 0
+        self.calls_per_plan = calls_per_plan  # map_reduce: num_chunks + 1 calls
+        self._grow(cap)
+
+    def _grow(self, cap: int):
+        dev = torch.device("cuda", self.c.device)
+        pin = lambda shape, dt: torch.zeros(shape, dtype=dt, pin_memory=True)  # noqa: E731
+        self.cap = cap
+        self.t_spaces, self.t_profiles = pin((cap, 16), torch.uint8), pin((cap, 16), torch.uint8)
+        self.t_hasprof, self.t_qlen = pin(cap, torch.uint8), pin(cap, torch.int32)
+        self.t_configs, self.t_info, self.t_result = pin((cap, 16), torch.uint8), pin((cap, 16), torch.uint8), \
+            pin(24, torch.uint8)
+        self.t_offsets, self.t_totals, self.t_status = pin(cap + 1, torch.int64), pin(cap, torch.int64), \
+            pin(cap, torch.uint8)
+        self._grow_calls(cap * self.calls_per_plan)
+        self.ws = torch.empty(max(int(self.c.lib.rs_plan_calls_workspace_size(cap)), 1), dtype=torch.uint8,
+                              device=dev)
+        self.spaces = self.t_spaces.numpy()
+        self.profiles = self.t_profiles.numpy()
+        self.hasprof = self.t_hasprof.numpy()
+        self.qlen = self.t_qlen.numpy()
+        self.configs = self.t_configs.numpy().reshape(-1).view(CONFIG_DTYPE)
+        self.info = self.t_info.numpy().reshape(-1).view(_lib.ADMIT_INFO_DTYPE)
+        self.result = self.t_result.numpy().view(_lib.ADMIT_RESULT_DTYPE)
+        self.offsets = self.t_offsets.numpy()
+        self.totals = self.t_totals.numpy()
+        self.status = self.t_status.numpy()
+
+    def _grow_calls(self, n: int):
+        self.calls_cap = n
+        self.t_calls = torch.zeros((n, 24), dtype=torch.uint8, pin_memory=True)
+        self.calls = self.t_calls.numpy().reshape(-1).view(_lib.CALL_DTYPE)
+
+    def ensure(self, n: int):
+        if n > self.cap:
+            self._grow(max(n, 2 * self.cap))
+
+    def admit(self, n: int, params: _lib.SelectParamsC, capacity: int, used: int, max_ctx: int) -> tuple[int, int]:
+        """rs_admit_fifo over entries [0, n) (filled by the caller).  Returns
+        (admitted, stop)."""
+        c = self.c
+        ap = _lib.AdmitParamsC(int(capacity), int(used), int(max_ctx))
+        p = lambda t: int(t.data_ptr())  # noqa: E731
+        _lib.check(c.lib.rs_admit_fifo(p(self.t_spaces), p(self.t_profiles), p(self.t_hasprof), p(self.t_qlen), n,
+                                       ctypes.byref(params), ctypes.byref(ap), p(self.t_configs), p(self.t_info),
+                                       p(self.t_result), c.sptr), "rs_admit_fifo")
+        c.sync()
+        r = self.result[0]
+        return int(r["admitted"]), int(r["stop"])
+
+    def plan_calls(self, m: int, params: _lib.SelectParamsC, max_ctx: int):
+        """rs_plan_calls over the first m configs: the count pass, then (after
+        sizing) the fill pass.  Returns numpy views (offsets [m+1], calls,
+        totals [m], status [m])."""
+        c = self.c
+        p = lambda t: int(t.data_ptr())  # noqa: E731
+        args = (p(self.t_configs), p(self.t_qlen), m, ctypes.byref(params), int(max_ctx), p(self.t_offsets))
+        _lib.check(c.lib.rs_plan_calls(*args, 0, 0, p(self.t_status), int(self.ws.data_ptr()), self.ws.numel(),
+                                       c.sptr), "rs_plan_calls(count)")
+        c.sync()
+        if int(self.offsets[m]) > self.calls_cap:
+            self._grow_calls(int(self.offsets[m]))
+        _lib.check(c.lib.rs_plan_calls(*args, p(self.t_calls), p(self.t_totals), 0, int(self.ws.data_ptr()),
+                                       self.ws.numel(), c.sptr), "rs_plan_calls(fill)")
+        c.sync()
+        return self.offsets[:m + 1], self.calls, self.totals[:m], self.status[:m]

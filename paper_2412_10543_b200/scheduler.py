@@ -207,6 +207,7 @@ class Scheduler:
         self._sel = _b.SelectParams.from_model(params.model, params.meta, params.out_budget, params.template_tokens,
                                                params.max_chunks, g, allow_fallback=params.allow_fallback)
         self._dev = None
+        self._arena_obj = None
 
     @property
     def free_bytes(self) -> int:
@@ -289,32 +290,45 @@ class Scheduler:
             self._dev = _b.default_device()
         return self._dev
 
+    def _arena(self):
+        if self._arena_obj is None:
+            self._arena_obj = _scalar.AdmitArena(self.FIRST_CHUNK, self.params.max_chunks + 1)
+        return self._arena_obj
+
     def _admit_new(self, now: float, admissions: list, admitted: list) -> None:
         """The loop of scheduler.py:404-409 over _try_admit_new (:335-395),
-        as rs_admit_fifo launches over chunks of the waiting queue."""
+        as rs_admit_fifo launches over chunks of the waiting queue (packed
+        into a pinned, device-mapped arena: no copies, two round trips per
+        chunk).  An entry the C records cannot hold (e.g. a map_reduce range
+        starting at 0, memory.py:186-188) cuts the chunk before it; its error
+        is raised only once it reaches the head of the queue, as the
+        reference raises only for the entry it is admitting."""
         k, p = self._k, self.params
-        dev = self._device()
+        arena = self._arena()
         chunk = self.FIRST_CHUNK
         while self.waiting:
-            entries = [self._pack(pq) for pq in itertools.islice(self.waiting, 0, chunk)]
+            entries, pack_error = [], None
+            for pq in itertools.islice(self.waiting, 0, chunk):
+                try:
+                    entries.append(self._pack(pq))
+                except (ValueError, OverflowError) as e:
+                    pack_error = e
+                    break
             n = len(entries)
-            sp = torch.frombuffer(bytearray(b"".join(e[1] for e in entries)), dtype=torch.uint8).view(n, 16)
-            pr = torch.frombuffer(bytearray(b"".join(e[2] for e in entries)), dtype=torch.uint8).view(n, 16)
-            hp = torch.tensor([e[3] for e in entries], dtype=torch.uint8)
-            ql = torch.tensor([e[4] for e in entries], dtype=torch.int32)
-            sp, pr, hp, ql = (t.to(dev, non_blocking=True) for t in (sp, pr, hp, ql))
-            configs, info, result = _b.admit_fifo(sp, pr, ql, self._sel, capacity_bytes=self.capacity_bytes,
-                                                  used_bytes=self.used_bytes,
-                                                  max_context_tokens=p.model.max_context_tokens, has_profile=hp)
-            m_dev = None
-            res = _b.from_device(result.view(1, 24), _lib.ADMIT_RESULT_DTYPE)[0]
-            m, stop = int(res["admitted"]), int(res["stop"])
-            cfg_all = _b.from_device(configs[: min(m + 1, n)], _lib.CONFIG_DTYPE)
+            if n == 0:
+                raise pack_error
+            arena.ensure(n)
+            arena.spaces[:n] = np.frombuffer(b"".join(e[1] for e in entries), dtype=np.uint8).reshape(n, 16)
+            arena.profiles[:n] = np.frombuffer(b"".join(e[2] for e in entries), dtype=np.uint8).reshape(n, 16)
+            arena.hasprof[:n] = [e[3] for e in entries]
+            arena.qlen[:n] = [e[4] for e in entries]
+            m, stop = arena.admit(n, _b.params_c(self._sel), self.capacity_bytes, self.used_bytes,
+                                  p.model.max_context_tokens)
+            cfg_all = arena.configs[: min(m + 1, n)].copy()
             if m:
-                m_dev = configs[:m]
-                plans = _mem.plans_from_device(*_b.plan_calls(m_dev, ql[:m], self._sel, p.model.max_context_tokens),
-                                               call_cls=k.LlmCall, plan_cls=k.CallPlan, kind_enum=k.CallKind)
-                infos = _b.from_device(info[:m], _lib.ADMIT_INFO_DTYPE)
+                plans = _mem.plans_from_host(*arena.plan_calls(m, _b.params_c(self._sel), p.model.max_context_tokens),
+                                             call_cls=k.LlmCall, plan_cls=k.CallPlan, kind_enum=k.CallKind)
+                infos = arena.info[:m].copy()
             for j in range(m):
                 pending = self.waiting[0]
                 rec = cfg_all[j]
@@ -331,6 +345,8 @@ class Scheduler:
                 self._packed.pop(id(pending), None)
                 admissions.append(adm)
             if stop == _lib.RS_ADMIT_DRAINED:
+                if pack_error is not None:
+                    continue  # the unpackable entry is now the head: the next pass raises its error
                 chunk *= 2
                 continue
             if stop == _lib.RS_ADMIT_BLOCKED:
@@ -362,22 +378,9 @@ class Scheduler:
         raise OverflowError(f"KV byte arithmetic exceeds int64 for query {q.id}")
 
     def _overflow_message(self, qlen: int, cfg) -> str:
-        """The message of the first failing _check_context (memory.py:81-86,
-        :117-145) for this config."""
         p = self.params
-        C, T, O, ctx = p.meta.chunk_size, p.template_tokens, p.out_budget, p.model.max_context_tokens
-        n, m = cfg.num_chunks, cfg.synthesis_method.value
-        if m == "stuff":
-            checks = [("stuff call", qlen + n * C + T, O)]
-        elif m == "map_rerank":
-            checks = [("rerank call", qlen + C + T, O)]
-        else:
-            il = cfg.intermediate_length
-            checks = [("mapper call", qlen + C + T, il), ("reducer call", qlen + n * il + T, O)]
-        for label, prompt, out in checks:
-            if prompt + out > ctx:
-                return f"{label} needs {prompt + out} tokens, context window is {ctx}"
-        return "context window exceeded"
+        return _mem.context_overflow_message(qlen, cfg, p.meta.chunk_size, p.template_tokens, p.out_budget,
+                                             p.model.max_context_tokens)
 
     def step(self, now: float):
         """One admission round (scheduler.py:397-410): the backlog, then — if

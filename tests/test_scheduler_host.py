@@ -74,11 +74,53 @@ def fake_plan_calls(configs, qlen, params, max_context_tokens, stream=None):
             torch.tensor(totals, dtype=torch.int64), torch.tensor(status, dtype=torch.uint8))
 
 
+class FakeArena:
+    """scalar.AdmitArena's interface over host numpy arrays, filled by the
+    oracle's restatement of the two kernels instead of the GPU."""
+
+    def __init__(self):
+        self.cap = 0
+        self.ensure(32)
+
+    def ensure(self, n):
+        if n <= self.cap:
+            return
+        self.cap = max(n, 2 * self.cap)
+        self.spaces = np.zeros((self.cap, 16), np.uint8)
+        self.profiles = np.zeros((self.cap, 16), np.uint8)
+        self.hasprof = np.zeros(self.cap, np.uint8)
+        self.qlen = np.zeros(self.cap, np.int32)
+        self.configs = np.zeros(self.cap, _lib.CONFIG_DTYPE)
+        self.info = np.zeros(self.cap, _lib.ADMIT_INFO_DTYPE)
+
+    def admit(self, n, params_c, capacity, used, max_ctx):
+        p = self._params(params_c)
+        cfg, info, res = fake_admit_fifo(torch.from_numpy(self.spaces[:n]), torch.from_numpy(self.profiles[:n]),
+                                         torch.from_numpy(self.qlen[:n]), p, capacity_bytes=capacity,
+                                         used_bytes=used, max_context_tokens=max_ctx,
+                                         has_profile=torch.from_numpy(self.hasprof[:n]))
+        self.configs[:n] = cfg.numpy().reshape(-1).view(_lib.CONFIG_DTYPE)
+        self.info[:n] = info.numpy().reshape(-1).view(_lib.ADMIT_INFO_DTYPE)
+        r = res.numpy().view(_lib.ADMIT_RESULT_DTYPE)[0]
+        return int(r["admitted"]), int(r["stop"])
+
+    def plan_calls(self, m, params_c, max_ctx):
+        cfg = torch.from_numpy(self.configs[:m].view(np.uint8).reshape(m, 16))
+        off, calls, tot, st = fake_plan_calls(cfg, torch.from_numpy(self.qlen[:m]), self._params(params_c), max_ctx)
+        rec = calls.numpy().reshape(-1).view(_lib.CALL_DTYPE) if calls.numel() else np.zeros(0, _lib.CALL_DTYPE)
+        return off.numpy(), rec, tot.numpy(), st.numpy()
+
+    @staticmethod
+    def _params(c):
+        from paper_2412_10543_b200 import batch
+
+        return batch.SelectParams(c.per_token_bytes, c.chunk_size, c.out_budget, c.template_tokens, c.max_chunks,
+                                  c.chunk_step, c.interlen_step, bool(c.allow_fallback))
+
+
 @pytest.fixture()
 def oracle_backed(monkeypatch):
-    monkeypatch.setattr(S._b, "admit_fifo", fake_admit_fifo)
-    monkeypatch.setattr(S._b, "plan_calls", fake_plan_calls)
-    monkeypatch.setattr(S.Scheduler, "_device", lambda self: torch.device("cpu"))
+    monkeypatch.setattr(S.Scheduler, "_arena", lambda self: self.__dict__.setdefault("_fake_arena", FakeArena()))
 
 
 @pytest.mark.parametrize("rec", T.TRACES, ids=[r["name"] for r in T.TRACES])
