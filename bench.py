@@ -656,6 +656,8 @@ def main():
         if exchange == "peer":
             peer.close()
         dist.destroy_process_group()
+    if parity.get("peer_exchange_timeouts"):
+        sys.exit("peer exchange timed out inside the timed region: the line above is invalid")
 
 
 def gpu_side_parity(cfg, index, queries, D_full, I_full, data, dev):

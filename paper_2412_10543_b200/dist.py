@@ -163,6 +163,15 @@ class PeerExchange:
         self.scatter(keys, nq, epoch, stream)
         return self.merge_slice(nq, k, epoch, keep, stream)
 
+    def check(self) -> None:
+        """Raise if some merge of this exchange timed out waiting for a peer
+        (then its rows were merged from a stale buffer).  Synchronous: call it
+        at batch boundaries, or pass ``validate=True`` to
+        ``sharded_retrieve_select``."""
+        if self.error():
+            raise RuntimeError(f"peer exchange rank {self.rank}: a merge timed out after {self.timeout_ms} ms "
+                               "waiting for a peer's rows (results of that batch are invalid)")
+
     def error(self, clear: bool = False) -> int:
         """1 if some merge timed out waiting for a peer (synchronous read)."""
         out = ctypes.c_int32()
@@ -183,7 +192,8 @@ class PeerExchange:
 
 
 def sharded_retrieve_select(ops: ShardOps, queries, profiles, qlen, free_bytes, k: int, *, group=None,
-                            exchange: str = "all_to_all", peer: PeerExchange | None = None):
+                            exchange: str = "all_to_all", peer: PeerExchange | None = None,
+                            validate: bool = False):
     """One batch through the sharded path on this rank.  All inputs are the
     full batch (replicated); returns (q0, q1, configs, D, I) for this rank's
     query slice.
@@ -194,7 +204,9 @@ def sharded_retrieve_select(ops: ShardOps, queries, profiles, qlen, free_bytes, 
     receives every rank's full key matrix (P x more traffic).  ``"peer"``:
     the same traffic as all_to_all through ``peer`` (a ``PeerExchange``),
     stored by the library's kernels over NVLink, merged in the waiting
-    kernel."""
+    kernel.  ``validate=True`` (peer only) synchronises after the merge and
+    raises if it timed out waiting for a peer (``PeerExchange.check``); else
+    check ``peer.error()`` at batch boundaries."""
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     nq = queries.shape[0]
@@ -210,6 +222,8 @@ def sharded_retrieve_select(ops: ShardOps, queries, profiles, qlen, free_bytes, 
         spaces = ops.gate(profiles)
         configs = ops.select(spaces[q0:q1], profiles[q0:q1], qlen[q0:q1], free_bytes[q0:q1])
         D, I = peer.merge_slice(nq, k, epoch, keep=configs)
+        if validate:
+            peer.check()
         return q0, q1, configs, D, I
     keys = ops.search_keys(queries, k).contiguous()                     # [nq, k] local shard
     if exchange == "all_to_all":

@@ -48,16 +48,19 @@ def _all_inputs():
     return corpus, queries, prof, qlen, free
 
 
-def _worker(rank, world, port, exchange, q, nq):
+def _worker(rank, world, port, exchange, q, nq, multi_device=False):
     import torch.distributed as dist
 
     from paper_2412_10543_b200 import IndexFlatL2, batch
     from paper_2412_10543_b200 import dist as rdist
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
-    torch.cuda.set_device(0)
-    dev = torch.device("cuda", 0)
+    # multi_device: the measured configuration — one GPU per rank over NCCL
+    # (the peer exchange then stores over NVLink into the other GPUs' regions)
+    devi = rank if multi_device else 0
+    torch.cuda.set_device(devi)
+    dist.init_process_group("nccl" if multi_device else "gloo", rank=rank, world_size=world)
+    dev = torch.device("cuda", devi)
     corpus, queries, prof, qlen, free = _inputs(nq)
     r0, r1 = rdist.shard_range(N, rank, world)
     ix = IndexFlatL2(D, capacity=r1 - r0, id_base=r0)
@@ -88,13 +91,28 @@ def _iters(exchange):
 @pytest.mark.parametrize("world,exchange,nq", [(2, "all_to_all", NQ), (3, "all_to_all", NQ), (2, "all_gather", NQ),
                                                (2, "peer", NQ), (3, "peer", NQ), (3, "peer", 2)])
 def test_multirank_sharded_path_equals_single_index(world, exchange, nq):
+    _run_and_check(world, exchange, nq, multi_device=False)
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("world,exchange", [(2, "peer"), (2, "all_to_all"), (2, "all_gather"), (4, "peer"),
+                                            (8, "peer"), (8, "all_gather")])
+def test_multidevice_nccl_sharded_path_equals_single_index(world, exchange):
+    """Runs by itself on the first box with >= world GPUs: one rank per GPU
+    over NCCL, the peer exchange's stores crossing NVLink/NVSwitch."""
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs, {torch.cuda.device_count()} visible")
+    _run_and_check(world, exchange, NQ, multi_device=True)
+
+
+def _run_and_check(world, exchange, nq, multi_device):
     from paper_2412_10543_b200 import IndexFlatL2, batch
     from paper_2412_10543_b200.pipeline import RetrieveSelect
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, exchange, q, nq)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, exchange, q, nq, multi_device)) for r in range(world)]
     for p in procs:
         p.start()
     res = sorted([q.get(timeout=500) for _ in range(world)], key=lambda t: t[0])
