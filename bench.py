@@ -434,6 +434,8 @@ def main():
                     help="key exchange of the sharded path (N>1): the library's NVLink peer-memory kernels "
                          "(default) or NCCL")
     ap.add_argument("--corpus-rows", type=int, default=None, help="override the corpus size (debug)")
+    ap.add_argument("--segment-rows", type=int, default=0,
+                    help="tuning knob: corpus rows per segment of the pair kernel's schedule (0 = planner)")
     ap.add_argument("--queries", type=int, default=None,
                     help="override the queries per step (e.g. 128: the HBM-bound small-batch regime)")
     args = ap.parse_args()
@@ -467,6 +469,8 @@ def main():
     # ---- corpus shard (global rows [r0, r1), ids r0..), generated on the device ----
     r0, r1 = rdist.shard_range(n, rank, world)
     index = IndexFlatL2(d, dtype=tdtype, capacity=r1 - r0, device=dev, id_base=r0)
+    if args.segment_rows:
+        index.set_segment_rows(args.segment_rows)
     for a in range(r0, r1, 1 << 20):
         index.add(synth.corpus_rows(a, min(r1, a + (1 << 20)), d, SEED, tdtype, dev, args.data))
     queries_host = synth.make_queries(nq, n, d, SEED, tdtype, args.data)  # identical on every rank
@@ -598,13 +602,21 @@ def main():
     sustained = ms_max > 100.0
     tf_ref = tf_sust if sustained else tf_burst
     tc_peak = tf_ref / 2.0 if tf32 else tf_ref
+    tf32_src = "measured bf16 / 2"
+    if tf32:  # the measured tf32 GEMM peak (tools/measure_fp32_peaks.py), else bf16 / 2
+        try:
+            fp = json.load(open(os.path.join(ROOT, "profiles", "fp32_peaks.json")))
+            tc_peak = fp["tf32_tflops_sustained" if sustained else "tf32_tflops"]
+            tf32_src = "measured cuBLAS tf32 GEMM (profiles/fp32_peaks.json)"
+        except (OSError, KeyError, ValueError):
+            pass
     t_tensor = tc_flops / (tc_peak * 1e12)
     t_hbm = bytes_alg / (hbm * 1e9)
     if algo == "tcgen05" and t_tensor >= t_hbm:
         roof = {"bound": "tensor", "achieved": tc_flops / (kernel_ms * 1e-3) / 1e12, "peak": tc_peak,
                 "unit": "TFLOP/s"}
         if tf32:
-            roof["note"] = "tf32 MMA flops (3 per fp32 product); peak = measured bf16 / 2"
+            roof["note"] = f"tf32 MMA flops (3 per fp32 product); peak = {tf32_src}"
     else:
         roof = {"bound": "hbm", "achieved": bytes_alg / (kernel_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s"}
     roof["frac"] = roof["achieved"] / roof["peak"]
@@ -617,7 +629,7 @@ def main():
     roof["kernel_ms"] = kernel_ms
     roof["kernel_share_of_step"] = kernel_ms / (ms_max / args.steps)
     roof["peak_source"] = f"{peak_src}, " + (
-        ("sustained" if sustained else "burst") + (" bf16 / 2 (tf32)" if tf32 else " bf16")
+        ("sustained" if sustained else "burst") + (f" tf32 ({tf32_src})" if tf32 else " bf16")
         if roof["bound"] == "tensor" else "copy")
     prof_path = os.path.join(ROOT, "profiles", f"ncu_{args.workload}_n{world}.json")
     if os.path.exists(prof_path) and not (args.queries or args.corpus_rows) and args.data == "iso":

@@ -331,6 +331,11 @@ int rs_index_set_algo(rs_index* index, int32_t algo);
  * starts its corpus-segment walk bias*(qt+1) tiles past the segment frontier,
  * so the out-of-id-order (wrap-around) top-k path runs deterministically. */
 int rs_index_set_walk_bias(rs_index* index, int32_t bias);
+/* Tuning knob of the CTA-pair kernel's schedule: corpus rows per segment
+ * (rounded down to whole 256-row tiles; 0 = the planner's choice).  Shorter
+ * segments keep a segment L2-resident for units that join it late, at the cost
+ * of more partial lists to merge. */
+int rs_index_set_segment_rows(rs_index* index, int32_t rows);
 /* Preallocate the search workspace for up to nq_max queries of k results. */
 int rs_index_reserve(rs_index* index, int64_t nq_max, int32_t k);
 /* Search: queries device [nq, dim] of the index dtype; D device [nq,k] fp32,

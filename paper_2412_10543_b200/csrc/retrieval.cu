@@ -695,6 +695,7 @@ using rs::DeviceGuard;
 struct rs_index {
   int32_t dim = 0, dtype = 0, device = 0, algo = RS_ALGO_AUTO;
   int32_t walk_bias = 0;  // test hook (rs_index_set_walk_bias)
+  int32_t seg_rows_override = 0;  // tuning knob (rs_index_set_segment_rows): 0 = the planner's choice
   int64_t capacity = 0, ntotal = 0;
   void* data = nullptr;
   float* norms = nullptr;
@@ -772,6 +773,14 @@ rs::SearchPlan make_plan(const rs_index* ix, int algo, int64_t nq, int64_t n, in
     const bool small = pair_small(nq);
     SearchPlan p = plan_search(nq, n, pair_tile_rows(small) * kPairGroup, kTcBN, sms / (2 * kPairGroup),
                                eq_row_bytes, /*share_l2=*/false);
+    if (ix->seg_rows_override > 0) {  // fixed segment length (rounded to whole tiles)
+      const int64_t tps = std::max<int64_t>(1, ix->seg_rows_override / kTcBN);
+      const int64_t nt = ceil_div(std::max<int64_t>(n, 1), kTcBN);
+      p.segments = int32_t(std::min<int64_t>(ceil_div(nt, std::min(tps, nt)), kMaxSegments));
+      p.seg_rows = ceil_div(nt, p.segments) * kTcBN;
+      p.segments = int32_t(ceil_div(nt * kTcBN, p.seg_rows));
+      p.ctas = int32_t(std::min<int64_t>(int64_t(p.qtiles) * p.segments, sms / (2 * kPairGroup)));
+    }
     p.lists_per_seg = small ? 2 : kPairEpiGroups;
     return p;
   }
@@ -989,6 +998,12 @@ extern "C" int rs_index_data(const rs_index* ix, const void** emb, const float**
   RS_REQUIRE(ix != nullptr, "index is NULL");
   if (emb) *emb = ix->data;
   if (norms) *norms = ix->norms;
+  return RS_OK;
+}
+
+extern "C" int rs_index_set_segment_rows(rs_index* ix, int32_t rows) {
+  RS_REQUIRE(ix != nullptr && rows >= 0, "bad arguments");
+  ix->seg_rows_override = rows;
   return RS_OK;
 }
 

@@ -81,6 +81,10 @@ class IndexFlatL2:
     def set_algo(self, algo: str) -> None:
         _lib.check(self._lib.rs_index_set_algo(self._h, ALGOS[algo]))
 
+    def set_segment_rows(self, rows: int) -> None:
+        """Tuning knob: corpus rows per segment of the CTA-pair schedule (0 = auto)."""
+        _lib.check(self._lib.rs_index_set_segment_rows(self._h, int(rows)))
+
     def set_walk_bias(self, bias: int) -> None:
         """Test hook: start every pair-kernel unit past its segment frontier
         (exercises the wrap-around, out-of-id-order top-k path)."""
