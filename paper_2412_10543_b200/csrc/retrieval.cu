@@ -29,9 +29,18 @@ __device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 v) {
 }
 
 // ---- squared norms: one warp per row, fp32 accumulate ---------------------
+// For an fp32 matrix headed for the 3xTF32 kernel the same pass also writes
+// the tf32 residuals lo = x - trunc_tf32(x) (the tensor core reads an fp32
+// operand as tf32 by dropping the low 13 mantissa bits; the residual is exact
+// in fp32), so the split costs no extra read of x.
+__device__ __forceinline__ float tf32_residual(float v) {
+  return v - __uint_as_float(__float_as_uint(v) & 0xffffe000u);
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) row_norms_kernel(const T* __restrict__ x, int64_t n, int dim,
-                                                        float* __restrict__ out, unsigned int* __restrict__ max_bits) {
+                                                        float* __restrict__ out, unsigned int* __restrict__ max_bits,
+                                                        float* __restrict__ lo) {
   const int lane = threadIdx.x & 31;
   float mx = 0.0f;
   for (int64_t r = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r < n;
@@ -41,6 +50,9 @@ __global__ void __launch_bounds__(256) row_norms_kernel(const T* __restrict__ x,
     for (int i = lane; i < dim; i += 32) {
       const float v = to_f(row[i]);
       s = fmaf(v, v, s);
+      if constexpr (sizeof(T) == 4) {
+        if (lo) lo[r * dim + i] = tf32_residual(v);
+      }
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
@@ -276,6 +288,55 @@ __device__ __forceinline__ void peer_wait(const PeerWait& pw) {
   __syncthreads();
 }
 
+// One query's 64-list tournament (the warp): emits the first `limit` keys of
+// the merged order through emit(j, key) (lane 0) and returns how many it
+// emitted (fewer when every list runs out).
+template <bool WAIT, typename Emit>
+__device__ __forceinline__ int warp_merge64(const uint64_t* base, int nlists, int k_in, int64_t list_stride,
+                                            int limit, Emit emit) {
+  // named registers, not arrays: a [tb]-indexed array would live in local memory
+  const int lane = threadIdx.x & 31;
+  const uint64_t* lp0 = base + int64_t(lane) * list_stride;
+  const uint64_t* lp1 = base + int64_t(lane + 32) * list_stride;
+  uint64_t cur0 = lane < nlists ? merge_key<WAIT>(lp0) : kEmptyKey;
+  uint64_t nxt0 = (lane < nlists && k_in > 1) ? merge_key<WAIT>(lp0 + 1) : kEmptyKey;
+  uint64_t cur1 = lane + 32 < nlists ? merge_key<WAIT>(lp1) : kEmptyKey;
+  uint64_t nxt1 = (lane + 32 < nlists && k_in > 1) ? merge_key<WAIT>(lp1 + 1) : kEmptyKey;
+  int head0 = 0, head1 = 0;
+  int j = 0;
+  for (; j < limit; ++j) {
+    const bool tb = cur1 < cur0;
+    const uint64_t mine = tb ? cur1 : cur0;
+    const uint32_t hi = uint32_t(mine >> 32);
+    const uint32_t dmin = __reduce_min_sync(0xffffffffu, hi);
+    const uint32_t idmin = __reduce_min_sync(0xffffffffu, hi == dmin ? uint32_t(mine) : 0xffffffffu);
+    const uint64_t v = (uint64_t(dmin) << 32) | idmin;
+    if (v == kEmptyKey) break;  // every list is exhausted
+    const unsigned win = __ballot_sync(0xffffffffu, mine == v);
+    if (lane == 0) emit(j, v);
+    if (lane == __ffs(win) - 1) {
+      // advance the winning list: the prefetched key moves up, the next one is requested
+      if (tb) {
+        cur1 = nxt1;
+        ++head1;
+        nxt1 = head1 + 1 < k_in ? merge_key<WAIT>(lp1 + head1 + 1) : kEmptyKey;
+      } else {
+        cur0 = nxt0;
+        ++head0;
+        nxt0 = head0 + 1 < k_in ? merge_key<WAIT>(lp0 + head0 + 1) : kEmptyKey;
+      }
+    }
+  }
+  return j;
+}
+
+__device__ __forceinline__ int keep_limit(const rs_config* keep, int64_t q, int k) {
+  if (!keep) return k;
+  const rs_config c = keep[q];
+  const int limit = (c.status == RS_SELECT_BEST_FIT || c.status == RS_SELECT_FALLBACK) ? c.num_chunks : 0;
+  return limit > k ? k : limit;
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(kMergeWarps * 32) merge_topk64_kernel(
     const uint64_t* keys, int64_t nq, int nlists, int k_in, int64_t list_stride, int64_t q_stride,
@@ -285,46 +346,13 @@ __global__ void __launch_bounds__(kMergeWarps * 32) merge_topk64_kernel(
   if constexpr (WAIT) peer_wait(pa.wait);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int64_t q = int64_t(blockIdx.x) * kMergeWarps + w; q < nq; q += int64_t(gridDim.x) * kMergeWarps) {
-    const uint64_t* base = keys + q * q_stride;
     uint64_t* orow = MODE == kMergeScatter ? peer_row(pa.ex, nq, q, pa.epoch) : keys_out ? keys_out + q * k : nullptr;
-    uint64_t cur[2], nxt[2];
-    int head[2] = {0, 0};
-#pragma unroll
-    for (int t = 0; t < 2; ++t) {
-      const int l = lane + 32 * t;
-      const uint64_t* lp = base + int64_t(l) * list_stride;
-      cur[t] = l < nlists ? merge_key<WAIT>(lp) : kEmptyKey;
-      nxt[t] = (l < nlists && k_in > 1) ? merge_key<WAIT>(lp + 1) : kEmptyKey;
-    }
-    int limit = k;
-    if (keep) {
-      const rs_config c = keep[q];
-      limit = (c.status == RS_SELECT_BEST_FIT || c.status == RS_SELECT_FALLBACK) ? c.num_chunks : 0;
-      if (limit > k) limit = k;
-    }
-    int j = 0;
-    for (; j < limit; ++j) {
-      const int tb = cur[1] < cur[0] ? 1 : 0;
-      const uint64_t mine = cur[tb];
-      const uint32_t hi = uint32_t(mine >> 32);
-      const uint32_t dmin = __reduce_min_sync(0xffffffffu, hi);
-      const uint32_t idmin = __reduce_min_sync(0xffffffffu, hi == dmin ? uint32_t(mine) : 0xffffffffu);
-      const uint64_t v = (uint64_t(dmin) << 32) | idmin;
-      if (v == kEmptyKey) break;  // every list is exhausted
-      const unsigned win = __ballot_sync(0xffffffffu, mine == v);
-      if (lane == 0) {
-        if (orow) orow[j] = v;
-        if (D) D[q * k + j] = key_dist(v);
-        if (I) I[q * k + j] = int64_t(uint32_t(v));
-      }
-      if (lane == __ffs(win) - 1) {
-        // advance the winning list: the prefetched key moves up, the next one is requested
-        const int h = ++head[tb];
-        cur[tb] = nxt[tb];
-        const int l = lane + 32 * tb;
-        nxt[tb] = h + 1 < k_in ? merge_key<WAIT>(base + int64_t(l) * list_stride + h + 1) : kEmptyKey;
-      }
-    }
+    const int j = warp_merge64<WAIT>(keys + q * q_stride, nlists, k_in, list_stride, keep_limit(keep, q, k),
+                                     [&](int jj, uint64_t v) {
+                                       if (orow) orow[jj] = v;
+                                       if (D) D[q * k + jj] = key_dist(v);
+                                       if (I) I[q * k + jj] = int64_t(uint32_t(v));
+                                     });
     for (int jj = j + lane; jj < k; jj += 32) {  // padding past the limit / the lists
       if (orow) orow[jj] = kEmptyKey;
       if (D) D[q * k + jj] = __int_as_float(0x7f800000);
@@ -396,116 +424,123 @@ int launch_merge(const uint64_t* keys, int64_t nq, int nlists, int k_in, int64_t
 // each MMA's products into the fp32 TMEM accumulator with truncation, so at
 // d = 768 a near neighbour's dot (~0.9) drifts by ~1.4e-5 relative — above the
 // north star's 1e-5 fp32 tolerance.  The fused kernel therefore keeps
-// kc = k + kRefineExtra candidates per query, and the two kernels below recompute
+// kc = k + kRefineExtra candidates per query, and the kernel below recomputes
 // their distances with fp32 FMAs on CUDA cores (lanes over the dimension,
-// float4 loads, warp reduction; error ~1e-7), ranks them by (distance, id)
+// float4 loads, in-group reduction; error ~1e-7), ranks them by (distance, id)
 // and emits the top k — the FAISS semantics the oracle checks, at a cost of
 // nq * kc * d FMAs (negligible next to the GEMM).
-// Scoring: one warp per (query, 8 candidates); its four 8-lane groups each
-// hold one candidate row in flight (float4 loads spread over the group,
-// three in-group shuffles), two rows per group.  Thousands of independent
-// warps keep the random row gathers in flight — a warp per query left the
-// SMs ~12% occupied and latency-bound on these loads.
-constexpr int kRefinePerWarp = 8;
-__global__ void __launch_bounds__(256) refine_score_kernel(const uint64_t* __restrict__ cand, int kc,
-                                                           const float* __restrict__ Q, const float* __restrict__ qn,
-                                                           const float* __restrict__ C, const float* __restrict__ cn,
-                                                           int64_t nq, int dim, int64_t id_base,
-                                                           uint64_t* __restrict__ exact) {
-  const int lane = threadIdx.x & 31;
-  const int chunks = (kc + kRefinePerWarp - 1) / kRefinePerWarp;
-  const int64_t wid = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  if (wid >= nq * chunks) return;
-  const int64_t q = wid / chunks;
-  const int c0 = int(wid - q * chunks) * kRefinePerWarp;
+//
+// One CTA per query, three phases, one launch (the merge of the per-segment
+// lists, the scoring and the ranking were three kernels in round 1):
+//  1. warp 0 merges the query's sorted tf32 lists into the kc smallest keys;
+//  2. all 8 warps score them: each 8-lane group holds one candidate row in
+//     flight (float4 loads spread over the group, three in-group shuffles), so
+//     32 random row gathers per CTA overlap;
+//  3. warp 0 ranks the exact keys (lane j owns candidates j and j + 32) and
+//     writes the top k with the keep limit.  Keys are unique except padding.
+constexpr int kRefineWarps = 8;
+__global__ void __launch_bounds__(kRefineWarps * 32) refine_fp32_kernel(
+    const uint64_t* __restrict__ lists, int nlists, int k_in, int64_t list_stride, int64_t q_stride, int kc,
+    const float* __restrict__ Q, const float* __restrict__ qn, const float* __restrict__ C,
+    const float* __restrict__ cn, int64_t nq, int dim, int64_t id_base, int k, const rs_config* __restrict__ keep,
+    float* __restrict__ D, int64_t* __restrict__ I, uint64_t* __restrict__ keys_out) {
+  __shared__ uint64_t cand[64], exact[64];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int grp = lane >> 3, gl = lane & 7;
   const unsigned gmask = 0xFFu << (grp * 8);
-  const float4* qv = reinterpret_cast<const float4*>(Q + q * dim);
   const int d4 = dim / 4;
-  const float qq = qn[q];
-  for (int j = c0 + grp; j < c0 + kRefinePerWarp && j < kc; j += 4) {
-    const uint64_t key = cand[q * kc + j];
-    uint64_t out = kEmptyKey;
-    if (key != kEmptyKey) {  // group-uniform
-      const int64_t row = int64_t(uint32_t(key)) - id_base;
-      const float4* cv = reinterpret_cast<const float4*>(C + row * dim);
-      float acc = 0.0f;
-      for (int i = gl; i < d4; i += 8) {
-        const float4 a = qv[i], b = cv[i];
-        acc = fmaf(a.x, b.x, acc);
-        acc = fmaf(a.y, b.y, acc);
-        acc = fmaf(a.z, b.z, acc);
-        acc = fmaf(a.w, b.w, acc);
+  for (int64_t q = blockIdx.x; q < nq; q += gridDim.x) {
+    if (w == 0) {  // 1. candidates
+      const int got = warp_merge64<false>(lists + q * q_stride, nlists, k_in, list_stride, kc,
+                                          [&](int j, uint64_t v) { cand[j] = v; });
+      for (int j = got + lane; j < 64; j += 32) cand[j] = kEmptyKey;
+      for (int j = kc + lane; j < 64; j += 32) exact[j] = kEmptyKey;
+    }
+    __syncthreads();
+    const float4* qv = reinterpret_cast<const float4*>(Q + q * dim);
+    const float qq = qn[q];
+    for (int j = w * 4 + grp; j < kc; j += kRefineWarps * 4) {  // 2. exact distances
+      const uint64_t key = cand[j];
+      uint64_t out = kEmptyKey;
+      if (key != kEmptyKey) {  // group-uniform
+        const int64_t row = int64_t(uint32_t(key)) - id_base;
+        const float4* cv = reinterpret_cast<const float4*>(C + row * dim);
+        float acc = 0.0f;
+        for (int i = gl; i < d4; i += 8) {
+          const float4 a = qv[i], b = cv[i];
+          acc = fmaf(a.x, b.x, acc);
+          acc = fmaf(a.y, b.y, acc);
+          acc = fmaf(a.z, b.z, acc);
+          acc = fmaf(a.w, b.w, acc);
+        }
+#pragma unroll
+        for (int off = 4; off > 0; off >>= 1) acc += __shfl_xor_sync(gmask, acc, off);
+        float dist = fmaf(-2.0f, acc, qq + cn[row]);
+        dist = dist > 0.0f ? dist : 0.0f;  // FAISS clamps round-off at 0 (and NaN -> 0)
+        out = (uint64_t(__float_as_uint(dist)) << 32) | uint32_t(key);
+      }
+      if (gl == 0) exact[j] = out;
+    }
+    __syncthreads();
+    if (w == 0) {  // 3. rank
+      const uint64_t mine[2] = {exact[lane], exact[lane + 32]};
+      const int limit = keep_limit(keep, q, k);
+      int rank[2] = {0, 0};
+      for (int j = 0; j < 64; ++j) {
+        const uint64_t o = exact[j];
+#pragma unroll
+        for (int t = 0; t < 2; ++t) rank[t] += (o < mine[t] || (o == mine[t] && j < lane + 32 * t)) ? 1 : 0;
       }
 #pragma unroll
-      for (int off = 4; off > 0; off >>= 1) acc += __shfl_xor_sync(gmask, acc, off);
-      float dist = fmaf(-2.0f, acc, qq + cn[row]);
-      dist = dist > 0.0f ? dist : 0.0f;  // FAISS clamps round-off at 0 (and NaN -> 0)
-      out = (uint64_t(__float_as_uint(dist)) << 32) | uint32_t(key);
+      for (int t = 0; t < 2; ++t) {
+        const int r = rank[t];
+        if (r < k) {
+          const bool real = mine[t] != kEmptyKey && r < limit;
+          if (keys_out) keys_out[q * k + r] = real ? mine[t] : kEmptyKey;
+          if (D) D[q * k + r] = real ? key_dist(mine[t]) : __int_as_float(0x7f800000);
+          if (I) I[q * k + r] = real ? int64_t(uint32_t(mine[t])) : int64_t(-1);
+        }
+      }
     }
-    if (gl == 0) exact[q * kc + j] = out;
+    __syncthreads();
   }
 }
 
-// Ranking: one warp per query; lane j owns candidates j and j + 32 (kc <= 40
-// < 64); ranks by (exact distance, id) and writes the top k with the keep
-// limit.  Keys are unique except the padding.
-__global__ void __launch_bounds__(256) refine_rank_kernel(const uint64_t* __restrict__ exact, int kc, int64_t nq,
-                                                          int k, const rs_config* __restrict__ keep,
-                                                          float* __restrict__ D, int64_t* __restrict__ I,
-                                                          uint64_t* __restrict__ keys_out) {
-  const int lane = threadIdx.x & 31;
-  const int64_t q = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  if (q >= nq) return;
-  uint64_t mine[2];
-  mine[0] = lane < kc ? exact[q * kc + lane] : kEmptyKey;
-  mine[1] = lane + 32 < kc ? exact[q * kc + lane + 32] : kEmptyKey;
-  int limit = k;
-  if (keep) {
-    const rs_config c = keep[q];
-    limit = (c.status == RS_SELECT_BEST_FIT || c.status == RS_SELECT_FALLBACK) ? c.num_chunks : 0;
-    if (limit > k) limit = k;
-  }
-  int rank[2] = {0, 0};
-  for (int j = 0; j < 64; ++j) {
-    const uint64_t o = shfl_u64(mine[j >> 5], j & 31);
-#pragma unroll
-    for (int t = 0; t < 2; ++t) rank[t] += (o < mine[t] || (o == mine[t] && j < lane + 32 * t)) ? 1 : 0;
-  }
-#pragma unroll
-  for (int t = 0; t < 2; ++t) {
-    const int r = rank[t];
-    if (r < k) {
-      const bool real = mine[t] != kEmptyKey && r < limit;
-      if (keys_out) keys_out[q * k + r] = real ? mine[t] : kEmptyKey;
-      if (D) D[q * k + r] = real ? key_dist(mine[t]) : __int_as_float(0x7f800000);
-      if (I) I[q * k + r] = real ? int64_t(uint32_t(mine[t])) : int64_t(-1);
-    }
-  }
-}
-
-int launch_refine_fp32(const uint64_t* cand, uint64_t* exact, int kc, const float* Q, const float* qn,
-                       const float* C, const float* cn, int64_t nq, int dim, int64_t id_base, int k,
-                       const rs_config* keep, float* D, int64_t* I, uint64_t* keys_out, cudaStream_t st) {
+// lists: the fused search's per-segment tf32 lists (nlists sorted lists of
+// k_in keys per query); more than 64 lists are first merged to one list of kc
+// (into `scratch`, nq * kc keys).
+int launch_refine_fp32(const uint64_t* lists, int nlists, int k_in, int64_t list_stride, int64_t q_stride,
+                       uint64_t* scratch, int kc, const float* Q, const float* qn, const float* C, const float* cn,
+                       int64_t nq, int dim, int64_t id_base, int k, const rs_config* keep, float* D, int64_t* I,
+                       uint64_t* keys_out, int sms, cudaStream_t st) {
   RS_REQUIRE(kc >= k && kc <= 64 && dim % 4 == 0, "refine: bad shape");
-  const int64_t warps = nq * ((kc + kRefinePerWarp - 1) / kRefinePerWarp);
-  refine_score_kernel<<<(unsigned)ceil_div(warps * 32, 256), 256, 0, st>>>(cand, kc, Q, qn, C, cn, nq, dim, id_base,
-                                                                          exact);
-  RS_CHECK_LAUNCH("refine_score_kernel");
-  refine_rank_kernel<<<(unsigned)ceil_div(nq * 32, 256), 256, 0, st>>>(exact, kc, nq, k, keep, D, I, keys_out);
-  RS_CHECK_LAUNCH("refine_rank_kernel");
+  if (nlists > 64) {
+    int rc = launch_merge(lists, nq, nlists, k_in, list_stride, q_stride, kc, nullptr, nullptr, nullptr, scratch, st);
+    if (rc) return rc;
+    lists = scratch;
+    nlists = 1;
+    k_in = kc;
+    list_stride = kc;
+    q_stride = kc;
+  }
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(nq, int64_t(sms) * 8));
+  refine_fp32_kernel<<<(unsigned)blocks, kRefineWarps * 32, 0, st>>>(lists, nlists, k_in, list_stride, q_stride, kc,
+                                                                     Q, qn, C, cn, nq, dim, id_base, k, keep, D, I,
+                                                                     keys_out);
+  RS_CHECK_LAUNCH("refine_fp32_kernel");
   return RS_OK;
 }
 
 int launch_norms(const void* x, int64_t n, int dim, int dtype, float* out, cudaStream_t st,
-                 float* max_out = nullptr) {
+                 float* max_out, float* lo) {
   if (n <= 0) return RS_OK;
   const int64_t blocks = std::min<int64_t>(ceil_div(n * 32, 256), 148 * 64);
   unsigned int* mb = reinterpret_cast<unsigned int*>(max_out);
   if (dtype == RS_BF16)
-    row_norms_kernel<__nv_bfloat16><<<(unsigned)blocks, 256, 0, st>>>((const __nv_bfloat16*)x, n, dim, out, mb);
+    row_norms_kernel<__nv_bfloat16><<<(unsigned)blocks, 256, 0, st>>>((const __nv_bfloat16*)x, n, dim, out, mb,
+                                                                      nullptr);
   else
-    row_norms_kernel<float><<<(unsigned)blocks, 256, 0, st>>>((const float*)x, n, dim, out, mb);
+    row_norms_kernel<float><<<(unsigned)blocks, 256, 0, st>>>((const float*)x, n, dim, out, mb, lo);
   RS_CHECK_LAUNCH("row_norms_kernel");
   return RS_OK;
 }
@@ -589,30 +624,6 @@ int launch_merge_to_peers(const uint64_t* keys, int64_t nq, int nlists, int k_in
   merge_topk64_kernel<kMergeScatter><<<(unsigned)blocks, kMergeWarps * 32, 0, st>>>(
       keys, nq, nlists, k_in, list_stride, q_stride, ex.k, nullptr, nullptr, nullptr, nullptr, pa);
   RS_CHECK_LAUNCH("merge_topk64_kernel<scatter>");
-  return RS_OK;
-}
-
-// ---- 3xTF32 operand split ------------------------------------------------------
-__global__ void tf32_lo_kernel(const float4* __restrict__ x, int64_t n4, float4* __restrict__ lo) {
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += int64_t(gridDim.x) * blockDim.x) {
-    float4 v = x[i], r;
-    // the tensor core reads fp32 operands as tf32 by dropping the low 13
-    // mantissa bits; the residual below is exact in fp32
-    r.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xffffe000u);
-    r.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xffffe000u);
-    r.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xffffe000u);
-    r.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xffffe000u);
-    lo[i] = r;
-  }
-}
-
-int launch_tf32_lo(const float* x, int64_t count, float* lo, cudaStream_t st) {
-  if (count == 0) return RS_OK;
-  RS_REQUIRE(count % 4 == 0, "tf32 split needs a multiple of 4 elements");
-  const int64_t n4 = count / 4;
-  const unsigned blocks = unsigned(std::min<int64_t>(ceil_div(n4, 256), 148 * 16));
-  tf32_lo_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const float4*>(x), n4, reinterpret_cast<float4*>(lo));
-  RS_CHECK_LAUNCH("tf32_lo_kernel");
   return RS_OK;
 }
 
@@ -705,7 +716,7 @@ struct rs_index {
   float* lo = nullptr;        // fp32 index: [capacity, dim] tf32 residuals x - trunc_tf32(x) (3xTF32 path)
   float* qlo = nullptr;       // per-search query residuals [qlo_cap, dim]
   int64_t qlo_cap = 0;
-  uint64_t* cand = nullptr;   // fp32 path: merged 3xTF32 candidates [nq, kc] before the exact re-rank
+  uint64_t* cand = nullptr;   // fp32 path with > 64 lists: merged 3xTF32 candidates [nq, kc] before the re-rank
   size_t cand_cap = 0;        // bytes
   float* qnorm = nullptr;
   uint32_t* qtau = nullptr;   // pair kernel: per-query shared k-th distance (threshold sharing)
@@ -803,7 +814,9 @@ int run_partial(rs_index* ix, const void* queries, int64_t nq, int k, int64_t id
   const size_t part_bytes = size_t(nq) * plan.lists() * k * sizeof(uint64_t);
   int rc = ensure_ws(ix, nq, part_bytes);
   if (rc) return rc;
-  rc = launch_norms(queries, nq, ix->dim, ix->dtype, ix->qnorm, st);
+  // 3xTF32 (fp32 corpus on the tensor cores): the same pass splits the queries
+  const bool tf_split = ix->dtype == RS_F32 && algo == RS_ALGO_TCGEN05;
+  rc = launch_norms(queries, nq, ix->dim, ix->dtype, ix->qnorm, st, nullptr, tf_split ? ix->qlo : nullptr);
   if (rc) return rc;
   const int slot = ix->ev_next;
   if (ix->timing) {
@@ -824,9 +837,7 @@ int run_partial(rs_index* ix, const void* queries, int64_t nq, int k, int64_t id
     if (rc) return rc;
     rc = encode_kmajor_map(&tmc, ix->data, ix->ntotal, ix->dim, crows, ix->dtype);
     if (rc) return rc;
-    if (tf) {  // 3xTF32: the queries' residuals (the corpus's were made at add)
-      rc = launch_tf32_lo(static_cast<const float*>(queries), nq * ix->dim, ix->qlo, st);
-      if (rc) return rc;
+    if (tf) {  // 3xTF32: the residuals (the queries' from launch_norms above, the corpus's from add)
       rc = encode_kmajor_map(&tmql, ix->qlo, nq, ix->dim, qrows, RS_F32);
       if (rc) return rc;
       if (RS_TF32_STORED_LO) {
@@ -964,16 +975,13 @@ extern "C" int rs_index_add(rs_index* ix, const void* emb, int64_t n, void* stre
   RS_CHECK_CUDA(cudaMemcpyAsync((char*)ix->data + size_t(ix->ntotal) * row, emb, size_t(n) * row,
                                 cudaMemcpyDeviceToDevice, st),
                 "cudaMemcpyAsync(add)");
+  // + the 3xTF32 residuals of the new rows (fp32, dim % 4 == 0: the tcgen05 path exists)
   int rc = rs::launch_norms((char*)ix->data + size_t(ix->ntotal) * row, n, ix->dim, ix->dtype,
-                            ix->norms + ix->ntotal, st, ix->norm_max);
+                            ix->norms + ix->ntotal, st, ix->norm_max,
+                            ix->lo ? ix->lo + size_t(ix->ntotal) * ix->dim : nullptr);
   if (rc) return rc;
   rc = rs::launch_chunk_min(ix->norms, ix->ntotal, ix->ntotal + n, ix->cmin, st);
   if (rc) return rc;
-  if (ix->lo != nullptr) {  // 3xTF32 residuals of the new rows (fp32, dim % 4 == 0: the tcgen05 path exists)
-    const size_t off = size_t(ix->ntotal) * ix->dim;
-    rc = rs::launch_tf32_lo(static_cast<const float*>(ix->data) + off, n * ix->dim, ix->lo + off, st);
-    if (rc) return rc;
-  }
   ix->ntotal += n;
   return RS_OK;
 }
@@ -1075,19 +1083,19 @@ static int search_impl(rs_index* ix, const void* queries, int64_t nq, int32_t k,
     const int kc = k + kRefineExtra;  // <= kTcMaxK + kRefineExtra: the tf32 lists' capacity
     rc = run_partial(ix, queries, nq, kc, id_base, st, &plan, k);
     if (rc) return rc;
-    const size_t cb = 2 * size_t(nq) * kc * sizeof(uint64_t);  // merged candidates + their exact keys
-    if (cb > ix->cand_cap) {
-      if (ix->cand) cudaFree(ix->cand);
-      ix->cand = nullptr;
-      RS_CHECK_CUDA(cudaMalloc(&ix->cand, cb), "cudaMalloc(refine candidates)");
-      ix->cand_cap = cb;
+    if (plan.lists() > 64) {  // the candidate lists are merged to one list of kc first
+      const size_t cb = size_t(nq) * kc * sizeof(uint64_t);
+      if (cb > ix->cand_cap) {
+        if (ix->cand) cudaFree(ix->cand);
+        ix->cand = nullptr;
+        RS_CHECK_CUDA(cudaMalloc(&ix->cand, cb), "cudaMalloc(refine candidates)");
+        ix->cand_cap = cb;
+      }
     }
-    rc = launch_merge(ix->part, nq, plan.lists(), kc, kc, int64_t(plan.lists()) * kc, kc, nullptr, nullptr, nullptr,
-                      ix->cand, st);
-    if (rc) return rc;
-    return finish(launch_refine_fp32(ix->cand, ix->cand + size_t(nq) * kc, kc, static_cast<const float*>(queries),
-                                     ix->qnorm, static_cast<const float*>(ix->data), ix->norms, nq, ix->dim, id_base,
-                                     k, keep, D, I, keys, st));
+    return finish(launch_refine_fp32(ix->part, plan.lists(), kc, kc, int64_t(plan.lists()) * kc, ix->cand, kc,
+                                     static_cast<const float*>(queries), ix->qnorm,
+                                     static_cast<const float*>(ix->data), ix->norms, nq, ix->dim, id_base, k, keep,
+                                     D, I, keys, sm_count(ix->device), st));
   }
   rc = run_partial(ix, queries, nq, k, id_base, st, &plan);
   if (rc) return rc;
@@ -1132,5 +1140,5 @@ extern "C" int rs_merge_topk(const uint64_t* keys, int64_t nq, int32_t nlists, i
 extern "C" int rs_row_norms(const void* x, int64_t n, int32_t dim, int32_t dtype, float* out, void* stream) {
   RS_REQUIRE(n >= 0 && dim >= 1 && (dtype == RS_F32 || dtype == RS_BF16), "bad arguments");
   if (n == 0) return RS_OK;
-  return rs::launch_norms(x, n, dim, dtype, out, rs::as_stream(stream));
+  return rs::launch_norms(x, n, dim, dtype, out, rs::as_stream(stream), nullptr, nullptr);
 }

@@ -156,8 +156,6 @@ int launch_chunk_min(const float* norms, int64_t r0, int64_t r1, float* cmin, cu
 int encode_kmajor_bf16_map(CUtensorMap* map, const void* base, int64_t rows, int dim, int box_rows);
 // dtype RS_BF16 or RS_F32: 128-byte boxes (64 bf16 / 32 fp32) x box_rows, SWIZZLE_128B.
 int encode_kmajor_map(CUtensorMap* map, const void* base, int64_t rows, int dim, int box_rows, int dtype);
-// 3xTF32 operand split: lo[i] = x[i] - trunc_tf32(x[i]) (exact in fp32).
-int launch_tf32_lo(const float* x, int64_t count, float* lo, cudaStream_t st);
 
 // CUDA-core kernel for fp32 (and bf16 cross-checks), retrieval.cu.
 constexpr int kSimtBQ = 64;

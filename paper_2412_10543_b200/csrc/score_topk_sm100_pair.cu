@@ -283,7 +283,10 @@ __device__ __forceinline__ int next_unit(SmemTail* tail, uint32_t i, bool schedu
 #define RS_PAIR_PROFILE 0
 #endif
 #if RS_PAIR_PROFILE
-__device__ unsigned long long g_pair_prof[1024][8];
+// [cta][0..7]: role cycles (below); [cta][8..11]: epilogue event counts summed
+// over the CTA's epilogue lanes (warp-collective events once per warp):
+// slow-path 8-column groups, candidate appends, flushes, warp insert steps
+__device__ unsigned long long g_pair_prof[1024][16];
 #define PROF(slot, stmt)                       \
   do {                                         \
     const long long _t0 = clock64();           \
@@ -698,6 +701,17 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 #endif
       if (qrow < p.nq) rt.finish(p.part + ((qrow * p.segments + seg) * C::LPS + eg) * p.k);
     }
+#if RS_PAIR_PROFILE && RS_TOPK_COUNTERS
+    if (blockIdx.x < 1024) {
+      const uint32_t cnt[4] = {rt.c_groups, rt.c_appends, rt.c_flushes, rt.c_inserts};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        // groups / flushes / inserts are warp-uniform events: count them once per warp
+        const uint32_t v = i == 1 ? __reduce_add_sync(0xffffffffu, cnt[i]) : cnt[i];
+        if (lane == 0) atomicAdd(&g_pair_prof[blockIdx.x][8 + i], (unsigned long long)v);
+      }
+    }
+#endif
   }
 #if RS_PAIR_PROFILE
   prof[7] = clock64() - t_start;
@@ -721,10 +735,10 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 #if RS_PAIR_PROFILE
 extern "C" int rs_debug_pair_profile(unsigned long long* host_out, int nblocks) {
   cudaDeviceSynchronize();
-  return int(cudaMemcpyFromSymbol(host_out, g_pair_prof, sizeof(unsigned long long) * 8 * nblocks));
+  return int(cudaMemcpyFromSymbol(host_out, g_pair_prof, sizeof(unsigned long long) * 16 * nblocks));
 }
 extern "C" int rs_debug_pair_profile_reset() {
-  static unsigned long long zeros[1024][8];
+  static unsigned long long zeros[1024][16];
   return int(cudaMemcpyToSymbol(g_pair_prof, zeros, sizeof(zeros)));
 }
 #endif

@@ -198,6 +198,13 @@ __device__ __forceinline__ void epi_group8(RowTopK<ROWS, BUF>& rt, const uint32_
 // around) switches to phase 0 at the wrap: every later id is lower than every
 // id seen before it, and phase 0 sorts before phase 1 at equal distance, so
 // the rule stays exact at the same cost.
+#ifndef RS_TOPK_COUNTERS  // event counters in the profiling build (-DRS_PAIR_PROFILE=1)
+#if defined(RS_PAIR_PROFILE)
+#define RS_TOPK_COUNTERS RS_PAIR_PROFILE
+#else
+#define RS_TOPK_COUNTERS 0
+#endif
+#endif
 template <int KREG, int ROWS, int BUF>
 struct RegTopK {
   uint32_t key[KREG];  // (distance bits << 1) | phase
@@ -211,6 +218,13 @@ struct RegTopK {
   float qn;       // this row's |q|^2
   uint32_t wbase; // shared-window byte address of this row's buffer slot 0
   uint32_t wp;    // next free buffer slot
+#if RS_TOPK_COUNTERS
+  // event counts (tuning builds): slow-path groups, appends, flushes, inserts
+  uint32_t c_groups = 0, c_appends = 0, c_flushes = 0, c_inserts = 0;
+#define RS_TOPK_COUNT(field, n) (field) += (n)
+#else
+#define RS_TOPK_COUNT(field, n) ((void)0)
+#endif
 
   static constexpr uint32_t kEmpty = 0xff000001u;  // +inf, phase 1
 
@@ -229,6 +243,7 @@ struct RegTopK {
   }
 
   __device__ __forceinline__ void append_raw(float e, uint32_t cid) {
+    RS_TOPK_COUNT(c_appends, 1);
     asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(wp), "r"(cid), "r"(__float_as_uint(e)) : "memory");
     wp += ROWS * 8;
   }
@@ -291,12 +306,16 @@ struct RegTopK {
   __device__ __forceinline__ void flush() {
     const int n = buffered();
     const int nmax = __reduce_max_sync(0xffffffffu, n);
+    RS_TOPK_COUNT(c_flushes, 1);
     for (int j = 0; j < nmax; ++j) {
       uint32_t lo = 0, hi = 0;
       if (j < n) asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(lo), "=r"(hi) : "r"(wbase + j * ROWS * 8));
       // clamp negative round-off (and -0, NaN) to +0: bit pattern 0
       const uint32_t xk = j < n ? ((__uint_as_float(hi) > 0.0f ? hi : 0u) << 1) | phase : kEmpty;
-      if (__any_sync(0xffffffffu, xk < ktau)) insert(xk < ktau ? xk : kEmpty, lo);
+      if (__any_sync(0xffffffffu, xk < ktau)) {
+        RS_TOPK_COUNT(c_inserts, 1);
+        insert(xk < ktau ? xk : kEmpty, lo);
+      }
     }
     wp = wbase;
     refresh_tau();
@@ -317,6 +336,7 @@ template <int KREG, int ROWS, int BUF, int CHECK, bool FULL>
 __device__ __forceinline__ void epi_group8r(RegTopK<KREG, ROWS, BUF>& rt, const uint32_t* r, const float* cn,
                                             uint32_t id, int lim) {
   static_assert(BUF >= CHECK, "buffer must hold one group");
+  RS_TOPK_COUNT(rt.c_groups, 1);
   const float4 a = *reinterpret_cast<const float4*>(cn);
   const float4 b = *reinterpret_cast<const float4*>(cn + 4);
   const float2 q2 = make_float2(rt.qn, rt.qn);

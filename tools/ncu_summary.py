@@ -27,10 +27,13 @@ def launches(path, out):
     agg = collections.OrderedDict()
     for r in data:
         name = r[ki].split("(")[0].replace("rs::<unnamed>::", "").replace("(anonymous namespace)::", "")
+        if "at::" in name or "at_cuda_detail" in name:  # torch's own kernels (the synthetic-data generator)
+            continue
         agg.setdefault(name, []).append(float(r[vi].replace(",", "")) * UNIT[r[ui]])
     tot = sum(sum(v) for v in agg.values())
     lines = [f"# ncu launch list: `{path.split('/')[-1]}`", "",
-             "Cold-cache, serialised per-launch device times (`gpu__time_duration.sum`); compare shares.", "",
+             "Cold-cache, serialised per-launch device times (`gpu__time_duration.sum`) of the library's kernels "
+             "(torch's data-generator kernels dropped); compare shares.", "",
              "| kernel | launches | total ms | share |", "|---|---:|---:|---:|"]
     for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
         lines.append(f"| `{k}` | {len(v)} | {sum(v):.3f} | {100 * sum(v) / tot:.2f}% |")
