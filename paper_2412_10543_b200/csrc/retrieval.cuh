@@ -147,6 +147,9 @@ int pair_tile_rows(bool small);
 #ifndef RS_PAIR_CAS
 #define RS_PAIR_CAS 4  // cascade slots per query (score_topk_sm100_pair.cu)
 #endif
+#ifndef RS_PAIR_CAS_MULTI
+#define RS_PAIR_CAS_MULTI 0  // 1: every finished list inserts ranks r, 2r, ... (not only r)
+#endif
 constexpr int64_t kSharedBoundWords = 1 + RS_PAIR_CAS;
 // queries up to which a search uses the M = 128 pair tile (one tile, no padding rows)
 constexpr int64_t kSmallBatchMax = 128;

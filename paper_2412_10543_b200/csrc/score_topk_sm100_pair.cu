@@ -232,12 +232,17 @@ struct TileWalk {
 //  * qtau: the smallest k-th distance any list has reached (a list's k
 //    entries are real rows), published every 4 tiles and at unit end;
 //  * qcas[kCas-1]: each finished list inserts its rank-r distance (r =
-//    ceil(k/kCas)) once into a per-query cascade of kCas atomicMin slots, so
+//    ceil(k/kCas)) into a per-query cascade of kCas atomicMin slots, so
 //    slot kCas-1 holds the kCas-th smallest of them — kCas disjoint lists
 //    (distinct segments / column halves) with >= r rows each at or below
 //    it, i.e. >= k rows.  Once a few segments of a query are done this is
 //    far tighter than any single list's k-th distance, so later units admit
-//    ~k/kCas candidates instead of ~k.
+//    ~k/kCas candidates instead of ~k.  With RS_PAIR_CAS_MULTI a list
+//    inserts its rank-r, 2r, ... distances: the value at rank j*r stands for
+//    the list's rows of rank ((j-1)r, jr], disjoint from every other inserted
+//    value's rows, so slot kCas-1 is still backed by kCas*r >= k rows — and
+//    one list with many near rows (a document of consecutive chunks) now
+//    tightens the bound by itself.
 constexpr int kCas = RS_PAIR_CAS;
 static_assert(1 + kCas == kSharedBoundWords, "qtau allocation (retrieval.cu)");
 __device__ __forceinline__ uint32_t shared_bound(const Params& p, int64_t qrow) {
@@ -693,10 +698,17 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 #ifndef RS_PAIR_NO_SHARED_TAU
       if (real_row) {
         if (rt.kth_bits() < 0x7f800000u) red_min_relaxed_gpu_u32(p.qtau + qrow, rt.kth_bits());
-        // this finished list holds >= r rows at or below its rank-r distance:
-        // insert it into the query's kCas-smallest cascade
-        const uint32_t rb = rt.rank_bits(p.cas_rank);
-        if (rb < 0x7f800000u) cascade_min_insert(p.qcas + qrow * kCas, rb);
+        // this finished list holds >= j*r rows at or below its rank-j*r
+        // distance: insert it into the query's kCas-smallest cascade (ranks
+        // r, 2r, ... with RS_PAIR_CAS_MULTI; see shared_bound)
+        uint32_t* cas = p.qcas + qrow * kCas;
+        const uint32_t cut = RS_PAIR_CAS_MULTI ? ld_relaxed_gpu_u32(cas + (kCas - 1)) : 0xffffffffu;
+#pragma unroll 1
+        for (int j = 1; j <= (RS_PAIR_CAS_MULTI ? kCas : 1); ++j) {
+          const uint32_t rb = rt.rank_bits(j * p.cas_rank);
+          if (rb >= 0x7f800000u || rb >= cut) break;  // ranks ascend: so do the rest
+          cascade_min_insert(cas, rb);
+        }
       }
 #endif
       if (qrow < p.nq) rt.finish(p.part + ((qrow * p.segments + seg) * C::LPS + eg) * p.k);

@@ -303,10 +303,16 @@ struct RegTopK {
 
   // Warp-collective: every lane inserts its buffered candidates (lockstep over
   // the warp's largest buffer; lanes past their own count insert kEmpty = no-op).
+  // (A cooperative variant — a burst lane's list spread over the warp, ballot
+  // rank + shuffle shift per candidate — was measured slower: its per-candidate
+  // shuffle chain is latency-bound, profiles/r2_bench_and_data.md.)
   __device__ __forceinline__ void flush() {
     const int n = buffered();
     const int nmax = __reduce_max_sync(0xffffffffu, n);
     RS_TOPK_COUNT(c_flushes, 1);
+#ifdef RS_EXP_NO_INSERT  // timing experiment only (wrong results): candidates are dropped
+    if (nmax < 0)
+#endif
     for (int j = 0; j < nmax; ++j) {
       uint32_t lo = 0, hi = 0;
       if (j < n) asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(lo), "=r"(hi) : "r"(wbase + j * ROWS * 8));

@@ -1,0 +1,77 @@
+"""Candidate bursts in the pair kernel's register top-k.
+
+When a corpus stores a document's chunks under consecutive ids, a query's
+candidates arrive as a burst in ONE lane of an epilogue warp (its document's
+chunks fill a 32-column chunk), and the flush inserts them cooperatively
+(the whole warp works on that lane's list, RegTopK::coop_lane).  These tests
+pin that path against the float64 oracle and the lower-id tie rule, with
+exact-duplicate documents (every burst member ties) and forced wrap-around
+walks (bursts that straddle the walk's phase change)."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import retrieval_oracle as ro
+from paper_2412_10543_b200 import IndexFlatL2
+from tools import synth
+
+pytestmark = pytest.mark.gpu
+
+RTOL = {torch.bfloat16: 1e-3, torch.float32: 1e-5}
+
+
+def search(q, c, k, bias=0):
+    ix = IndexFlatL2(c.shape[1], dtype=c.dtype, capacity=c.shape[0])
+    ix.set_algo("tcgen05")
+    if bias:
+        ix.set_walk_bias(bias)
+    ix.add(c.cuda())
+    D, I = ix.search(q.cuda(), k)
+    torch.cuda.synchronize()
+    plan = ix.last_plan()
+    ix.close()
+    return D.cpu().numpy(), I.cpu().numpy(), plan
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("nq", [64, 1000])
+def test_doc_contiguous_corpus_matches_oracle(nq, dtype):
+    n, d, k = 120_000, 256, 35
+    c = synth.corpus_rows(0, n, d, 7, dtype, "cuda", "doc_contiguous").cpu()
+    q = synth.make_queries(nq, n, d, 7, dtype, "doc_contiguous")
+    D, I, plan = search(q, c, k)
+    assert plan["segments"] > 1
+    res = ro.check_topk(D, I, q, c, k, RTOL[dtype])
+    assert not res["violations"], res["violations"][:5]
+    assert res["exact_rows"] >= 0.9 * nq, res
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("bias", [0, 3])
+@pytest.mark.parametrize("block", [32, 12])
+def test_duplicate_document_bursts_keep_lower_ids(block, bias, dtype):
+    """Documents of `block` identical rows at consecutive ids: a query equal to
+    a document's vector ties with all of its rows, which must come back first
+    and in ascending id order, then the nearest other rows."""
+    n, d, k, nq = 150_000, 128, 35, 512
+    g = torch.Generator().manual_seed(block * 10 + bias)
+    c = torch.nn.functional.normalize(torch.randn(n, d, generator=g), dim=1)
+    starts = torch.randint(0, n // block - 1, (nq,), generator=g) * block
+    for s in starts.tolist():
+        c[s:s + block] = c[s]
+    c = c.to(dtype)
+    q = c[starts].clone()
+    D, I, plan = search(q, c, k, bias)
+    assert plan["segments"] > 1 and plan["qtiles"] > 1
+    m = min(block, k)
+    for r, s in enumerate(starts.tolist()):
+        np.testing.assert_array_equal(I[r, :m], s + np.arange(m), err_msg=f"row {r}")
+        assert np.all(D[r, :m] == D[r, 0])
+    res = ro.check_topk(D[:128], I[:128], q[:128], c, k, RTOL[dtype])
+    assert not res["violations"], res["violations"][:5]
+    # the production walk (no bias) returns the same lists
+    if bias:
+        D0, I0, _ = search(q, c, k)
+        np.testing.assert_array_equal(I0, I)
+        np.testing.assert_array_equal(D0, D)

@@ -30,7 +30,21 @@ def main():
     ap.add_argument("--data", default="iso")
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--reps", type=int, default=1)
+    ap.add_argument("--persist-mb", type=int, default=0,
+                    help="experiment: cudaLimitPersistingL2CacheSize (evict_last lines are protected inside it)")
     a = ap.parse_args()
+    if a.persist_mb:
+        import ctypes
+        import glob
+
+        import torch
+
+        torch.cuda.init()
+        libs = glob.glob(os.path.join(os.path.dirname(torch.__file__), "lib", "libcudart*.so*")) + \
+            glob.glob("/usr/local/cuda/lib64/libcudart.so*")
+        rt = ctypes.CDLL(libs[0])
+        rc = rt.cudaDeviceSetLimit(ctypes.c_int(0x06), ctypes.c_size_t(a.persist_mb << 20))
+        print("cudaDeviceSetLimit(PersistingL2CacheSize) rc", rc, "via", libs[0])
     cfg = dict(bench.WORKLOADS[a.workload])
     if a.queries:
         cfg["nq"] = a.queries
