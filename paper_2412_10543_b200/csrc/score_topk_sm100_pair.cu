@@ -49,8 +49,14 @@ using namespace sm100;
 #ifndef RS_PAIR_STAGES
 #define RS_PAIR_STAGES 6
 #endif
+#ifndef RS_TOPK_COOP_ALL_SITES
+#define RS_TOPK_COOP_ALL_SITES 1  // 0: the walk-wrap and unit-end flushes stay lockstep-only
+#endif
 #ifndef RS_PAIR_BUF
-#define RS_PAIR_BUF 16  // swept 8..48 with 5/6 stages on B200: 6 stages x 16 best
+// candidate buffer slots per row: one check per RS_TOPK_CHECK_GROUPS 8-column
+// groups flushes above 8 buffered, so a check interval of 16 columns needs 24
+// (swept 8..48 with one check per group and 5/6 stages: 6 x 16 was best then)
+#define RS_PAIR_BUF (8 + 8 * RS_TOPK_CHECK_GROUPS)
 #endif
 
 constexpr int BM = 128;         // query rows per CTA (TMEM lanes)
@@ -71,7 +77,7 @@ constexpr int KREG_TF32 = kTcMaxK + kRefineExtra;
 // candidate buffer per row; a warp flushes when one of its lanes holds more
 // than BUF - CHECK entries, so every flush batches many candidates per lane
 constexpr int BUF = RS_PAIR_BUF;
-constexpr int CHECK = 8;
+constexpr int CHECK = 8 * RS_TOPK_CHECK_GROUPS;  // candidates one check interval can add per row
 constexpr int EPI_COLS = 32;    // TMEM columns per tcgen05.ld
 #ifndef RS_PAIR_EPI_PAIRED
 #define RS_PAIR_EPI_PAIRED 0       // 1: two loads per tcgen05.wait::ld
@@ -167,13 +173,14 @@ struct Cfg {
   static constexpr int OFF_B = NT * A_BYTESv;  // stage layout: A hi | [A lo] | B hi | [B lo]
   static constexpr uint32_t IDESC = TF ? umma_idesc_tf32_f32(PMv, BN) : umma_idesc_bf16_f32(PMv, BN);
   using Tail = SmemTailT<STAGES>;
-  static constexpr size_t OFF_BUF = size_t(STAGES) * STAGE_BYTES;
-  static constexpr size_t OFF_CN = OFF_BUF + size_t(BUF) * EPI_THREADS * 8;
-  static constexpr size_t OFF_TAIL = OFF_CN + 2 * BN * sizeof(float);
-  static constexpr size_t SMEM_BYTES = OFF_TAIL + sizeof(Tail);
-  static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
   static constexpr int KR = TF ? KREG_TF32 : KREG;  // register top-k capacity
   using TopK = RegTopK<KR, EPI_THREADS, BUF>;
+  static constexpr size_t OFF_BUF = size_t(STAGES) * STAGE_BYTES;
+  static constexpr size_t OFF_CN = OFF_BUF + size_t(BUF) * EPI_THREADS * 8;
+  static constexpr size_t OFF_SCR = OFF_CN + 2 * BN * sizeof(float);  // per epilogue warp: KR x 8 B (coop_merge)
+  static constexpr size_t OFF_TAIL = OFF_SCR + size_t(EPI_THREADS / 32) * KR * 8;
+  static constexpr size_t SMEM_BYTES = OFF_TAIL + sizeof(Tail);
+  static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
 };
 
 struct Params {
@@ -580,6 +587,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     typename C::TopK rt;
     rt.k = p.k;
     rt.wbase = smem_u32(smem + C::OFF_BUF) + uint32_t(et) * 8u;
+    rt.sbase = smem_u32(smem + C::OFF_SCR) + uint32_t(warp - EPI_WARP0) * uint32_t(C::KR) * 8u;
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tail->tempty[0]), pair_leader);
     const uint32_t tempty_leader1 = mapa_shared(smem_u32(&tail->tempty[1]), pair_leader);
     uint32_t tile_iter = 0;
@@ -608,7 +616,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         // ids below every one seen so far from here on: flush the earlier
         // phase's candidates, then tag the rest phase 0 (RegTopK ordering)
         if (rt.phase && walk.wrapped(j)) {
-          rt.flush();
+          rt.template flush<RS_TOPK_COOP_ALL_SITES>();
           rt.phase = 0;
         }
         const uint32_t acc = tile_iter & 1;
@@ -694,7 +702,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         }
       }
       // every lane flushes (warp-collective), then writes its row if it is a real query
-      PROF(5, rt.flush());
+      PROF(5, rt.template flush<RS_TOPK_COOP_ALL_SITES>());
 #ifndef RS_PAIR_NO_SHARED_TAU
       if (real_row) {
         if (rt.kth_bits() < 0x7f800000u) red_min_relaxed_gpu_u32(p.qtau + qrow, rt.kth_bits());
@@ -715,9 +723,9 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     }
 #if RS_PAIR_PROFILE && RS_TOPK_COUNTERS
     if (blockIdx.x < 1024) {
-      const uint32_t cnt[4] = {rt.c_groups, rt.c_appends, rt.c_flushes, rt.c_inserts};
+      const uint32_t cnt[5] = {rt.c_groups, rt.c_appends, rt.c_flushes, rt.c_inserts, rt.c_coop};
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
+      for (int i = 0; i < 5; ++i) {
         // groups / flushes / inserts are warp-uniform events: count them once per warp
         const uint32_t v = i == 1 ? __reduce_add_sync(0xffffffffu, cnt[i]) : cnt[i];
         if (lane == 0) atomicAdd(&g_pair_prof[blockIdx.x][8 + i], (unsigned long long)v);

@@ -205,6 +205,93 @@ __device__ __forceinline__ void epi_group8(RowTopK<ROWS, BUF>& rt, const uint32_
 #define RS_TOPK_COUNTERS 0
 #endif
 #endif
+#ifndef RS_TOPK_COOP
+#define RS_TOPK_COOP 6  // buffered candidates from which a lane may be merged cooperatively (0 = never)
+#endif
+#ifndef RS_TOPK_CHECK_GROUPS
+#define RS_TOPK_CHECK_GROUPS 2  // 8-column groups per buffer check in epi_chunk32b (1 or 2)
+#endif
+#ifndef RS_TOPK_COOP_GAIN
+#define RS_TOPK_COOP_GAIN 5  // ...and that lane holds at least this many more than every other lane
+#endif
+// Warp-cooperative sort behind RegTopK::flush for a burst lane (a document
+// of consecutive chunks puts up to 32 candidates of one query in one
+// 32-column chunk, and the lockstep insert would cost the warp one KREG-wide
+// sweep per candidate).  The scratch holds the lane's KREG sorted list
+// entries (key, id); every lane takes two of 64 elements (four of 128 when
+// KREG + BUF > 64) — list entries,
+// then the lane's admitted buffer entries (sbuf: its slot 0), then kEmpty —
+// packed u64 (key << 32 | id); a 21-stage (28) bitonic sort over the warp orders
+// them and the first KREG go back to the scratch.  u64 order on (key, id) is
+// exactly the sequential insert's order: within a phase equal keys arrive
+// with ascending ids, and the phase bit in the key orders the two phases.
+// Not inlined: ~1k instructions that only bursts execute stay out of the
+// epilogue's ~10 inlined flush sites.  (A per-candidate cooperative variant
+// — ballot rank + shuffle shift — was slower.)
+template <int KREG, int ROWS, int BUF>
+__device__ __noinline__ void coop_sort64(uint32_t scr, uint32_t sbuf, int ns, uint32_t kt, uint32_t ph) {
+  constexpr int E = KREG + BUF <= 64 ? 2 : 4;  // elements per lane: 64 or 128 in all
+  static_assert(KREG % 2 == 0 && KREG + BUF <= 32 * E, "cooperative merge capacity");
+  constexpr uint32_t kEmptyKey = 0xff000001u;
+  const int lane = int(threadIdx.x & 31);
+  unsigned long long v[E];
+#pragma unroll
+  for (int s = 0; s < E; ++s) {
+    const int e = E * lane + s;
+    uint32_t a = kEmptyKey, b = 0xffffffffu;
+    if (e < KREG) {
+      asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(a), "=r"(b) : "r"(scr + e * 8));
+    } else if (e - KREG < ns) {
+      uint32_t cid, dbits;
+      asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(cid), "=r"(dbits) : "r"(sbuf + (e - KREG) * ROWS * 8));
+      // clamp negative round-off (and -0, NaN) to +0, as the lockstep flush
+      const uint32_t xk = ((__uint_as_float(dbits) > 0.0f ? dbits : 0u) << 1) | ph;
+      if (xk < kt) {
+        a = xk;
+        b = cid;
+      }
+    }
+    v[s] = (static_cast<unsigned long long>(a) << 32) | b;
+  }
+  // bitonic sort of the 32*E elements (element e = E*lane + s), ascending
+#pragma unroll
+  for (int size = 2; size <= 32 * E; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      if (stride < E) {  // partner in the same lane
+#pragma unroll
+        for (int s = 0; s < E; ++s) {
+          if (s & stride) continue;
+          const int e = E * lane + s;
+          const bool asc = (e & size) == 0;
+          const unsigned long long x = v[s], y = v[s + stride];
+          const bool sw = asc ? y < x : x < y;
+          v[s] = sw ? y : x;
+          v[s + stride] = sw ? x : y;
+        }
+      } else {
+#pragma unroll
+        for (int s = 0; s < E; ++s) {
+          const int e = E * lane + s;
+          const unsigned long long o = __shfl_xor_sync(0xffffffffu, v[s], stride / E);
+          const bool keep_min = ((e & stride) == 0) == ((e & size) == 0);
+          v[s] = keep_min ? (o < v[s] ? o : v[s]) : (o < v[s] ? v[s] : o);
+        }
+      }
+    }
+  }
+  __syncwarp();  // every lane read the scratch before it is rewritten
+#pragma unroll
+  for (int s = 0; s < E; ++s) {
+    const int e = E * lane + s;
+    if (e < KREG)
+      asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(scr + e * 8), "r"(uint32_t(v[s] >> 32)),
+                   "r"(uint32_t(v[s]))
+                   : "memory");
+  }
+  __syncwarp();
+}
+
 template <int KREG, int ROWS, int BUF>
 struct RegTopK {
   uint32_t key[KREG];  // (distance bits << 1) | phase
@@ -220,7 +307,7 @@ struct RegTopK {
   uint32_t wp;    // next free buffer slot
 #if RS_TOPK_COUNTERS
   // event counts (tuning builds): slow-path groups, appends, flushes, inserts
-  uint32_t c_groups = 0, c_appends = 0, c_flushes = 0, c_inserts = 0;
+  uint32_t c_groups = 0, c_appends = 0, c_flushes = 0, c_inserts = 0, c_coop = 0;
 #define RS_TOPK_COUNT(field, n) (field) += (n)
 #else
 #define RS_TOPK_COUNT(field, n) ((void)0)
@@ -301,13 +388,54 @@ struct RegTopK {
     return t >> 1;
   }
 
+  // Cooperative merge of ONE lane's list with its buffered candidates, by the
+  // whole warp (coop_sort64 below): lane src publishes its KREG sorted
+  // entries to the warp's scratch, the warp sorts them with src's admitted
+  // buffer entries, src reloads the first KREG.
+  uint32_t sbase;  // shared-window byte address of this warp's 64 x 8-byte scratch
+  __device__ __forceinline__ void coop_merge(int src, int ns, uint32_t kt) {
+    const int lane = int(threadIdx.x & 31);
+    if (lane == src) {
+#pragma unroll
+      for (int j = 0; j < KREG; j += 2)
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(sbase + j * 8), "r"(key[j]), "r"(id[j]),
+                     "r"(key[j + 1]), "r"(id[j + 1])
+                     : "memory");
+    }
+    __syncwarp();
+    coop_sort64<KREG, ROWS, BUF>(sbase, wbase + uint32_t(src - lane) * 8u, ns, kt, phase);
+    if (lane == src) {
+#pragma unroll
+      for (int j = 0; j < KREG; j += 2)
+        asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(key[j]), "=r"(id[j]), "=r"(key[j + 1]), "=r"(id[j + 1])
+                     : "r"(sbase + j * 8));
+    }
+    __syncwarp();  // src read the scratch before the next merge rewrites it
+  }
+
   // Warp-collective: every lane inserts its buffered candidates (lockstep over
   // the warp's largest buffer; lanes past their own count insert kEmpty = no-op).
-  // (A cooperative variant — a burst lane's list spread over the warp, ballot
-  // rank + shuffle shift per candidate — was measured slower: its per-candidate
-  // shuffle chain is latency-bound, profiles/r2_bench_and_data.md.)
+  // Lockstep costs the warp one KREG-wide sweep per candidate of its FULLEST
+  // lane, so a lane that holds RS_TOPK_COOP_GAIN or more candidates beyond
+  // every other lane (a burst) is merged cooperatively first, fullest first.
+  template <bool COOP = true>
   __device__ __forceinline__ void flush() {
-    const int n = buffered();
+    int n = buffered();
+#if RS_TOPK_COOP
+    const int lane = int(threadIdx.x & 31);
+#pragma unroll 1
+    for (; COOP;) {
+      const int top = __reduce_max_sync(0xffffffffu, n);
+      if (top < RS_TOPK_COOP) break;
+      const int src = __ffs(__ballot_sync(0xffffffffu, n == top)) - 1;
+      const int second = __reduce_max_sync(0xffffffffu, lane == src ? 0 : n);
+      if (top - second < RS_TOPK_COOP_GAIN) break;
+      RS_TOPK_COUNT(c_coop, 1);
+      coop_merge(src, top, __shfl_sync(0xffffffffu, ktau, src));
+      if (lane == src) n = 0;
+    }
+#endif
     const int nmax = __reduce_max_sync(0xffffffffu, n);
     RS_TOPK_COUNT(c_flushes, 1);
 #ifdef RS_EXP_NO_INSERT  // timing experiment only (wrong results): candidates are dropped
@@ -338,10 +466,10 @@ struct RegTopK {
 
 // Exact distances and predicated appends of 8 columns for RegTopK (the slow
 // path of epi_chunk32b).
-template <int KREG, int ROWS, int BUF, int CHECK, bool FULL>
+template <int KREG, int ROWS, int BUF, int CHECK, bool FULL, bool CHK = true>
 __device__ __forceinline__ void epi_group8r(RegTopK<KREG, ROWS, BUF>& rt, const uint32_t* r, const float* cn,
                                             uint32_t id, int lim) {
-  static_assert(BUF >= CHECK, "buffer must hold one group");
+  static_assert(BUF >= CHECK, "buffer must hold the groups between two checks");
   RS_TOPK_COUNT(rt.c_groups, 1);
   const float4 a = *reinterpret_cast<const float4*>(cn);
   const float4 b = *reinterpret_cast<const float4*>(cn + 4);
@@ -359,7 +487,7 @@ __device__ __forceinline__ void epi_group8r(RegTopK<KREG, ROWS, BUF>& rt, const 
 #pragma unroll
   for (int j = 0; j < 8; ++j)
     if ((FULL || j < lim) && e[j] <= rt.tau) rt.append_raw(e[j], id + j);
-  if (__any_sync(0xffffffffu, rt.buffered() > BUF - CHECK)) rt.flush();
+  if (CHK && __any_sync(0xffffffffu, rt.buffered() > BUF - CHECK)) rt.flush();
 }
 
 // Bound-filtered epilogue (epi_chunk32b below).  For the columns of a 32-column chunk,
@@ -391,6 +519,7 @@ __device__ __forceinline__ void epi_chunk32b(RegTopK<KREG, ROWS, BUF>& rt, const
 #pragma unroll
   for (int g = 0; g < 4; ++g) hit |= __any_sync(0xffffffffu, m[g] >= thr) ? (1u << g) : 0u;
   if (hit == 0) return;
+#if RS_TOPK_CHECK_GROUPS == 1
 #pragma unroll
   for (int g = 0; g < 4; ++g)
     if (hit & (1u << g)) {
@@ -399,6 +528,20 @@ __device__ __forceinline__ void epi_chunk32b(RegTopK<KREG, ROWS, BUF>& rt, const
       else
         epi_group8r<KREG, ROWS, BUF, CHECK, false>(rt, r + g * 8, cn + g * 8, id + g * 8, lim - g * 8);
     }
+#else
+  // one buffer check per two groups (half the inlined flush sites; CHECK
+  // then covers 16 columns)
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    if (hit & (1u << g)) {
+      if (FULL)
+        epi_group8r<KREG, ROWS, BUF, CHECK, true, false>(rt, r + g * 8, cn + g * 8, id + g * 8, 8);
+      else
+        epi_group8r<KREG, ROWS, BUF, CHECK, false, false>(rt, r + g * 8, cn + g * 8, id + g * 8, lim - g * 8);
+    }
+    if ((g & 1) && (hit & (3u << (g - 1))) && __any_sync(0xffffffffu, rt.buffered() > BUF - CHECK)) rt.flush();
+  }
+#endif
 }
 
 // Dot threshold of a chunk whose smallest corpus norm is cmin (see

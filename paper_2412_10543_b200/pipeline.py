@@ -215,3 +215,24 @@ class SelectHostStream(HostStream):
         if delay is not None:
             res["delay"] = delay
         return slot.download(self.ring.d2h, main, res)
+
+
+class FnHostStream(HostStream):
+    """Any device pipeline end to end with host inputs, pipelined like
+    ``RetrieveSelect.submit_host``: ``fn(*device_inputs)`` runs on the current
+    stream and returns a dict of device outputs, which are copied back to
+    pinned host buffers.  The sharded multi-GPU pipeline (``dist``) uses it
+    for its end-to-end numbers."""
+
+    def __init__(self, fn, host_inputs, *, device=None):
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.ring = _HostRing(self.device, HOST_DEPTH)
+        self.fn, self.host_inputs = fn, tuple(host_inputs)
+        super().__init__(self._submit)
+
+    def _submit(self) -> HostTicket:
+        slot = self.ring.acquire()
+        ins = slot.upload(self.ring.h2d, self.host_inputs)
+        main = torch.cuda.current_stream(self.device)
+        main.wait_event(slot.uploaded)
+        return slot.download(self.ring.d2h, main, self.fn(*ins))

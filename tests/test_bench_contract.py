@@ -102,3 +102,24 @@ def test_our_arm_parity_block_on_a_small_corpus():
     assert p["retrieval"]["violations"] == 0 and p["retrieval"]["sample_queries"] == 128
     assert p["retrieval"]["max_rel_err"] < 1e-3
     assert d["cpu_baseline"]["value"] > 0 and d["cpu_baseline"]["cores"] >= 1
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(900)
+def test_two_rank_line_with_pipelined_e2e():
+    """Two ranks (torchrun; both on cuda:0 over gloo, the plumbing check this
+    one-GPU pool allows): the corpus-sharded cfg4 path prints one line from
+    rank 0 with n_gpus = 2 and an end-to-end number through the pipelined
+    host stream (FnHostStream)."""
+    env = dict(os.environ, RS_BENCH_BACKEND="gloo", RS_BENCH_DEVICE="0")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", "29517", os.path.join(ROOT, "bench.py"),
+                        "--gpus", "2", "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--corpus-rows", "300000"],
+                       capture_output=True, text=True, timeout=800, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0
+    assert d["e2e"]["value"] > 0 and "copy streams" in d["e2e"]["overlap"]
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0

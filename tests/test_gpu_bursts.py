@@ -2,11 +2,15 @@
 
 When a corpus stores a document's chunks under consecutive ids, a query's
 candidates arrive as a burst in ONE lane of an epilogue warp (its document's
-chunks fill a 32-column chunk), and the flush inserts them cooperatively
-(the whole warp works on that lane's list, RegTopK::coop_lane).  These tests
-pin that path against the float64 oracle and the lower-id tie rule, with
-exact-duplicate documents (every burst member ties) and forced wrap-around
-walks (bursts that straddle the walk's phase change)."""
+chunks fill a 32-column chunk), and the flush merges that lane's list
+cooperatively (the whole warp sorts it with the lane's buffered candidates,
+RegTopK::coop_merge / coop_sort64) whenever the lane holds
+RS_TOPK_COOP_GAIN more candidates than every other lane; the rest goes
+through the lockstep insert.  These tests pin both paths against the float64
+oracle and the lower-id tie rule, with exact-duplicate documents (every
+burst member ties), forced wrap-around walks (bursts that straddle the
+walk's phase change) and mixed burst sizes inside one warp (the greedy
+fullest-lane-first loop, then lockstep for the remainder)."""
 
 import numpy as np
 import pytest
@@ -75,3 +79,35 @@ def test_duplicate_document_bursts_keep_lower_ids(block, bias, dtype):
         D0, I0, _ = search(q, c, k)
         np.testing.assert_array_equal(I0, I)
         np.testing.assert_array_equal(D0, D)
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("bias", [0, 5])
+def test_mixed_burst_sizes_in_one_warp(bias, dtype):
+    """Each 32-row corpus chunk of a group holds duplicate documents of sizes
+    16, 8, 3 and 5; four consecutive queries (lanes of one epilogue warp) equal
+    those four documents, so one flush sees bursts of different sizes in
+    several lanes: the fullest lane is merged cooperatively while it leads the
+    others by the gain threshold, the rest in lockstep.  Every query must get
+    its document's rows first, in ascending id order, then the oracle's."""
+    n, d, k = 160_000, 128, 35
+    sizes = [16, 8, 3, 5]
+    g = torch.Generator().manual_seed(99 + bias)
+    c = torch.nn.functional.normalize(torch.randn(n, d, generator=g), dim=1)
+    groups = torch.randperm(n // 32 - 1, generator=g)[:192].tolist()
+    starts = []
+    for grp in groups:
+        b = grp * 32
+        for sz in sizes:
+            c[b:b + sz] = torch.nn.functional.normalize(torch.randn(d, generator=g), dim=0)
+            starts.append((b, sz))
+            b += sz
+    c = c.to(dtype)
+    q = torch.stack([c[s] for s, _ in starts]).clone()
+    D, I, plan = search(q, c, k, bias)
+    assert plan["segments"] > 1 and plan["qtiles"] > 1
+    for r, (s, sz) in enumerate(starts):
+        np.testing.assert_array_equal(I[r, :sz], s + np.arange(sz), err_msg=f"row {r}")
+        assert np.all(D[r, :sz] == D[r, 0])
+    res = ro.check_topk(D, I, q, c, k, RTOL[dtype])
+    assert not res["violations"], res["violations"][:5]

@@ -34,7 +34,7 @@ NAMES = {0: "producer wait empty (ring full)", 1: "mma wait tempty (epilogue-bou
          2: "mma wait full (operand-bound)", 3: "epilogue wait tfull (4 warps)",
          5: "epilogue final flush (4 warps)", 4: "epilogue filter (4 warps)",
          6: "epilogue TMEM load wait (4 warps)"}
-COUNTERS = {8: "slow-path groups", 9: "appends", 10: "flushes", 11: "insert steps"}
+COUNTERS = {8: "slow-path groups", 9: "appends", 10: "flushes", 11: "insert steps", 12: "cooperative merges"}
 
 
 def main():
@@ -83,7 +83,7 @@ def main():
     tiles = -(-n // 256)
     rows_total = plan["qtiles"] * (256 if nq > 128 else 128)
     warp_tiles = rows_total / 32 * tiles
-    c = arr[:, 8:12].sum(0)
+    c = arr[:, 8:13].sum(0)
     out["per_warp_tile"] = {nm: round(float(c[i - 8]) / warp_tiles, 4) for i, nm in COUNTERS.items()}
     out["appends_per_query"] = round(float(c[1]) / nq, 1)
     print("epilogue events per (32 query rows, 256-row corpus tile):", out["per_warp_tile"])
