@@ -432,74 +432,103 @@ int launch_merge(const uint64_t* keys, int64_t nq, int nlists, int k_in, int64_t
 //
 // One CTA per query, three phases, one launch (the merge of the per-segment
 // lists, the scoring and the ranking were three kernels in round 1):
-//  1. warp 0 merges the query's sorted tf32 lists into the kc smallest keys;
-//  2. all 8 warps score them: each 8-lane group holds one candidate row in
-//     flight (float4 loads spread over the group, three in-group shuffles), so
-//     32 random row gathers per CTA overlap;
-//  3. warp 0 ranks the exact keys (lane j owns candidates j and j + 32) and
-//     writes the top k with the keep limit.  Keys are unique except padding.
-constexpr int kRefineWarps = 8;
-__global__ void __launch_bounds__(kRefineWarps * 32) refine_fp32_kernel(
+//  1. all threads copy the query's lists (nlists x k_in keys, contiguous) into
+//     shared memory in one coalesced pass, then warp 0 merges them into the kc
+//     smallest keys (warp_merge64 over shared memory: the round-2 version
+//     walked the lists in global memory, one dependent L2 round trip per
+//     merged key, and the other warps idled at the barrier);
+//  2. all warps score them, one candidate row per warp at a time: every lane
+//     issues its (up to 8) float4 loads of the row at once (the query row is
+//     staged in shared memory in phase 1), so a row costs one DRAM round
+//     trip, then a 5-step butterfly;
+//  3. warps 0-1 rank the exact keys (thread t owns candidate t) and write the
+//     top k with the keep limit.  Keys are unique except padding.
+#ifndef RS_REFINE_WARPS
+#define RS_REFINE_WARPS 4  // 8 / 4 / 2 measured at cfg1: 46.5 / 35.5 / 51 us (profiles/r2_refine.md)
+#endif
+constexpr int kRefineWarps = RS_REFINE_WARPS;
+constexpr int kRefineVec = 8;  // float4 loads per lane per 1024-element slice of a row
+__global__ void __launch_bounds__(kRefineWarps * 32, 32 / kRefineWarps) refine_fp32_kernel(
     const uint64_t* __restrict__ lists, int nlists, int k_in, int64_t list_stride, int64_t q_stride, int kc,
     const float* __restrict__ Q, const float* __restrict__ qn, const float* __restrict__ C,
     const float* __restrict__ cn, int64_t nq, int dim, int64_t id_base, int k, const rs_config* __restrict__ keep,
     float* __restrict__ D, int64_t* __restrict__ I, uint64_t* __restrict__ keys_out) {
-  __shared__ uint64_t cand[64], exact[64];
+  extern __shared__ uint64_t refine_smem[];
+  uint64_t* cand = refine_smem;         // [64]
+  uint64_t* exact = refine_smem + 64;   // [64]
+  float4* qsm = reinterpret_cast<float4*>(refine_smem + 128);  // [dim / 4]: the query row
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int grp = lane >> 3, gl = lane & 7;
-  const unsigned gmask = 0xFFu << (grp * 8);
   const int d4 = dim / 4;
+  uint64_t* lsm = refine_smem + 128 + 2 * d4;  // [nlists][k_in] (a float4 is two 8-byte words)
+  const int nkeys = nlists * k_in;
   for (int64_t q = blockIdx.x; q < nq; q += gridDim.x) {
+    const uint64_t* lq = lists + q * q_stride;
+    for (int t = threadIdx.x; t < nkeys; t += kRefineWarps * 32) {
+      const int l = t / k_in;
+      lsm[t] = lq[int64_t(l) * list_stride + (t - l * k_in)];
+    }
+    const float4* qv = reinterpret_cast<const float4*>(Q + q * dim);
+    for (int t = threadIdx.x; t < d4; t += kRefineWarps * 32) qsm[t] = __ldg(qv + t);
+    __syncthreads();
     if (w == 0) {  // 1. candidates
-      const int got = warp_merge64<false>(lists + q * q_stride, nlists, k_in, list_stride, kc,
-                                          [&](int j, uint64_t v) { cand[j] = v; });
+      const int got = warp_merge64<false>(lsm, nlists, k_in, k_in, kc, [&](int j, uint64_t v) { cand[j] = v; });
       for (int j = got + lane; j < 64; j += 32) cand[j] = kEmptyKey;
+    } else if (w == 1) {
       for (int j = kc + lane; j < 64; j += 32) exact[j] = kEmptyKey;
     }
     __syncthreads();
-    const float4* qv = reinterpret_cast<const float4*>(Q + q * dim);
     const float qq = qn[q];
-    for (int j = w * 4 + grp; j < kc; j += kRefineWarps * 4) {  // 2. exact distances
+    for (int j = w; j < kc; j += kRefineWarps) {  // 2. exact distances, one row per warp
       const uint64_t key = cand[j];
-      uint64_t out = kEmptyKey;
-      if (key != kEmptyKey) {  // group-uniform
-        const int64_t row = int64_t(uint32_t(key)) - id_base;
-        const float4* cv = reinterpret_cast<const float4*>(C + row * dim);
-        float acc = 0.0f;
-        for (int i = gl; i < d4; i += 8) {
-          const float4 a = qv[i], b = cv[i];
-          acc = fmaf(a.x, b.x, acc);
-          acc = fmaf(a.y, b.y, acc);
-          acc = fmaf(a.z, b.z, acc);
-          acc = fmaf(a.w, b.w, acc);
+      if (key == kEmptyKey) {  // warp-uniform
+        if (lane == 0) exact[j] = kEmptyKey;
+        continue;
+      }
+      const int64_t row = int64_t(uint32_t(key)) - id_base;
+      const float4* cv = reinterpret_cast<const float4*>(C + row * dim);
+      float acc = 0.0f;
+      for (int base = 0; base < d4; base += 32 * kRefineVec) {
+        float4 b[kRefineVec];  // the row's loads all in flight; the query comes from shared memory
+#pragma unroll
+        for (int i = 0; i < kRefineVec; ++i) {
+          const int x = base + lane + 32 * i;
+          if (x < d4) b[i] = __ldg(cv + x);
         }
 #pragma unroll
-        for (int off = 4; off > 0; off >>= 1) acc += __shfl_xor_sync(gmask, acc, off);
+        for (int i = 0; i < kRefineVec; ++i) {
+          if (base + lane + 32 * i < d4) {
+            const float4 a = qsm[base + lane + 32 * i];
+            acc = fmaf(a.x, b[i].x, acc);
+            acc = fmaf(a.y, b[i].y, acc);
+            acc = fmaf(a.z, b[i].z, acc);
+            acc = fmaf(a.w, b[i].w, acc);
+          }
+        }
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+      if (lane == 0) {
         float dist = fmaf(-2.0f, acc, qq + cn[row]);
         dist = dist > 0.0f ? dist : 0.0f;  // FAISS clamps round-off at 0 (and NaN -> 0)
-        out = (uint64_t(__float_as_uint(dist)) << 32) | uint32_t(key);
+        exact[j] = (uint64_t(__float_as_uint(dist)) << 32) | uint32_t(key);
       }
-      if (gl == 0) exact[j] = out;
     }
     __syncthreads();
-    if (w == 0) {  // 3. rank
-      const uint64_t mine[2] = {exact[lane], exact[lane + 32]};
-      const int limit = keep_limit(keep, q, k);
-      int rank[2] = {0, 0};
+    if (threadIdx.x < 64) {  // 3. rank: thread t owns candidate t
+      const int t = threadIdx.x;
+      const uint64_t mine = exact[t];
+      int r = 0;
+#pragma unroll 8
       for (int j = 0; j < 64; ++j) {
         const uint64_t o = exact[j];
-#pragma unroll
-        for (int t = 0; t < 2; ++t) rank[t] += (o < mine[t] || (o == mine[t] && j < lane + 32 * t)) ? 1 : 0;
+        r += (o < mine || (o == mine && j < t)) ? 1 : 0;
       }
-#pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        const int r = rank[t];
-        if (r < k) {
-          const bool real = mine[t] != kEmptyKey && r < limit;
-          if (keys_out) keys_out[q * k + r] = real ? mine[t] : kEmptyKey;
-          if (D) D[q * k + r] = real ? key_dist(mine[t]) : __int_as_float(0x7f800000);
-          if (I) I[q * k + r] = real ? int64_t(uint32_t(mine[t])) : int64_t(-1);
-        }
+      if (r < k) {
+        const int limit = keep_limit(keep, q, k);
+        const bool real = mine != kEmptyKey && r < limit;
+        if (keys_out) keys_out[q * k + r] = real ? mine : kEmptyKey;
+        if (D) D[q * k + r] = real ? key_dist(mine) : __int_as_float(0x7f800000);
+        if (I) I[q * k + r] = real ? int64_t(uint32_t(mine)) : int64_t(-1);
       }
     }
     __syncthreads();
@@ -523,10 +552,21 @@ int launch_refine_fp32(const uint64_t* lists, int nlists, int k_in, int64_t list
     list_stride = kc;
     q_stride = kc;
   }
-  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(nq, int64_t(sms) * 8));
-  refine_fp32_kernel<<<(unsigned)blocks, kRefineWarps * 32, 0, st>>>(lists, nlists, k_in, list_stride, q_stride, kc,
-                                                                     Q, qn, C, cn, nq, dim, id_base, k, keep, D, I,
-                                                                     keys_out);
+  // cand + exact (1 KB), the query row, the lists (<= 64 x 255 keys)
+  const size_t smem = size_t(128 + 2 * (dim / 4) + nlists * k_in) * sizeof(uint64_t);
+  RS_REQUIRE(smem <= 160 * 1024, "refine: %d lists x %d keys at d = %d exceed shared memory", nlists, k_in, dim);
+  if (smem > 48 * 1024) {
+    static bool opted = false;
+    if (!opted) {
+      RS_CHECK_CUDA(cudaFuncSetAttribute(refine_fp32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024),
+                    "cudaFuncSetAttribute(refine_fp32_kernel)");
+      opted = true;
+    }
+  }
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(nq, int64_t(sms) * (64 / kRefineWarps)));
+  refine_fp32_kernel<<<(unsigned)blocks, kRefineWarps * 32, smem, st>>>(lists, nlists, k_in, list_stride, q_stride,
+                                                                         kc, Q, qn, C, cn, nq, dim, id_base, k, keep,
+                                                                         D, I, keys_out);
   RS_CHECK_LAUNCH("refine_fp32_kernel");
   return RS_OK;
 }
