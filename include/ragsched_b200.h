@@ -336,6 +336,16 @@ int rs_index_set_walk_bias(rs_index* index, int32_t bias);
  * segments keep a segment L2-resident for units that join it late, at the cost
  * of more partial lists to merge. */
 int rs_index_set_segment_rows(rs_index* index, int32_t rows);
+/* The CTA-pair kernel's burst merge (a query's candidates arriving as a burst
+ * in one epilogue lane, e.g. a document's consecutive chunks, merged by the
+ * whole warp).  mode -1 (default): automatic — the lean kernel variant runs
+ * until a search reports more than RS_BURST_ON bursty flushes per
+ * (32 query rows x 256-row tile), then the cooperative variant until the rate
+ * falls below RS_BURST_OFF; 0: always lean; 1: always cooperative.  Both
+ * variants return bit-identical results; only the timing differs.
+ * rs_index_burst_merge_active reports the variant the next search will use. */
+int rs_index_set_burst_merge(rs_index* index, int32_t mode);
+int rs_index_burst_merge_active(rs_index* index, int32_t* active);
 /* Preallocate the search workspace for up to nq_max queries of k results. */
 int rs_index_reserve(rs_index* index, int64_t nq_max, int32_t k);
 /* Search: queries device [nq, dim] of the index dtype; D device [nq,k] fp32,

@@ -751,7 +751,13 @@ struct rs_index {
   void* data = nullptr;
   float* norms = nullptr;
   float* norm_max = nullptr;  // device scalar: max squared norm over the shard
-  int32_t* sched_counter = nullptr;  // pair kernel: [0] unit counter, [1 + s] frontier tile of segment s
+  int32_t* sched_counter = nullptr;  // pair kernel: [0] unit counter, [1] burst count, [2 + s] frontier of segment s
+  // burst merge (rs_index_set_burst_merge): mode, the automatic choice, and the
+  // last pair launch's burst count, copied asynchronously to pinned memory
+  int32_t burst_mode = -1;
+  bool coop_active = false;
+  uint32_t* burst_host = nullptr;
+  double burst_tiles = 0.0;  // (32-row, 256-row) tiles of the launch whose count was copied last
   float* cmin = nullptr;      // [ceil(capacity/256)*8 + 8]: min squared norm per 32-row chunk
   float* lo = nullptr;        // fp32 index: [capacity, dim] tf32 residuals x - trunc_tf32(x) (3xTF32 path)
   float* qlo = nullptr;       // per-search query residuals [qlo_cap, dim]
@@ -840,6 +846,23 @@ rs::SearchPlan make_plan(const rs_index* ix, int algo, int64_t nq, int64_t n, in
                      int64_t(ix->dim) * esize(ix->dtype), true);
 }
 
+// Lean or cooperative pair-kernel variant (rs_index_set_burst_merge).  In the
+// automatic mode the previous launch's burst count (copied to pinned memory
+// without a synchronisation, so possibly one search stale) is normalised by
+// that launch's (32-row, 256-row) tile visits: isotropic data measures
+// ~1e-4 bursty flushes per visit, a doc-contiguous corpus 0.03-0.2
+// (profiles/r2_burst_merge.md).
+constexpr double kBurstOn = 4e-3, kBurstOff = 1e-3;
+bool burst_choice(rs_index* ix) {
+  if (ix->burst_mode >= 0) return ix->burst_mode != 0;
+  if (ix->burst_tiles > 0.0) {
+    const double rate = double(*reinterpret_cast<volatile uint32_t*>(ix->burst_host)) / ix->burst_tiles;
+    if (rate > kBurstOn) ix->coop_active = true;
+    else if (rate < kBurstOff) ix->coop_active = false;
+  }
+  return ix->coop_active;
+}
+
 // partial lists for (queries x this shard) -> part; returns the plan
 int run_partial(rs_index* ix, const void* queries, int64_t nq, int k, int64_t id_base, cudaStream_t st,
                 rs::SearchPlan* plan_out, int algo_for_k = -1) {
@@ -885,12 +908,21 @@ int run_partial(rs_index* ix, const void* queries, int64_t nq, int k, int64_t id
         if (rc) return rc;
       }
     }
-    rc = pair ? launch_score_topk_pair(tmq, tf ? &tmql : nullptr, tmc, (tf && RS_TF32_STORED_LO) ? &tmcl : nullptr,
-                                       ix->qnorm, ix->norms,
-                                       ix->cmin, nq, ix->ntotal, ix->dim, k, id_base, plan, small, ix->part,
-                                       ix->sched_counter, ix->walk_bias, ix->qtau, st)
-              : launch_score_topk_tc(tmq, tmc, ix->qnorm, ix->norms, nq, ix->ntotal, ix->dim, k, id_base, plan,
-                                     ix->part, st);
+    if (pair) {
+      const bool coop = burst_choice(ix);
+      rc = launch_score_topk_pair(tmq, tf ? &tmql : nullptr, tmc, (tf && RS_TF32_STORED_LO) ? &tmcl : nullptr,
+                                  ix->qnorm, ix->norms, ix->cmin, nq, ix->ntotal, ix->dim, k, id_base, plan, small,
+                                  ix->part, ix->sched_counter, ix->walk_bias, ix->qtau, coop, st);
+      if (rc == RS_OK && ix->burst_mode < 0) {  // this launch's count, for the next search's choice
+        RS_CHECK_CUDA(cudaMemcpyAsync(ix->burst_host, ix->sched_counter + 1, sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                                      st),
+                      "cudaMemcpyAsync(burst count)");
+        ix->burst_tiles = double(plan.qtiles) * pair_tile_rows(small) / 32.0 * double(ceil_div(ix->ntotal, kTcBN));
+      }
+    } else {
+      rc = launch_score_topk_tc(tmq, tmc, ix->qnorm, ix->norms, nq, ix->ntotal, ix->dim, k, id_base, plan, ix->part,
+                                st);
+    }
   } else {
     rc = launch_simt(ix->dtype, queries, ix->qnorm, nq, ix->data, ix->norms, ix->ntotal, ix->dim, k, id_base, plan,
                      ix->part, st);
@@ -940,7 +972,9 @@ extern "C" int rs_index_create(int32_t dim, int32_t dtype, int64_t capacity, int
     // granules of norms past the last row of a partial tile
     if (e == cudaSuccess) e = cudaMalloc(&ix->norms, sizeof(float) * (capacity + rs::kTcBN));
     if (e == cudaSuccess) e = cudaMalloc(&ix->norm_max, sizeof(float));
-    if (e == cudaSuccess) e = cudaMalloc(&ix->sched_counter, sizeof(int32_t) * (1 + rs::kMaxSegments));
+    if (e == cudaSuccess) e = cudaMalloc(&ix->sched_counter, sizeof(int32_t) * (2 + rs::kMaxSegments));
+    if (e == cudaSuccess) e = cudaHostAlloc(&ix->burst_host, sizeof(uint32_t), cudaHostAllocDefault);
+    if (e == cudaSuccess) *ix->burst_host = 0;
     if (e == cudaSuccess && dtype == RS_F32 && RS_TF32_STORED_LO && dim % 4 == 0)
       e = cudaMalloc(&ix->lo, size_t(capacity) * dim * sizeof(float));
     if (e == cudaSuccess) e = cudaMalloc(&ix->cmin, sizeof(float) * (rs::ceil_div(capacity, 256) * 8 + 8));
@@ -990,6 +1024,7 @@ extern "C" int rs_index_destroy(rs_index* ix) {
   cudaFree(ix->norms);
   cudaFree(ix->norm_max);
   cudaFree(ix->sched_counter);
+  if (ix->burst_host) cudaFreeHost(ix->burst_host);
   cudaFree(ix->lo);
   cudaFree(ix->cmin);
   cudaFree(ix->qlo);
@@ -1052,6 +1087,27 @@ extern "C" int rs_index_data(const rs_index* ix, const void** emb, const float**
 extern "C" int rs_index_set_segment_rows(rs_index* ix, int32_t rows) {
   RS_REQUIRE(ix != nullptr && rows >= 0, "bad arguments");
   ix->seg_rows_override = rows;
+  return RS_OK;
+}
+
+extern "C" int rs_index_set_burst_merge(rs_index* ix, int32_t mode) {
+  RS_REQUIRE(ix != nullptr, "index is NULL");
+  RS_REQUIRE(mode >= -1 && mode <= 1, "burst merge mode must be -1 (auto), 0 or 1, got %d", mode);
+  ix->burst_mode = mode;
+  ix->burst_tiles = 0.0;
+  if (mode >= 0) ix->coop_active = mode != 0;
+  return RS_OK;
+}
+
+extern "C" int rs_index_burst_merge_active(rs_index* ix, int32_t* active) {
+  RS_REQUIRE(ix != nullptr && active != nullptr, "NULL argument");
+  if (ix->burst_mode >= 0) {
+    *active = ix->burst_mode;
+    return RS_OK;
+  }
+  // the automatic choice the next search makes from the counts copied so far
+  DeviceGuard g(ix->device);
+  *active = burst_choice(ix) ? 1 : 0;
   return RS_OK;
 }
 

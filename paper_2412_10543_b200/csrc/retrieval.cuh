@@ -140,7 +140,8 @@ constexpr int kPairEpiGroups = RS_PAIR_EPI_GROUPS;
 int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap* tmql, const CUtensorMap& tmc,
                            const CUtensorMap* tmcl, const float* qn, const float* cn, const float* cmin, int64_t nq,
                            int64_t n, int dim, int k, int64_t id_base, const SearchPlan& plan, bool small,
-                           uint64_t* part, int32_t* counter, int32_t walk_bias, uint32_t* qtau, cudaStream_t st);
+                           uint64_t* part, int32_t* counter, int32_t walk_bias, uint32_t* qtau, bool coop,
+                           cudaStream_t st);
 // query rows per pair tile: 256, or 128 for the small-batch (M = 128) variant
 int pair_tile_rows(bool small);
 // 32-bit words of shared-bound state per query the pair kernel needs (qtau + cascade)

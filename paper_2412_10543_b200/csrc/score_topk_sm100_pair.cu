@@ -174,7 +174,6 @@ struct Cfg {
   static constexpr uint32_t IDESC = TF ? umma_idesc_tf32_f32(PMv, BN) : umma_idesc_bf16_f32(PMv, BN);
   using Tail = SmemTailT<STAGES>;
   static constexpr int KR = TF ? KREG_TF32 : KREG;  // register top-k capacity
-  using TopK = RegTopK<KR, EPI_THREADS, BUF>;
   static constexpr size_t OFF_BUF = size_t(STAGES) * STAGE_BYTES;
   static constexpr size_t OFF_CN = OFF_BUF + size_t(BUF) * EPI_THREADS * 8;
   static constexpr size_t OFF_SCR = OFF_CN + 2 * BN * sizeof(float);  // per epilogue warp: KR x 8 B (coop_merge)
@@ -195,6 +194,7 @@ struct Params {
   int64_t seg_rows;
   uint64_t* part;
   int32_t* counter;  // dynamic unit counter (zeroed before the launch)
+  uint32_t* bursts;  // flushes that found a burst lane, summed over warps (zeroed; read back by the host)
   int32_t* seg_pos;  // per segment: absolute tile index the most advanced pair last started (zeroed)
   int32_t walk_bias; // test hook: unit of query tile qt starts walk_bias*(qt+1) tiles past the frontier
   uint32_t* qtau;    // per query: best k-th distance bits published by any unit (memset 0xff per search)
@@ -309,7 +309,7 @@ __device__ unsigned long long g_pair_prof[1024][16];
 #define PROF(slot, stmt) stmt
 #endif
 
-template <bool TF, bool SM>
+template <bool TF, bool SM, bool COOP>
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     score_topk_pair_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmql,
                            const __grid_constant__ CUtensorMap tmc, const __grid_constant__ CUtensorMap tmcl,
@@ -584,7 +584,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     const int row = SM ? (ew & 1) * 32 + lane : ew * 32 + lane;
     const int tcol0 = SM ? eg * SLICE : 0;  // tile column held at this accumulator's TMEM column 0
     const int et = (warp - EPI_WARP0) * 32 + lane;
-    typename C::TopK rt;
+    RegTopK<C::KR, EPI_THREADS, BUF, COOP> rt;
     rt.k = p.k;
     rt.wbase = smem_u32(smem + C::OFF_BUF) + uint32_t(et) * 8u;
     rt.sbase = smem_u32(smem + C::OFF_SCR) + uint32_t(warp - EPI_WARP0) * uint32_t(C::KR) * 8u;
@@ -652,9 +652,9 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           return;
 #endif
           if (base + EPI_COLS <= valid)
-            epi_chunk32b<C::KR, EPI_THREADS, BUF, CHECK, true>(rt, r, cn_t + base, id0 + base, EPI_COLS, thr);
+            epi_chunk32b<C::KR, EPI_THREADS, BUF, CHECK, true, COOP>(rt, r, cn_t + base, id0 + base, EPI_COLS, thr);
           else
-            epi_chunk32b<C::KR, EPI_THREADS, BUF, CHECK, false>(rt, r, cn_t + base, id0 + base, valid - base, thr);
+            epi_chunk32b<C::KR, EPI_THREADS, BUF, CHECK, false, COOP>(rt, r, cn_t + base, id0 + base, valid - base, thr);
         };
 #if RS_PAIR_EPI_PAIRED
         // two 32-column loads in flight per wait (4 waits per 256-column tile)
@@ -721,6 +721,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 #endif
       if (qrow < p.nq) rt.finish(p.part + ((qrow * p.segments + seg) * C::LPS + eg) * p.k);
     }
+    if (lane == 0 && rt.bursts) atomicAdd(p.bursts, rt.bursts);  // the host's lean / cooperative choice
 #if RS_PAIR_PROFILE && RS_TOPK_COUNTERS
     if (blockIdx.x < 1024) {
       const uint32_t cnt[5] = {rt.c_groups, rt.c_appends, rt.c_flushes, rt.c_inserts, rt.c_coop};
@@ -765,11 +766,11 @@ extern "C" int rs_debug_pair_profile_reset() {
 
 namespace {
 
-template <bool TF, bool SM>
+template <bool TF, bool SM, bool COOP>
 int set_smem_attr() {
   static bool done = false;
   if (!done) {
-    RS_CHECK_CUDA(cudaFuncSetAttribute(score_topk_pair_kernel<TF, SM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    RS_CHECK_CUDA(cudaFuncSetAttribute(score_topk_pair_kernel<TF, SM, COOP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        int(Cfg<TF, SM>::SMEM_BYTES)),
                   "cudaFuncSetAttribute(score_topk_pair_kernel)");
     done = true;
@@ -777,12 +778,13 @@ int set_smem_attr() {
   return RS_OK;
 }
 
-template <bool TF, bool SM>
+template <bool TF, bool SM, bool COOP>
 int launch_t(const CUtensorMap& tmq, const CUtensorMap& tmql, const CUtensorMap& tmc, const CUtensorMap& tmcl,
              const Params& p, int ctas, cudaStream_t st) {
-  int rc = set_smem_attr<TF, SM>();
+  int rc = set_smem_attr<TF, SM, COOP>();
   if (rc) return rc;
-  score_topk_pair_kernel<TF, SM><<<CL * ctas, NUM_THREADS, Cfg<TF, SM>::SMEM_BYTES, st>>>(tmq, tmql, tmc, tmcl, p);
+  score_topk_pair_kernel<TF, SM, COOP>
+      <<<CL * ctas, NUM_THREADS, Cfg<TF, SM>::SMEM_BYTES, st>>>(tmq, tmql, tmc, tmcl, p);
   RS_CHECK_LAUNCH("score_topk_pair_kernel");
   return RS_OK;
 }
@@ -794,7 +796,8 @@ int pair_tile_rows(bool small) { return small ? Cfg<false, true>::PMv : Cfg<fals
 int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap* tmql, const CUtensorMap& tmc,
                            const CUtensorMap* tmcl, const float* qn, const float* cn, const float* cmin, int64_t nq,
                            int64_t n, int dim, int k, int64_t id_base, const SearchPlan& plan, bool small,
-                           uint64_t* part, int32_t* counter, int32_t walk_bias, uint32_t* qtau, cudaStream_t st) {
+                           uint64_t* part, int32_t* counter, int32_t walk_bias, uint32_t* qtau, bool coop,
+                           cudaStream_t st) {
   const bool tf = tmql != nullptr;
   RS_REQUIRE(!tf || !RS_TF32_STORED_LO || tmcl != nullptr, "tf32 path with stored residuals needs the corpus lo map");
   RS_REQUIRE(!tf || G == 1, "the tf32 path has no multicast (RS_PAIR_GROUP) variant");
@@ -805,8 +808,8 @@ int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap* tmql, cons
   RS_REQUIRE(!small || EG == 1, "the M = 128 variant has one epilogue warp group");
   RS_REQUIRE(plan.lists_per_seg == (small ? 2 : kPairEpiGroups), "plan lists per segment do not match the kernel");
   RS_REQUIRE(plan.segments >= 1 && plan.segments <= kMaxSegments, "segments out of range (%d)", plan.segments);
-  RS_CHECK_CUDA(cudaMemsetAsync(counter, 0, sizeof(int32_t) * (1 + plan.segments), st),
-                "cudaMemsetAsync(unit counter, segment frontiers)");
+  RS_CHECK_CUDA(cudaMemsetAsync(counter, 0, sizeof(int32_t) * (2 + plan.segments), st),
+                "cudaMemsetAsync(unit counter, burst count, segment frontiers)");
   RS_CHECK_CUDA(cudaMemsetAsync(qtau, 0xff, sizeof(uint32_t) * size_t(nq) * (1 + kCas), st),
                 "cudaMemsetAsync(shared bounds)");
   Params p{};
@@ -826,7 +829,8 @@ int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap* tmql, cons
   p.seg_rows = plan.seg_rows;
   p.part = part;
   p.counter = counter;
-  p.seg_pos = counter + 1;
+  p.bursts = reinterpret_cast<uint32_t*>(counter + 1);
+  p.seg_pos = counter + 2;
   p.walk_bias = walk_bias;
   p.qtau = qtau;
   p.qcas = qtau + nq;  // the caller allocates nq * (1 + kCas) words
@@ -834,10 +838,16 @@ int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap* tmql, cons
   p.cunits = int64_t(plan.qtiles) * plan.segments;
   const CUtensorMap& ql = tf ? *tmql : tmq;
   const CUtensorMap& cl = (tf && tmcl) ? *tmcl : tmc;
-  if (tf) return small ? launch_t<true, true>(tmq, ql, tmc, cl, p, plan.ctas, st)
-                       : launch_t<true, false>(tmq, ql, tmc, cl, p, plan.ctas, st);
-  return small ? launch_t<false, true>(tmq, ql, tmc, cl, p, plan.ctas, st)
-               : launch_t<false, false>(tmq, ql, tmc, cl, p, plan.ctas, st);
+  if (coop) {
+    if (tf) return small ? launch_t<true, true, true>(tmq, ql, tmc, cl, p, plan.ctas, st)
+                         : launch_t<true, false, true>(tmq, ql, tmc, cl, p, plan.ctas, st);
+    return small ? launch_t<false, true, true>(tmq, ql, tmc, cl, p, plan.ctas, st)
+                 : launch_t<false, false, true>(tmq, ql, tmc, cl, p, plan.ctas, st);
+  }
+  if (tf) return small ? launch_t<true, true, false>(tmq, ql, tmc, cl, p, plan.ctas, st)
+                       : launch_t<true, false, false>(tmq, ql, tmc, cl, p, plan.ctas, st);
+  return small ? launch_t<false, true, false>(tmq, ql, tmc, cl, p, plan.ctas, st)
+               : launch_t<false, false, false>(tmq, ql, tmc, cl, p, plan.ctas, st);
 }
 
 }  // namespace rs

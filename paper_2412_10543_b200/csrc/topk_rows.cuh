@@ -292,7 +292,9 @@ __device__ __noinline__ void coop_sort64(uint32_t scr, uint32_t sbuf, int ns, ui
   __syncwarp();
 }
 
-template <int KREG, int ROWS, int BUF>
+// COOP = false: the same list without the cooperative merge code (the lean
+// kernel variant; its flushes still count bursts, see flush()).
+template <int KREG, int ROWS, int BUF, bool COOP = true>
 struct RegTopK {
   uint32_t key[KREG];  // (distance bits << 1) | phase
   uint32_t id[KREG];
@@ -302,6 +304,7 @@ struct RegTopK {
   uint32_t seedk; // shared-threshold seed (see seed()), kEmpty when none
   uint32_t kthk;  // key of the current k-th best (kEmpty until k entries)
   uint32_t phase; // 1 until the walk wraps to lower ids, then 0
+  uint32_t bursts = 0;  // flushes that found a burst lane (warp-uniform; the host's variant choice)
   float qn;       // this row's |q|^2
   uint32_t wbase; // shared-window byte address of this row's buffer slot 0
   uint32_t wp;    // next free buffer slot
@@ -419,21 +422,28 @@ struct RegTopK {
   // Lockstep costs the warp one KREG-wide sweep per candidate of its FULLEST
   // lane, so a lane that holds RS_TOPK_COOP_GAIN or more candidates beyond
   // every other lane (a burst) is merged cooperatively first, fullest first.
-  template <bool COOP = true>
+  // SITE = false: a flush site that never merges cooperatively (nor counts).
+  template <bool SITE = true>
   __device__ __forceinline__ void flush() {
     int n = buffered();
 #if RS_TOPK_COOP
-    const int lane = int(threadIdx.x & 31);
+    if (SITE) {
+      const int lane = int(threadIdx.x & 31);
+      bool first = true;
 #pragma unroll 1
-    for (; COOP;) {
-      const int top = __reduce_max_sync(0xffffffffu, n);
-      if (top < RS_TOPK_COOP) break;
-      const int src = __ffs(__ballot_sync(0xffffffffu, n == top)) - 1;
-      const int second = __reduce_max_sync(0xffffffffu, lane == src ? 0 : n);
-      if (top - second < RS_TOPK_COOP_GAIN) break;
-      RS_TOPK_COUNT(c_coop, 1);
-      coop_merge(src, top, __shfl_sync(0xffffffffu, ktau, src));
-      if (lane == src) n = 0;
+      for (;;) {
+        const int top = __reduce_max_sync(0xffffffffu, n);
+        if (top < RS_TOPK_COOP) break;
+        const int src = __ffs(__ballot_sync(0xffffffffu, n == top)) - 1;
+        const int second = __reduce_max_sync(0xffffffffu, lane == src ? 0 : n);
+        if (top - second < RS_TOPK_COOP_GAIN) break;
+        if (first) ++bursts;
+        first = false;
+        if constexpr (!COOP) break;
+        RS_TOPK_COUNT(c_coop, 1);
+        coop_merge(src, top, __shfl_sync(0xffffffffu, ktau, src));
+        if (lane == src) n = 0;
+      }
     }
 #endif
     const int nmax = __reduce_max_sync(0xffffffffu, n);
@@ -466,8 +476,8 @@ struct RegTopK {
 
 // Exact distances and predicated appends of 8 columns for RegTopK (the slow
 // path of epi_chunk32b).
-template <int KREG, int ROWS, int BUF, int CHECK, bool FULL, bool CHK = true>
-__device__ __forceinline__ void epi_group8r(RegTopK<KREG, ROWS, BUF>& rt, const uint32_t* r, const float* cn,
+template <int KREG, int ROWS, int BUF, int CHECK, bool FULL, bool CHK = true, bool COOP = true>
+__device__ __forceinline__ void epi_group8r(RegTopK<KREG, ROWS, BUF, COOP>& rt, const uint32_t* r, const float* cn,
                                             uint32_t id, int lim) {
   static_assert(BUF >= CHECK, "buffer must hold the groups between two checks");
   RS_TOPK_COUNT(rt.c_groups, 1);
@@ -503,8 +513,8 @@ __device__ __forceinline__ void epi_group8r(RegTopK<KREG, ROWS, BUF>& rt, const 
 // of the warp has a candidate anywhere in the chunk (a one-warp-per-SMSP
 // epilogue is latency-bound, so the short dependency chains and the single
 // branch matter more than the instruction count).
-template <int KREG, int ROWS, int BUF, int CHECK, bool FULL>
-__device__ __forceinline__ void epi_chunk32b(RegTopK<KREG, ROWS, BUF>& rt, const uint32_t* r, const float* cn,
+template <int KREG, int ROWS, int BUF, int CHECK, bool FULL, bool COOP>
+__device__ __forceinline__ void epi_chunk32b(RegTopK<KREG, ROWS, BUF, COOP>& rt, const uint32_t* r, const float* cn,
                                              uint32_t id, int lim, float thr) {
   float m[4];
 #pragma unroll
@@ -524,9 +534,9 @@ __device__ __forceinline__ void epi_chunk32b(RegTopK<KREG, ROWS, BUF>& rt, const
   for (int g = 0; g < 4; ++g)
     if (hit & (1u << g)) {
       if (FULL)
-        epi_group8r<KREG, ROWS, BUF, CHECK, true>(rt, r + g * 8, cn + g * 8, id + g * 8, 8);
+        epi_group8r<KREG, ROWS, BUF, CHECK, true, true, COOP>(rt, r + g * 8, cn + g * 8, id + g * 8, 8);
       else
-        epi_group8r<KREG, ROWS, BUF, CHECK, false>(rt, r + g * 8, cn + g * 8, id + g * 8, lim - g * 8);
+        epi_group8r<KREG, ROWS, BUF, CHECK, false, true, COOP>(rt, r + g * 8, cn + g * 8, id + g * 8, lim - g * 8);
     }
 #else
   // one buffer check per two groups (half the inlined flush sites; CHECK
@@ -535,9 +545,9 @@ __device__ __forceinline__ void epi_chunk32b(RegTopK<KREG, ROWS, BUF>& rt, const
   for (int g = 0; g < 4; ++g) {
     if (hit & (1u << g)) {
       if (FULL)
-        epi_group8r<KREG, ROWS, BUF, CHECK, true, false>(rt, r + g * 8, cn + g * 8, id + g * 8, 8);
+        epi_group8r<KREG, ROWS, BUF, CHECK, true, false, COOP>(rt, r + g * 8, cn + g * 8, id + g * 8, 8);
       else
-        epi_group8r<KREG, ROWS, BUF, CHECK, false, false>(rt, r + g * 8, cn + g * 8, id + g * 8, lim - g * 8);
+        epi_group8r<KREG, ROWS, BUF, CHECK, false, false, COOP>(rt, r + g * 8, cn + g * 8, id + g * 8, lim - g * 8);
     }
     if ((g & 1) && (hit & (3u << (g - 1))) && __any_sync(0xffffffffu, rt.buffered() > BUF - CHECK)) rt.flush();
   }

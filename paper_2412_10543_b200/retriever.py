@@ -85,6 +85,20 @@ class IndexFlatL2:
         """Tuning knob: corpus rows per segment of the CTA-pair schedule (0 = auto)."""
         _lib.check(self._lib.rs_index_set_segment_rows(self._h, int(rows)))
 
+    def set_burst_merge(self, mode: str | int) -> None:
+        """The pair kernel's cooperative burst merge: "auto" (default; the lean
+        variant until searches report bursts — a document's consecutive chunks
+        landing in one epilogue lane — then the cooperative one), "off"/0 or
+        "on"/1.  Results are bit-identical in every mode."""
+        m = {"auto": -1, "off": 0, "on": 1}.get(mode, mode)
+        _lib.check(self._lib.rs_index_set_burst_merge(self._h, int(m)))
+
+    def burst_merge_active(self) -> bool:
+        """Whether the next search runs the cooperative variant."""
+        v = ctypes.c_int32(0)
+        _lib.check(self._lib.rs_index_burst_merge_active(self._h, ctypes.byref(v)))
+        return bool(v.value)
+
     def set_walk_bias(self, bias: int) -> None:
         """Test hook: start every pair-kernel unit past its segment frontier
         (exercises the wrap-around, out-of-id-order top-k path)."""

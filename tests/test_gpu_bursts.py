@@ -111,3 +111,50 @@ def test_mixed_burst_sizes_in_one_warp(bias, dtype):
         assert np.all(D[r, :sz] == D[r, 0])
     res = ro.check_topk(D, I, q, c, k, RTOL[dtype])
     assert not res["violations"], res["violations"][:5]
+
+
+def _index(c, mode):
+    ix = IndexFlatL2(c.shape[1], dtype=c.dtype, capacity=c.shape[0])
+    ix.set_algo("tcgen05")
+    ix.set_burst_merge(mode)
+    ix.add(c.cuda())
+    return ix
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("data", ["doc_contiguous", "iso"])
+def test_lean_and_cooperative_variants_are_bit_identical(data, dtype):
+    """The lean kernel (no cooperative merge) and the cooperative one return
+    the same keys bit for bit, and the automatic mode equals both."""
+    n, d, k, nq = 200_000, 256, 35, 700
+    c = synth.corpus_rows(0, n, d, 3, dtype, "cuda", data).cpu()
+    q = synth.make_queries(nq, n, d, 3, dtype, data).cuda()
+    out = {}
+    for mode in ("off", "on", "auto"):
+        ix = _index(c, mode)
+        keys = [ix.search_keys(q, k).cpu() for _ in range(3)]  # auto may switch variants between searches
+        torch.cuda.synchronize()
+        ix.close()
+        for t in keys[1:]:
+            assert torch.equal(t, keys[0]), mode
+        out[mode] = keys[0]
+    assert torch.equal(out["off"], out["on"]) and torch.equal(out["auto"], out["on"])
+
+
+def test_auto_mode_switches_on_bursty_corpora_only():
+    """Automatic choice: a doc-contiguous corpus turns the cooperative variant
+    on after one search; an isotropic one keeps the lean variant."""
+    n, d, k, nq = 400_000, 256, 35, 2048
+    for data, want in (("doc_contiguous", True), ("iso", False)):
+        c = synth.corpus_rows(0, n, d, 5, torch.bfloat16, "cuda", data).cpu()
+        q = synth.make_queries(nq, n, d, 5, torch.bfloat16, data).cuda()
+        ix = _index(c, "auto")
+        assert not ix.burst_merge_active()  # lean until a search reports bursts
+        ix.search_keys(q, k)
+        torch.cuda.synchronize()
+        assert ix.burst_merge_active() == want, data
+        ix.set_burst_merge("on")
+        assert ix.burst_merge_active()
+        ix.set_burst_merge("off")
+        assert not ix.burst_merge_active()
+        ix.close()
