@@ -751,9 +751,9 @@ struct rs_index {
   void* data = nullptr;
   float* norms = nullptr;
   float* norm_max = nullptr;  // device scalar: max squared norm over the shard
-  int32_t* sched_counter = nullptr;  // pair kernel: [0] unit counter, [1] burst count, [2 + s] frontier of segment s
+  int32_t* sched_counter = nullptr;  // pair kernel: [0] units, [1] bursts, [2] finished CTAs, [3 + s] frontier of segment s
   // burst merge (rs_index_set_burst_merge): mode, the automatic choice, and the
-  // last pair launch's burst count, copied asynchronously to pinned memory
+  // last pair launch's burst count, posted by its last CTA to pinned memory
   int32_t burst_mode = -1;
   bool coop_active = false;
   uint32_t* burst_host = nullptr;
@@ -847,8 +847,8 @@ rs::SearchPlan make_plan(const rs_index* ix, int algo, int64_t nq, int64_t n, in
 }
 
 // Lean or cooperative pair-kernel variant (rs_index_set_burst_merge).  In the
-// automatic mode the previous launch's burst count (copied to pinned memory
-// without a synchronisation, so possibly one search stale) is normalised by
+// automatic mode the previous launch's burst count (posted to pinned memory by
+// its last CTA; read without a synchronisation, so possibly one search stale) is normalised by
 // that launch's (32-row, 256-row) tile visits: isotropic data measures
 // ~1e-4 bursty flushes per visit, a doc-contiguous corpus 0.03-0.2
 // (profiles/r2_burst_merge.md).
@@ -910,15 +910,13 @@ int run_partial(rs_index* ix, const void* queries, int64_t nq, int k, int64_t id
     }
     if (pair) {
       const bool coop = burst_choice(ix);
+      const bool count = ix->burst_mode < 0;  // automatic: this launch's count, for the next search's choice
       rc = launch_score_topk_pair(tmq, tf ? &tmql : nullptr, tmc, (tf && RS_TF32_STORED_LO) ? &tmcl : nullptr,
                                   ix->qnorm, ix->norms, ix->cmin, nq, ix->ntotal, ix->dim, k, id_base, plan, small,
-                                  ix->part, ix->sched_counter, ix->walk_bias, ix->qtau, coop, st);
-      if (rc == RS_OK && ix->burst_mode < 0) {  // this launch's count, for the next search's choice
-        RS_CHECK_CUDA(cudaMemcpyAsync(ix->burst_host, ix->sched_counter + 1, sizeof(uint32_t), cudaMemcpyDeviceToHost,
-                                      st),
-                      "cudaMemcpyAsync(burst count)");
+                                  ix->part, ix->sched_counter, ix->walk_bias, ix->qtau, coop,
+                                  count ? ix->burst_host : nullptr, st);
+      if (rc == RS_OK && count)
         ix->burst_tiles = double(plan.qtiles) * pair_tile_rows(small) / 32.0 * double(ceil_div(ix->ntotal, kTcBN));
-      }
     } else {
       rc = launch_score_topk_tc(tmq, tmc, ix->qnorm, ix->norms, nq, ix->ntotal, ix->dim, k, id_base, plan, ix->part,
                                 st);
@@ -972,7 +970,7 @@ extern "C" int rs_index_create(int32_t dim, int32_t dtype, int64_t capacity, int
     // granules of norms past the last row of a partial tile
     if (e == cudaSuccess) e = cudaMalloc(&ix->norms, sizeof(float) * (capacity + rs::kTcBN));
     if (e == cudaSuccess) e = cudaMalloc(&ix->norm_max, sizeof(float));
-    if (e == cudaSuccess) e = cudaMalloc(&ix->sched_counter, sizeof(int32_t) * (2 + rs::kMaxSegments));
+    if (e == cudaSuccess) e = cudaMalloc(&ix->sched_counter, sizeof(int32_t) * (3 + rs::kMaxSegments));
     if (e == cudaSuccess) e = cudaHostAlloc(&ix->burst_host, sizeof(uint32_t), cudaHostAllocDefault);
     if (e == cudaSuccess) *ix->burst_host = 0;
     if (e == cudaSuccess && dtype == RS_F32 && RS_TF32_STORED_LO && dim % 4 == 0)

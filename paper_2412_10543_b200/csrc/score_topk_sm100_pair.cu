@@ -194,7 +194,9 @@ struct Params {
   int64_t seg_rows;
   uint64_t* part;
   int32_t* counter;  // dynamic unit counter (zeroed before the launch)
-  uint32_t* bursts;  // flushes that found a burst lane, summed over warps (zeroed; read back by the host)
+  uint32_t* bursts;  // flushes that found a burst lane, summed over warps (zeroed)
+  int32_t* done;     // CTAs finished (zeroed): the last one posts *bursts to bursts_host
+  uint32_t* bursts_host;  // pinned host word (device-accessible under unified addressing) or null
   int32_t* seg_pos;  // per segment: absolute tile index the most advanced pair last started (zeroed)
   int32_t walk_bias; // test hook: unit of query tile qt starts walk_bias*(qt+1) tiles past the frontier
   uint32_t* qtau;    // per query: best k-th distance bits published by any unit (memset 0xff per search)
@@ -591,6 +593,9 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tail->tempty[0]), pair_leader);
     const uint32_t tempty_leader1 = mapa_shared(smem_u32(&tail->tempty[1]), pair_leader);
     uint32_t tile_iter = 0;
+#if RS_PAIR_PROFILE
+    unsigned long long busy_all = 0, busy_early = 0, n_early = 0;
+#endif
     for (uint32_t i = 0;; ++i) {
       int32_t start;
       const int u = next_unit(tail, i, scheduler, false, start);
@@ -631,6 +636,9 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         const float4 cm1 = __ldg(reinterpret_cast<const float4*>(p.cmin + (c0 >> 5)) + 1);
         PROF(3, mbar_wait(&tail->tfull[acc], (tile_iter >> 1) & 1));
         tc_fence_after();
+#if RS_PAIR_PROFILE
+        const long long t_tile0 = clock64();
+#endif
         const uint32_t t_row = tmem_base + (uint32_t(ew * 32) << 16) + acc * C::ACC_COLS - tcol0;
         const uint32_t id0 = uint32_t(p.id_base + c0);
         // this chunk's dot bound (epi_chunk32b)
@@ -692,6 +700,16 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           rt.seed(tau_pending);
         }
 #endif
+#if RS_PAIR_PROFILE
+        {  // busy epilogue cycles of this tile: the first 4 tiles of a unit vs all
+          const long long dt = clock64() - t_tile0;
+          busy_all += dt;
+          if (j < 4) {
+            busy_early += dt;
+            ++n_early;
+          }
+        }
+#endif
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
@@ -733,6 +751,13 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       }
     }
 #endif
+#if RS_PAIR_PROFILE
+    if (lane == 0 && blockIdx.x < 1024) {  // [13] busy cycles in a unit's first 4 tiles, [14] in all, [15] first-4 tiles
+      atomicAdd(&g_pair_prof[blockIdx.x][13], busy_early);
+      atomicAdd(&g_pair_prof[blockIdx.x][14], busy_all);
+      atomicAdd(&g_pair_prof[blockIdx.x][15], n_early);
+    }
+#endif
   }
 #if RS_PAIR_PROFILE
   prof[7] = clock64() - t_start;
@@ -748,6 +773,16 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   if (warp == WARP_TMEM) {
     tc_fence_after();
     tmem_dealloc_pair(tmem_base, TMEM_COLS);
+  }
+  // the last CTA to finish posts the launch's burst count straight to pinned
+  // host memory (the host's lean / cooperative choice for the next search):
+  // no copy in the stream, no synchronisation
+  if (p.bursts_host && threadIdx.x == 0) {  // every warp of this CTA added its count before cluster_sync
+    __threadfence();
+    if (atomicAdd(p.done, 1) == int(gridDim.x) - 1) {
+      __threadfence();
+      *reinterpret_cast<volatile uint32_t*>(p.bursts_host) = atomicAdd(p.bursts, 0u);
+    }
   }
 }
 
@@ -797,7 +832,7 @@ int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap* tmql, cons
                            const CUtensorMap* tmcl, const float* qn, const float* cn, const float* cmin, int64_t nq,
                            int64_t n, int dim, int k, int64_t id_base, const SearchPlan& plan, bool small,
                            uint64_t* part, int32_t* counter, int32_t walk_bias, uint32_t* qtau, bool coop,
-                           cudaStream_t st) {
+                           uint32_t* bursts_host, cudaStream_t st) {
   const bool tf = tmql != nullptr;
   RS_REQUIRE(!tf || !RS_TF32_STORED_LO || tmcl != nullptr, "tf32 path with stored residuals needs the corpus lo map");
   RS_REQUIRE(!tf || G == 1, "the tf32 path has no multicast (RS_PAIR_GROUP) variant");
@@ -808,8 +843,8 @@ int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap* tmql, cons
   RS_REQUIRE(!small || EG == 1, "the M = 128 variant has one epilogue warp group");
   RS_REQUIRE(plan.lists_per_seg == (small ? 2 : kPairEpiGroups), "plan lists per segment do not match the kernel");
   RS_REQUIRE(plan.segments >= 1 && plan.segments <= kMaxSegments, "segments out of range (%d)", plan.segments);
-  RS_CHECK_CUDA(cudaMemsetAsync(counter, 0, sizeof(int32_t) * (2 + plan.segments), st),
-                "cudaMemsetAsync(unit counter, burst count, segment frontiers)");
+  RS_CHECK_CUDA(cudaMemsetAsync(counter, 0, sizeof(int32_t) * (3 + plan.segments), st),
+                "cudaMemsetAsync(unit counter, burst count, finished CTAs, segment frontiers)");
   RS_CHECK_CUDA(cudaMemsetAsync(qtau, 0xff, sizeof(uint32_t) * size_t(nq) * (1 + kCas), st),
                 "cudaMemsetAsync(shared bounds)");
   Params p{};
@@ -830,7 +865,9 @@ int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap* tmql, cons
   p.part = part;
   p.counter = counter;
   p.bursts = reinterpret_cast<uint32_t*>(counter + 1);
-  p.seg_pos = counter + 2;
+  p.done = counter + 2;
+  p.bursts_host = bursts_host;
+  p.seg_pos = counter + 3;
   p.walk_bias = walk_bias;
   p.qtau = qtau;
   p.qcas = qtau + nq;  // the caller allocates nq * (1 + kCas) words

@@ -86,6 +86,14 @@ def main():
     c = arr[:, 8:13].sum(0)
     out["per_warp_tile"] = {nm: round(float(c[i - 8]) / warp_tiles, 4) for i, nm in COUNTERS.items()}
     out["appends_per_query"] = round(float(c[1]) / nq, 1)
+    busy_early, busy_all, n_early = arr[:, 13].sum(), arr[:, 14].sum(), arr[:, 15].sum()
+    if busy_all > 0:
+        out["epilogue_busy"] = {"first4_share": round(float(busy_early / busy_all), 4),
+                                "first4_cycles_per_tile": round(float(busy_early / max(n_early, 1)), 1),
+                                "other_cycles_per_tile": round(float((busy_all - busy_early) /
+                                                                     max(warp_tiles - n_early, 1)), 1),
+                                "first4_tile_share": round(float(n_early / warp_tiles), 4)}
+        print("epilogue busy cycles:", out["epilogue_busy"])
     print("epilogue events per (32 query rows, 256-row corpus tile):", out["per_warp_tile"])
     print("candidate appends per query:", out["appends_per_query"])
     print(json.dumps(out))
