@@ -176,8 +176,8 @@ struct Cfg {
   static constexpr int KR = TF ? KREG_TF32 : KREG;  // register top-k capacity
   static constexpr size_t OFF_BUF = size_t(STAGES) * STAGE_BYTES;
   static constexpr size_t OFF_CN = OFF_BUF + size_t(BUF) * EPI_THREADS * 8;
-  static constexpr size_t OFF_SCR = OFF_CN + 2 * BN * sizeof(float);  // per epilogue warp: KR x 8 B (coop_merge)
-  static constexpr size_t OFF_TAIL = OFF_SCR + size_t(EPI_THREADS / 32) * KR * 8;
+  static constexpr size_t OFF_SCR = OFF_CN + 2 * BN * sizeof(float);  // per epilogue warp: (KR + BUF) x 8 B (coop_merge)
+  static constexpr size_t OFF_TAIL = OFF_SCR + size_t(EPI_THREADS / 32) * (KR + BUF) * 8;
   static constexpr size_t SMEM_BYTES = OFF_TAIL + sizeof(Tail);
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
 };
@@ -589,7 +589,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     RegTopK<C::KR, EPI_THREADS, BUF, COOP> rt;
     rt.k = p.k;
     rt.wbase = smem_u32(smem + C::OFF_BUF) + uint32_t(et) * 8u;
-    rt.sbase = smem_u32(smem + C::OFF_SCR) + uint32_t(warp - EPI_WARP0) * uint32_t(C::KR) * 8u;
+    rt.sbase = smem_u32(smem + C::OFF_SCR) + uint32_t(warp - EPI_WARP0) * uint32_t(C::KR + BUF) * 8u;
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tail->tempty[0]), pair_leader);
     const uint32_t tempty_leader1 = mapa_shared(smem_u32(&tail->tempty[1]), pair_leader);
     uint32_t tile_iter = 0;

@@ -208,6 +208,9 @@ __device__ __forceinline__ void epi_group8(RowTopK<ROWS, BUF>& rt, const uint32_
 #ifndef RS_TOPK_COOP
 #define RS_TOPK_COOP 6  // buffered candidates from which a lane may be merged cooperatively (0 = never)
 #endif
+#ifndef RS_TOPK_COOP_RANK
+#define RS_TOPK_COOP_RANK 1  // cooperative merge by slot ranks (1) or by a bitonic sort of all elements (0)
+#endif
 #ifndef RS_TOPK_CHECK_GROUPS
 #define RS_TOPK_CHECK_GROUPS 2  // 8-column groups per buffer check in epi_chunk32b (1 or 2)
 #endif
@@ -289,6 +292,60 @@ __device__ __noinline__ void coop_sort64(uint32_t scr, uint32_t sbuf, int ns, ui
                    "r"(uint32_t(v[s]))
                    : "memory");
   }
+  __syncwarp();
+}
+
+// Rank merge (the default cooperative merge, RS_TOPK_COOP_RANK = 1): the
+// list is already sorted, so instead of sorting all KREG + n elements each
+// element's output slot is computed directly.  Lane t < n holds buffer entry
+// t (admitted or kEmpty), lanes hold list entries t and t + 32; a list entry
+// lands at its index plus the buffer keys below it, a buffer entry at the
+// buffer keys below it (ties by index) plus the list keys at or below it.
+// Two loops of shared-memory broadcasts (n + KREG compares per lane) instead
+// of a 21-stage shuffle network.  Keys are unique except kEmpty padding, and
+// the tie rules make the slots a permutation.
+template <int KREG, int ROWS, int BUF>
+__device__ __noinline__ void coop_rank_merge(uint32_t scr, uint32_t sbuf, int ns, uint32_t kt, uint32_t ph) {
+  static_assert(KREG <= 64 && BUF <= 32, "rank merge: two list entries and one buffer entry per lane");
+  constexpr unsigned long long kE = (static_cast<unsigned long long>(0xff000001u) << 32) | 0xffffffffu;
+  const int lane = int(threadIdx.x & 31);
+  const uint32_t bscr = scr + KREG * 8;  // BUF packed buffer keys after the list
+  auto ld_entry = [](uint32_t addr) -> unsigned long long {
+    uint32_t a, b;
+    asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(a), "=r"(b) : "r"(addr));
+    return (static_cast<unsigned long long>(a) << 32) | b;
+  };
+  unsigned long long bv = kE;
+  if (lane < ns) {
+    uint32_t cid, dbits;
+    asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(cid), "=r"(dbits) : "r"(sbuf + lane * ROWS * 8));
+    // clamp negative round-off (and -0, NaN) to +0, as the lockstep flush
+    const uint32_t xk = ((__uint_as_float(dbits) > 0.0f ? dbits : 0u) << 1) | ph;
+    if (xk < kt) bv = (static_cast<unsigned long long>(xk) << 32) | cid;
+  }
+  if (lane < ns)
+    asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(bscr + lane * 8), "r"(uint32_t(bv >> 32)), "r"(uint32_t(bv))
+                 : "memory");
+  const unsigned long long l0 = lane < KREG ? ld_entry(scr + lane * 8) : kE;
+  const unsigned long long l1 = lane + 32 < KREG ? ld_entry(scr + (lane + 32) * 8) : kE;
+  __syncwarp();
+  int pb = 0, p0 = lane, p1 = lane + 32;
+#pragma unroll 4
+  for (int i = 0; i < ns; ++i) {
+    const unsigned long long b = ld_entry(bscr + i * 8);
+    pb += (b < bv || (b == bv && i < lane)) ? 1 : 0;
+    p0 += b < l0 ? 1 : 0;
+    p1 += b < l1 ? 1 : 0;
+  }
+#pragma unroll 8
+  for (int j = 0; j < KREG; ++j) pb += ld_entry(scr + j * 8) <= bv ? 1 : 0;
+  __syncwarp();  // every lane read the list before it is rewritten
+  auto st_entry = [](uint32_t addr, unsigned long long v) {
+    asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(addr), "r"(uint32_t(v >> 32)), "r"(uint32_t(v)) : "memory");
+  };
+  if (lane < ns && pb < KREG) st_entry(scr + pb * 8, bv);
+  if (lane < KREG && p0 < KREG) st_entry(scr + p0 * 8, l0);
+  if (lane + 32 < KREG && p1 < KREG) st_entry(scr + p1 * 8, l1);
   __syncwarp();
 }
 
@@ -395,7 +452,7 @@ struct RegTopK {
   // whole warp (coop_sort64 below): lane src publishes its KREG sorted
   // entries to the warp's scratch, the warp sorts them with src's admitted
   // buffer entries, src reloads the first KREG.
-  uint32_t sbase;  // shared-window byte address of this warp's 64 x 8-byte scratch
+  uint32_t sbase;  // shared-window byte address of this warp's (KREG + BUF) x 8-byte scratch
   __device__ __forceinline__ void coop_merge(int src, int ns, uint32_t kt) {
     const int lane = int(threadIdx.x & 31);
     if (lane == src) {
@@ -406,7 +463,11 @@ struct RegTopK {
                      : "memory");
     }
     __syncwarp();
+#if RS_TOPK_COOP_RANK
+    coop_rank_merge<KREG, ROWS, BUF>(sbase, wbase + uint32_t(src - lane) * 8u, ns, kt, phase);
+#else
     coop_sort64<KREG, ROWS, BUF>(sbase, wbase + uint32_t(src - lane) * 8u, ns, kt, phase);
+#endif
     if (lane == src) {
 #pragma unroll
       for (int j = 0; j < KREG; j += 2)
