@@ -246,6 +246,22 @@ enum rs_parse_status { RS_PARSE_OK = 0, RS_PARSE_UNPARSEABLE = 1 };
 enum rs_clamped_bits { RS_CLAMPED_PIECES = 1, RS_CLAMPED_SUMMARY = 2 };
 int rs_parse_profiles(const char* text, const int64_t* offsets, int64_t n, const double* confidence,
                       rs_profile* out, uint8_t* clamped, int32_t* line_numbers, uint8_t* status, int32_t nthreads);
+/* Per-field answer confidences (_per_field_confidences, profiler.py:427-464;
+ * the remote estimator's gate confidence is their minimum, :417-418): answer
+ * i (text[offsets[i] .. offsets[i+1]), UTF-8) came with the tokens
+ * [tok_offsets[i], tok_offsets[i+1]); token t's text is
+ * tok_text[tok_text_offsets[t] .. tok_text_offsets[t+1]) (UTF-8, its length
+ * counts code points) and its log-prob tok_lp[t] (tok_has_lp[t] = 0: None).
+ * Each token falls on the answer line (str.splitlines(keepends=True)) its
+ * starting character offset lies in; a field's confidence is exp(mean of its
+ * line's log-probs) — the mean as CPython 3.12's sum() computes it
+ * (Neumaier-compensated), then math.exp — or 1.0 without log-probs.  Answers
+ * with no tokens or that do not parse give 1.0 for every field.  out: n x 4
+ * doubles (complexity, joint_reasoning, pieces, summary_range).  Host memory;
+ * nthreads <= 0 uses every hardware thread. */
+int rs_field_confidences(const char* text, const int64_t* offsets, int64_t n, const int64_t* tok_offsets,
+                         const char* tok_text, const int64_t* tok_text_offsets, const double* tok_lp,
+                         const uint8_t* tok_has_lp, double* out, int32_t nthreads);
 
 /* ---- FIFO admission chain (Scheduler.step, scheduler.py:397-410) ----------
  * The new-query loop of Scheduler.step: for the waiting queue in FIFO order,

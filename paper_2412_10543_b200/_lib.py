@@ -139,6 +139,7 @@ SIGNATURES = {
     "rs_candidate_costs": (ctypes.c_int, [_P, _P, _P, _I64, ctypes.POINTER(SelectParamsC), ctypes.POINTER(CostModelC),
                                           _P, _P, _P, ctypes.c_size_t, _P]),
     "rs_parse_profiles": (ctypes.c_int, [ctypes.c_char_p, _P, _I64, _P, _P, _P, _P, _P, _I32]),
+    "rs_field_confidences": (ctypes.c_int, [ctypes.c_char_p, _P, _I64, _P, ctypes.c_char_p, _P, _P, _P, _P, _I32]),
     "rs_admit_fifo": (ctypes.c_int, [_P, _P, _P, _P, _I64, ctypes.POINTER(SelectParamsC),
                                      ctypes.POINTER(AdmitParamsC), _P, _P, _P, _P]),
     "rs_peer_region_bytes": (ctypes.c_int, [_I32, _I64, _I32, ctypes.POINTER(ctypes.c_uint64)]),

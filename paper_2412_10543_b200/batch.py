@@ -208,6 +208,44 @@ def parse_profiles(texts, confidences=None, *, nthreads: int = 0):
     return out, clamped, status, lines
 
 
+def field_confidences(texts, token_lists, *, nthreads: int = 0) -> np.ndarray:
+    """_per_field_confidences (profiler.py:427-464) for a batch of estimator
+    answers and their token streams (each a list of ``{"token", "logprob"}``
+    dicts, or None), on the host (``rs_field_confidences``, multi-threaded
+    native code).  Returns float64 [n, 4] in PROFILE_FIELDS order."""
+    n = len(texts)
+    if len(token_lists) != n:
+        raise ValueError("texts and token_lists differ in length")
+    enc = [t.encode("utf-8", "surrogatepass") for t in texts]
+    offsets = np.zeros(n + 1, dtype=np.int64)
+    if n:
+        offsets[1:] = np.cumsum([len(b) for b in enc])
+    tok_offsets = np.zeros(n + 1, dtype=np.int64)
+    tok_enc, lps, has = [], [], []
+    for i, toks in enumerate(token_lists):
+        for tok in toks or ():
+            text = tok.get("token", "")
+            if not isinstance(text, str):
+                raise TypeError(f"object of type {type(text).__name__!r} has no len()")  # len(text), :454
+            lp = tok.get("logprob")
+            tok_enc.append(text.encode("utf-8", "surrogatepass"))
+            lps.append(0.0 if lp is None else float(lp))
+            has.append(lp is not None)
+        tok_offsets[i + 1] = len(tok_enc)
+    tt_off = np.zeros(len(tok_enc) + 1, dtype=np.int64)
+    if tok_enc:
+        tt_off[1:] = np.cumsum([len(b) for b in tok_enc])
+    lp_arr = np.asarray(lps, dtype=np.float64)
+    has_arr = np.asarray(has, dtype=np.uint8)
+    out = np.empty((n, 4), dtype=np.float64)
+    lib = _lib.load()
+    _lib.check(lib.rs_field_confidences(b"".join(enc) + b"\0", offsets.ctypes.data, n, tok_offsets.ctypes.data,
+                                        b"".join(tok_enc) + b"\0", tt_off.ctypes.data, lp_arr.ctypes.data,
+                                        has_arr.ctypes.data, out.ctypes.data, int(nthreads)),
+               "rs_field_confidences")
+    return out
+
+
 def clamped_names(bits) -> frozenset:
     bits = int(bits)
     return frozenset(n for b, n in ((RS_CLAMPED_PIECES, "pieces"), (RS_CLAMPED_SUMMARY, "summary_range"))

@@ -22,6 +22,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cmath>
 #include <thread>
 #include <vector>
 
@@ -300,8 +301,113 @@ void parse_one(const unsigned char* s, const unsigned char* e, double conf, rs_p
   *status = RS_PARSE_OK;
 }
 
+// CPython 3.12 sum() over floats (builtin_sum_impl): 0 + x0, then Neumaier's
+// compensated additions, the compensation added at the end when finite.
+struct PySum {
+  double f = 0.0, c = 0.0;
+  int64_t n = 0;
+  void add(double x) {
+    if (n++ == 0) {
+      f = 0.0 + x;  // int 0 + float
+      return;
+    }
+    const double t = f + x;
+    if (std::fabs(f) >= std::fabs(x))
+      c += (f - t) + x;
+    else
+      c += (x - t) + f;
+    f = t;
+  }
+  double value() const { return (c != 0.0 && std::isfinite(c)) ? f + c : f; }
+};
+
+// code points in UTF-8 text (lead bytes; str len of the decoded token)
+inline int64_t code_points(const unsigned char* s, const unsigned char* e) {
+  int64_t n = 0;
+  for (; s < e; ++s) n += (*s & 0xC0) != 0x80;
+  return n;
+}
+
+void field_conf_one(const unsigned char* s, const unsigned char* e, int64_t t0, int64_t t1,
+                    const unsigned char* tt, const int64_t* tto, const double* lp, const uint8_t* has, double* out) {
+  for (int f = 0; f < 4; ++f) out[f] = 1.0;
+  if (t1 <= t0) return;  // `if not tokens` (profiler.py:431)
+  rs_profile prof;
+  uint8_t st;
+  int32_t lines[4];
+  parse_one(s, e, 1.0, &prof, nullptr, lines, &st);
+  if (st != RS_PARSE_OK) return;  // UnparseableAnswer -> 1.0 (:434-436)
+  // line_starts (:439-441): 0 and the end of every splitlines(keepends=True) line, in code points
+  std::vector<int64_t> starts{0};
+  int64_t cp = 0;
+  for (const unsigned char* p = s; p < e;) {
+    int nb;
+    const uint32_t c = decode(p, e, &nb);
+    p += nb;
+    ++cp;
+    if (is_linebreak(c)) {
+      if (c == 0x0D && p < e && *p == 0x0A) {  // \r\n is one break
+        ++p;
+        ++cp;
+      }
+      starts.push_back(cp);
+    }
+  }
+  if (cp > starts.back()) starts.push_back(cp);  // a last line without a break
+  const int64_t nlines = int64_t(starts.size());
+  PySum acc[4];
+  int64_t offset = 0;
+  for (int64_t t = t0; t < t1; ++t) {
+    // the first line whose end lies past the token's start, else the last line (:446-452)
+    int64_t lineno = nlines - 2;
+    const auto it = std::upper_bound(starts.begin() + 1, starts.end(), offset);
+    if (it != starts.end()) lineno = int64_t(it - starts.begin()) - 1;
+    if (has[t])
+      for (int f = 0; f < 4; ++f)
+        if (lines[f] == lineno) acc[f].add(lp[t]);
+    offset += code_points(tt + tto[t], tt + tto[t + 1]);
+  }
+  for (int f = 0; f < 4; ++f)
+    if (acc[f].n) out[f] = std::exp(acc[f].value() / double(acc[f].n));  // :461-462
+}
+
 }  // namespace
 }  // namespace rs
+
+extern "C" int rs_field_confidences(const char* text, const int64_t* offsets, int64_t n, const int64_t* tok_offsets,
+                                    const char* tok_text, const int64_t* tok_text_offsets, const double* tok_lp,
+                                    const uint8_t* tok_has_lp, double* out, int32_t nthreads) {
+  using namespace rs;
+  RS_REQUIRE(n >= 0, "n must be non-negative");
+  if (n == 0) return RS_OK;
+  RS_REQUIRE(text && offsets && tok_offsets && out, "NULL argument");
+  for (int64_t i = 0; i < n; ++i) {
+    RS_REQUIRE(offsets[i] <= offsets[i + 1] && offsets[i] >= 0, "offsets must be non-decreasing");
+    RS_REQUIRE(tok_offsets[i] <= tok_offsets[i + 1] && tok_offsets[i] >= 0, "token offsets must be non-decreasing");
+  }
+  const int64_t ntok = tok_offsets[n];
+  RS_REQUIRE(ntok == 0 || (tok_text && tok_text_offsets && tok_lp && tok_has_lp), "NULL token argument");
+  for (int64_t t = 0; t < ntok; ++t)
+    RS_REQUIRE(tok_text_offsets[t] <= tok_text_offsets[t + 1] && tok_text_offsets[t] >= 0,
+               "token text offsets must be non-decreasing");
+  const auto* base = reinterpret_cast<const unsigned char*>(text);
+  const auto* tbase = reinterpret_cast<const unsigned char*>(tok_text);
+  auto work = [&](int64_t a, int64_t b) {
+    for (int64_t i = a; i < b; ++i)
+      field_conf_one(base + offsets[i], base + offsets[i + 1], tok_offsets[i], tok_offsets[i + 1], tbase,
+                     tok_text_offsets, tok_lp, tok_has_lp, out + 4 * i);
+  };
+  int t = nthreads > 0 ? nthreads : int(std::thread::hardware_concurrency());
+  t = int(std::max<int64_t>(1, std::min<int64_t>(t, n / 256 + 1)));
+  if (t == 1) {
+    work(0, n);
+    return RS_OK;
+  }
+  std::vector<std::thread> pool;
+  for (int i = 0; i < t; ++i) pool.emplace_back(work, n * i / t, n * (i + 1) / t);
+  for (auto& th : pool) th.join();
+  return RS_OK;
+}
 
 extern "C" int rs_parse_profiles(const char* text, const int64_t* offsets, int64_t n, const double* confidence,
                                  rs_profile* out, uint8_t* clamped, int32_t* line_numbers, uint8_t* status,

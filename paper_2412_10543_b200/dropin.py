@@ -69,6 +69,7 @@ def install(ragsched_pkg) -> dict:
         (memory, "plan_calls"): memory.plan_calls,
         (prof, "parse_profile_text"): prof.parse_profile_text,
         (sched, "plan_calls"): sched.plan_calls,
+        (prof, "_per_field_confidences"): prof._per_field_confidences,
     }
 
     sched.best_fit_select = functools.partial(_scheduler.best_fit_select, **kw_cfg)
@@ -89,6 +90,7 @@ def install(ragsched_pkg) -> dict:
     sched.plan_calls = pc
     prof.parse_profile_text = functools.partial(_profiler.parse_profile_text, profile_cls=mapping.QueryProfile,
                                                 range_cls=types.IntRange, exc_cls=prof.UnparseableAnswer)
+    prof._per_field_confidences = _profiler.per_field_confidences
     return originals
 
 

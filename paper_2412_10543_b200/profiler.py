@@ -128,3 +128,15 @@ def parse_profile_text(text: str, confidence: float = 1.0, *, profile_cls=None, 
                       f"in estimator answer: {text!r}")
     return (_b.unpack_profile(recs[0], profile_cls=profile_cls, range_cls=range_cls),
             _b.clamped_names(clamped[0]), {f: int(lines[0, i]) for i, f in enumerate(PROFILE_FIELDS)})
+
+
+def per_field_confidences(content: str, tokens: list[dict] | None) -> dict[str, float]:
+    """_per_field_confidences (profiler.py:427-464) through the native
+    ``rs_field_confidences``: each answer token falls on the line its
+    starting character lies in; a field's confidence is the exponentiated
+    mean log-prob of its line's tokens, 1.0 without any (or without tokens,
+    or when the answer does not parse)."""
+    if not tokens:
+        return {name: 1.0 for name in PROFILE_FIELDS}
+    row = _b.field_confidences([content], [tokens], nthreads=1)[0]
+    return {name: float(row[i]) for i, name in enumerate(PROFILE_FIELDS)}

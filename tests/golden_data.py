@@ -102,3 +102,13 @@ def candidate_costs():
     """Per-candidate plan bytes and plan delays from the reference
     (tests/golden/make_golden.py gen_costs)."""
     return _load("costs.npz")
+
+
+def field_conf_rows():
+    """[text, tokens, [float.hex x 4]] from the reference's _per_field_confidences
+    (tests/golden/make_field_conf.py)."""
+    import gzip
+    import json
+
+    with gzip.open(os.path.join(GOLDEN, "field_conf.json.gz"), "rt", encoding="utf-8") as f:
+        return json.load(f)
