@@ -449,9 +449,10 @@ struct RegTopK {
   }
 
   // Cooperative merge of ONE lane's list with its buffered candidates, by the
-  // whole warp (coop_sort64 below): lane src publishes its KREG sorted
-  // entries to the warp's scratch, the warp sorts them with src's admitted
-  // buffer entries, src reloads the first KREG.
+  // whole warp (coop_rank_merge above; coop_sort64 with RS_TOPK_COOP_RANK=0):
+  // lane src publishes its KREG sorted entries to the warp's scratch, the
+  // warp merges them with src's admitted buffer entries, src reloads the
+  // first KREG.
   uint32_t sbase;  // shared-window byte address of this warp's (KREG + BUF) x 8-byte scratch
   __device__ __forceinline__ void coop_merge(int src, int ns, uint32_t kt) {
     const int lane = int(threadIdx.x & 31);
