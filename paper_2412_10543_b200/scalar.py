@@ -14,6 +14,7 @@ synchronize, read the block.  Same kernels, same results as the batch path.
 from __future__ import annotations
 
 import ctypes
+import struct
 import threading
 
 import numpy as np
@@ -26,6 +27,11 @@ from ._lib import CONFIG_DTYPE, PROFILE_DTYPE, SPACE_DTYPE, WINDOW_DTYPE
 _SPACE, _PROFILE, _QLEN, _FREE, _CONFIG, _WINDOW, _OUTSPACE = 0, 16, 32, 40, 48, 64, 240
 _LAT_IN, _LAT_OUT, _PB_IN, _PB_OUT = 256, 280, 288, 312
 _BLOCK = 512
+# struct layouts of the records written per call (PROFILE_DTYPE, SPACE_DTYPE, WINDOW_DTYPE in _lib)
+_PROFILE_FMT, _SPACE_FMT = "<BBHHHd", "<HHHHHHI"
+_SPACE_BYTES = struct.calcsize(_SPACE_FMT)
+_WINDOW_LEN = WINDOW_DTYPE.fields["len"][1]
+assert struct.calcsize(_PROFILE_FMT) == PROFILE_DTYPE.itemsize and _SPACE_BYTES == SPACE_DTYPE.itemsize
 
 
 class _Ctx:
@@ -52,6 +58,11 @@ class _Ctx:
         self.pb_in = v(_PB_IN, np.dtype("<i4"), 4)   # method, num_chunks, interlen, qlen
         self.pb_out = v(_PB_OUT, np.dtype("<i8"))
         self.sptr = int(self.stream.cuda_stream)
+        self.mv = memoryview(self.buf)  # struct.pack_into / unpack_from: cheaper than numpy setitem per call
+        self._lat_fn = self.lib.rs_call_latency
+        self._lat_args = (self.p(_LAT_IN), self.p(_LAT_IN + 8), self.p(_LAT_IN + 16), 1)
+        self._pb_fn = self.lib.rs_plan_bytes
+        self._pb_args = (self.p(_PB_IN), self.p(_PB_IN + 4), self.p(_PB_IN + 8), self.p(_PB_IN + 12), 1)
 
     def p(self, off: int) -> int:
         return self.base + off
@@ -65,11 +76,13 @@ _lock = threading.Lock()
 
 
 def ctx() -> _Ctx:
-    if not torch.cuda.is_available():
-        raise _lib.LibraryUnavailable("no CUDA device: paper_2412_10543_b200 runs only on a B200 (no CPU fallback)")
-    dev = torch.cuda.current_device()
-    c = _ctx.get(dev)
+    dev = torch.cuda.current_device() if _ctx else None  # no context yet: check the device first
+    c = _ctx.get(dev) if dev is not None else None
     if c is None:
+        # (torch.cuda.is_available() costs ~4 us: checked once per device context, not per call)
+        if not torch.cuda.is_available():
+            raise _lib.LibraryUnavailable("no CUDA device: paper_2412_10543_b200 runs only on a B200 (no CPU fallback)")
+        dev = torch.cuda.current_device()
         with _lock:
             c = _ctx.get(dev) or _Ctx(dev)
             _ctx[dev] = c
@@ -100,12 +113,11 @@ def gate_one(profile: tuple, window_spaces: list, gate_params: _lib.GateParamsC)
     Returns the rs_space record (a copy; ``gate_fallback`` set on fallback)."""
     c = ctx()
     with _lock:
-        c.profile[0] = profile
-        w = c.window[0]
+        struct.pack_into(_PROFILE_FMT, c.mv, _PROFILE, *profile)
         n = len(window_spaces)
         for i, s in enumerate(window_spaces):
-            w["spaces"][i] = (*s, 0, 0)
-        w["len"] = n
+            struct.pack_into(_SPACE_FMT, c.mv, _WINDOW + i * _SPACE_BYTES, *s, 0, 0)
+        struct.pack_into("<i", c.mv, _WINDOW + _WINDOW_LEN, n)
         _lib.check(c.lib.rs_prune_gate(c.p(_PROFILE), 1, ctypes.byref(gate_params), c.p(_WINDOW), c.p(_OUTSPACE),
                                        int(c.ws.data_ptr()), c.ws.numel(), c.sptr), "rs_prune_gate")
         c.sync()
@@ -115,21 +127,23 @@ def gate_one(profile: tuple, window_spaces: list, gate_params: _lib.GateParamsC)
 def call_latency_one(prompt_tokens: int, max_output_tokens: int, concurrent: int, cost: _lib.CostModelC) -> float:
     c = ctx()
     with _lock:
-        c.lat_in[:] = (prompt_tokens, max_output_tokens, concurrent)
-        _lib.check(c.lib.rs_call_latency(c.p(_LAT_IN), c.p(_LAT_IN + 8), c.p(_LAT_IN + 16), 1, ctypes.byref(cost),
-                                         c.p(_LAT_OUT), c.sptr), "rs_call_latency")
-        c.sync()
-        return float(c.lat_out[0])
+        struct.pack_into("<qqq", c.mv, _LAT_IN, prompt_tokens, max_output_tokens, concurrent)
+        rc = c._lat_fn(*c._lat_args, ctypes.byref(cost), c.p(_LAT_OUT), c.sptr)
+        if rc:
+            _lib.check(rc, "rs_call_latency")
+        c.stream.synchronize()
+        return struct.unpack_from("<d", c.mv, _LAT_OUT)[0]
 
 
 def plan_bytes_one(method: int, num_chunks: int, interlen: int, qlen: int, params: _lib.SelectParamsC) -> int:
     c = ctx()
     with _lock:
-        c.pb_in[:] = (method, num_chunks, interlen, qlen)
-        _lib.check(c.lib.rs_plan_bytes(c.p(_PB_IN), c.p(_PB_IN + 4), c.p(_PB_IN + 8), c.p(_PB_IN + 12), 1,
-                                       ctypes.byref(params), c.p(_PB_OUT), c.sptr), "rs_plan_bytes")
-        c.sync()
-        return int(c.pb_out[0])
+        struct.pack_into("<iiii", c.mv, _PB_IN, method, num_chunks, interlen, qlen)
+        rc = c._pb_fn(*c._pb_args, ctypes.byref(params), c.p(_PB_OUT), c.sptr)
+        if rc:
+            _lib.check(rc, "rs_plan_bytes")
+        c.stream.synchronize()
+        return struct.unpack_from("<q", c.mv, _PB_OUT)[0]
 
 
 class AdmitArena:
@@ -200,9 +214,13 @@ class AdmitArena:
         args = (p(self.t_configs), p(self.t_qlen), m, ctypes.byref(params), int(max_ctx), p(self.t_offsets))
         _lib.check(c.lib.rs_plan_calls(*args, 0, 0, p(self.t_status), int(self.ws.data_ptr()), self.ws.numel(),
                                        c.sptr), "rs_plan_calls(count)")
-        c.sync()
-        if int(self.offsets[m]) > self.calls_cap:
-            self._grow_calls(int(self.offsets[m]))
+        # a plan has at most max_chunks + 1 calls (map_reduce): when the buffer
+        # holds that for every config, the fill follows the count in stream
+        # order with no round trip in between
+        if m * (int(params.max_chunks) + 1) > self.calls_cap:
+            c.sync()
+            if int(self.offsets[m]) > self.calls_cap:
+                self._grow_calls(int(self.offsets[m]))
         _lib.check(c.lib.rs_plan_calls(*args, p(self.t_calls), p(self.t_totals), 0, int(self.ws.data_ptr()),
                                        self.ws.numel(), c.sptr), "rs_plan_calls(fill)")
         c.sync()

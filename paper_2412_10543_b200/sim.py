@@ -9,9 +9,16 @@ from .batch import CostModel  # sim.py:42-57
 __all__ = ["CostModel", "call_latency"]
 
 
+_COST_C: dict = {}  # (prefill, decode base, slowdown) -> rs_cost_model struct (a sim passes one CostModel)
+
+
 def call_latency(call, concurrent_seqs: int, cost: CostModel) -> float:
     """sim.py:84-92 — bit-exact IEEE double via ``rs_call_latency`` (scalar
     fast path, scalar.py)."""
-    c = _b.cost_c(_b.CostModel(cost.prefill_secs_per_token, cost.decode_secs_per_token_base,
-                               cost.batch_slowdown_per_seq))
+    key = (cost.prefill_secs_per_token, cost.decode_secs_per_token_base, cost.batch_slowdown_per_seq)
+    c = _COST_C.get(key)
+    if c is None:
+        c = _b.cost_c(_b.CostModel(*key))
+        if len(_COST_C) < 64:
+            _COST_C[key] = c
     return _scalar.call_latency_one(int(call.prompt_tokens), int(call.max_output_tokens), int(concurrent_seqs), c)
