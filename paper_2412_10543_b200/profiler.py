@@ -74,12 +74,34 @@ def _gate_one(profile, window_spaces, *, threshold, default_space, max_chunks, s
     prof = _b.profile_tuple(profile)
     if threshold is None:
         prof = prof[:5] + (1.0,)
-    ds = _b.space_record(default_space if default_space is not None else DEFAULT_FALLBACK_SPACE)
+    ds = _space_rec(default_space if default_space is not None else DEFAULT_FALLBACK_SPACE)
     gp = _gate_params(float(threshold) if threshold is not None else 1.0, ds, int(max_chunks))
-    r = _scalar.gate_one(prof, [_b.space_record(s) for s in window_spaces], gp)
-    if int(r["gate_fallback"]) and default_space is not None and not window_spaces:
+    r = _scalar.gate_one(prof, [_space_rec(s) for s in window_spaces], gp)
+    if r[5] and default_space is not None and not window_spaces:
         return default_space, True  # `window.hull() or default_space` returns the object itself
-    return _b.unpack_space(r, space_cls=space_cls, method_enum=method_enum, range_cls=range_cls), bool(r["gate_fallback"])
+    return _space_obj(r[:5], space_cls, method_enum, range_cls), bool(r[5])
+
+
+def _space_rec(space) -> tuple:
+    """space_record, memoised for hashable (frozen) spaces: a gate call
+    re-encodes the default space and up to 10 window spaces."""
+    try:
+        return _space_rec_cached(space)
+    except TypeError:  # unhashable space object
+        return _b.space_record(space)
+
+
+@functools.lru_cache(maxsize=4096)
+def _space_rec_cached(space) -> tuple:
+    return _b.space_record(space)
+
+
+@functools.lru_cache(maxsize=4096)
+def _space_obj(rec: tuple, space_cls, method_enum, range_cls):
+    """A gate result record -> the (frozen, immutable) space object, memoised."""
+    m, nlo, nhi, illo, ilhi = rec
+    return _b.unpack_space({"methods": m, "num_chunks_lo": nlo, "num_chunks_hi": nhi, "interlen_lo": illo,
+                            "interlen_hi": ilhi}, space_cls=space_cls, method_enum=method_enum, range_cls=range_cls)
 
 
 @functools.lru_cache(maxsize=64)

@@ -110,7 +110,8 @@ def select_one(space: tuple | None, profile: tuple | None, qlen: int, free_bytes
 
 def gate_one(profile: tuple, window_spaces: list, gate_params: _lib.GateParamsC) -> np.void:
     """rs_prune_gate for one profile against a window of <= 10 space tuples.
-    Returns the rs_space record (a copy; ``gate_fallback`` set on fallback)."""
+    Returns the rs_space record as a tuple (methods, num_chunks_lo,
+    num_chunks_hi, interlen_lo, interlen_hi, gate_fallback)."""
     c = ctx()
     with _lock:
         struct.pack_into(_PROFILE_FMT, c.mv, _PROFILE, *profile)
@@ -120,8 +121,8 @@ def gate_one(profile: tuple, window_spaces: list, gate_params: _lib.GateParamsC)
         struct.pack_into("<i", c.mv, _WINDOW + _WINDOW_LEN, n)
         _lib.check(c.lib.rs_prune_gate(c.p(_PROFILE), 1, ctypes.byref(gate_params), c.p(_WINDOW), c.p(_OUTSPACE),
                                        int(c.ws.data_ptr()), c.ws.numel(), c.sptr), "rs_prune_gate")
-        c.sync()
-        return c.outspace[0].copy()
+        c.stream.synchronize()
+        return struct.unpack_from(_SPACE_FMT, c.mv, _OUTSPACE)[:6]
 
 
 def call_latency_one(prompt_tokens: int, max_output_tokens: int, concurrent: int, cost: _lib.CostModelC) -> float:
