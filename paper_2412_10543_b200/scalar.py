@@ -59,6 +59,7 @@ class _Ctx:
         self.pb_out = v(_PB_OUT, np.dtype("<i8"))
         self.sptr = int(self.stream.cuda_stream)
         self.mv = memoryview(self.buf)  # struct.pack_into / unpack_from: cheaper than numpy setitem per call
+        self.many, self.many_np, self.many_cap = None, None, 0  # call_latency_many's pinned arrays
         self._lat_fn = self.lib.rs_call_latency
         self._lat_args = (self.p(_LAT_IN), self.p(_LAT_IN + 8), self.p(_LAT_IN + 16), 1)
         self._pb_fn = self.lib.rs_plan_bytes
@@ -134,6 +135,30 @@ def call_latency_one(prompt_tokens: int, max_output_tokens: int, concurrent: int
             _lib.check(rc, "rs_call_latency")
         c.stream.synchronize()
         return struct.unpack_from("<d", c.mv, _LAT_OUT)[0]
+
+
+def call_latency_many(prompt_tokens: list, max_output_tokens: list, concurrent: list,
+                      cost: _lib.CostModelC) -> list:
+    """rs_call_latency over a small batch through pinned, device-mapped
+    arrays: one launch + one synchronize for all of them."""
+    c = ctx()
+    n = len(prompt_tokens)
+    with _lock:
+        if c.many_cap < n:
+            cap = max(n, 2 * c.many_cap, 64)
+            c.many = torch.zeros((4, cap), dtype=torch.int64, pin_memory=True)  # prompt, out, concurrency, latency
+            c.many_np = c.many.numpy()
+            c.many_cap = cap
+        a = c.many_np
+        a[0, :n] = prompt_tokens
+        a[1, :n] = max_output_tokens
+        a[2, :n] = concurrent
+        base, row = int(c.many.data_ptr()), 8 * c.many_cap
+        rc = c._lat_fn(base, base + row, base + 2 * row, n, ctypes.byref(cost), base + 3 * row, c.sptr)
+        if rc:
+            _lib.check(rc, "rs_call_latency")
+        c.stream.synchronize()
+        return a[3, :n].view(np.float64).tolist()
 
 
 def plan_bytes_one(method: int, num_chunks: int, interlen: int, qlen: int, params: _lib.SelectParamsC) -> int:

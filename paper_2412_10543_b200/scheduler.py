@@ -208,6 +208,7 @@ class Scheduler:
                                                params.max_chunks, g, allow_fallback=params.allow_fallback)
         self._dev = None
         self._arena_obj = None
+        self._inflight = 0  # calls admitted by step() and not yet completed (the sim's `running`, sim.py:224-281)
 
     @property
     def free_bytes(self) -> int:
@@ -388,6 +389,14 @@ class Scheduler:
         decided, started = [], []
         if not self._admit_backlog(now, started) and self.waiting:
             self._admit_new(now, decided, started)
+        if started:
+            # the caller usually asks each started call's latency next, the
+            # i-th at concurrency (calls running before) + i (sim.py:223-229):
+            # evaluate them in one batch now (sim.precompute_latencies)
+            from .sim import precompute_latencies
+
+            precompute_latencies(started, self._inflight)
+            self._inflight += len(started)
         return decided, started
 
     # -- completion --------------------------------------------------------
@@ -403,6 +412,7 @@ class Scheduler:
         if call_index in run.completed or call_index not in run.admitted:
             raise k.UnknownCall(f"call {call_index} of {query_id} is not running")
         done_before = set(run.completed)
+        self._inflight -= 1
         self.used_bytes -= run.plan.calls[call_index].kv_bytes
         self._check_accounting()
         run.completed.add(call_index)

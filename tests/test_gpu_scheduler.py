@@ -81,7 +81,9 @@ def test_admit_chain_single_launch_for_a_burst():
     """A burst of waiting queries is admitted by one rs_admit_fifo launch per
     chunk (plus the plan expansion), not one launch per query."""
     from paper_2412_10543_b200 import _lib
+    from paper_2412_10543_b200 import sim as SIM
 
+    SIM._LAST_COST[0] = None  # no latency batch yet (test_dispatch_latencies_are_batch_evaluated)
     sc = dict(ps=0, capacity=64 * 1024**3)
     sched = make_scheduler(sc)
     prof = QueryProfile(False, True, 2, IntRange(30, 60), 0.95)
@@ -93,6 +95,55 @@ def test_admit_chain_single_launch_for_a_burst():
     adms, admitted = sched.step(0.0)
     assert len(adms) == 30 and len(admitted) == 30
     assert _lib.launch_count() - l0 <= 4
+
+
+def test_dispatch_latencies_are_batch_evaluated():
+    """Scheduler.step evaluates the started calls' latencies in one launch at
+    concurrency (running before) + i, as the reference's dispatch asks for
+    them (sim.py:223-229); call_latency then returns those values — bit-equal
+    to the scalar path — and takes the scalar path for anything else."""
+    from paper_2412_10543_b200 import _lib
+    from paper_2412_10543_b200 import sim as SIM
+    from paper_2412_10543_b200.batch import CostModel
+
+    cost = CostModel()
+    sched = make_scheduler(dict(ps=0, capacity=64 * 1024**3))
+    prof = QueryProfile(False, True, 2, IntRange(30, 60), 0.95)
+    for i in range(12):
+        sched.submit(S.PendingQuery(query=QueryRecord(id=f"q{i}", text="t", query_token_len=300 + 37 * i),
+                                    space=PrunedConfigSpace(frozenset({SynthesisMethod.MAP_RERANK}), IntRange(2, 6)),
+                                    arrival_time=0.0, profile=prof))
+    SIM._LAST_COST[0] = None
+    SIM._PRE.clear()
+    _, first = sched.step(0.0)  # no cost model seen yet: nothing precomputed
+    assert len(first) > 2 and not SIM._PRE
+    scalar = [SIM.call_latency(ac, i, cost) for i, ac in enumerate(first)]  # learns the cost model
+    for ac in first:
+        sched.complete(ac.query_id, ac.call_index, 1.0, rerank_confidence=0.5)
+    for i in range(12, 20):
+        sched.submit(S.PendingQuery(query=QueryRecord(id=f"q{i}", text="t", query_token_len=300 + 37 * i),
+                                    space=PrunedConfigSpace(frozenset({SynthesisMethod.MAP_RERANK}), IntRange(2, 6)),
+                                    arrival_time=1.0, profile=prof))
+    l0 = _lib.launch_count()
+    _, started = sched.step(1.0)
+    assert len(started) > 2 and len(SIM._PRE) == len(started)
+    launches = _lib.launch_count() - l0
+    running = 0  # every first-step call completed
+    got = [SIM.call_latency(ac, running + i, cost) for i, ac in enumerate(started)]
+    assert _lib.launch_count() - l0 == launches  # served from the batch, no scalar launch
+    SIM._PRE.clear()
+    want = [SIM.call_latency(ac, running + i, cost) for i, ac in enumerate(started)]  # scalar path
+    assert got == want and all(isinstance(x, float) for x in got)
+    # a different concurrency or cost model is never served from the batch
+    sched2 = make_scheduler(dict(ps=0, capacity=64 * 1024**3))
+    sched2.submit(S.PendingQuery(query=QueryRecord(id="z", text="t", query_token_len=500),
+                                 space=PrunedConfigSpace(frozenset({SynthesisMethod.MAP_RERANK}), IntRange(4, 4)),
+                                 arrival_time=0.0, profile=prof))
+    _, st2 = sched2.step(0.0)
+    v_wrong = SIM.call_latency(st2[0], 7, cost)
+    SIM._PRE.clear()
+    assert v_wrong == SIM.call_latency(st2[0], 7, cost)
+    assert scalar and all(isinstance(x, float) for x in scalar)
 
 
 SIM_GATES = [r for r in TRACES if r.get("gates")]
