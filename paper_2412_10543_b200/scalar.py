@@ -231,6 +231,33 @@ class AdmitArena:
         r = self.result[0]
         return int(r["admitted"]), int(r["stop"])
 
+    def admit_and_plan(self, n: int, params: _lib.SelectParamsC, capacity: int, used: int, max_ctx: int):
+        """rs_admit_fifo over entries [0, n), then rs_plan_calls (count and
+        fill) over all n configs, in stream order with ONE synchronize: the
+        entries the chain did not reach are pre-marked MustQueue (no calls),
+        and the calls buffer holds max_chunks + 1 calls per entry.  Returns
+        (admitted, stop, (offsets [m+1], calls, totals [m], status [m]))."""
+        c = self.c
+        need = n * (int(params.max_chunks) + 1)
+        if need > self.calls_cap:
+            self._grow_calls(need)
+        self.configs[:n] = np.zeros(1, dtype=CONFIG_DTYPE)
+        self.configs["status"][:n] = _lib.RS_SELECT_MUST_QUEUE
+        ap = _lib.AdmitParamsC(int(capacity), int(used), int(max_ctx))
+        p = lambda t: int(t.data_ptr())  # noqa: E731
+        pp = ctypes.byref(params)
+        _lib.check(c.lib.rs_admit_fifo(p(self.t_spaces), p(self.t_profiles), p(self.t_hasprof), p(self.t_qlen), n,
+                                       pp, ctypes.byref(ap), p(self.t_configs), p(self.t_info), p(self.t_result),
+                                       c.sptr), "rs_admit_fifo")
+        args = (p(self.t_configs), p(self.t_qlen), n, pp, int(max_ctx), p(self.t_offsets))
+        ws = (int(self.ws.data_ptr()), self.ws.numel(), c.sptr)
+        _lib.check(c.lib.rs_plan_calls(*args, 0, 0, p(self.t_status), *ws), "rs_plan_calls(count)")
+        _lib.check(c.lib.rs_plan_calls(*args, p(self.t_calls), p(self.t_totals), 0, *ws), "rs_plan_calls(fill)")
+        c.stream.synchronize()
+        r = self.result[0]
+        m = int(r["admitted"])
+        return m, int(r["stop"]), (self.offsets[:m + 1], self.calls, self.totals[:m], self.status[:m])
+
     def plan_calls(self, m: int, params: _lib.SelectParamsC, max_ctx: int):
         """rs_plan_calls over the first m configs: the count pass, then (after
         sizing) the fill pass.  Returns numpy views (offsets [m+1], calls,

@@ -299,8 +299,8 @@ class Scheduler:
     def _admit_new(self, now: float, admissions: list, admitted: list) -> None:
         """The loop of scheduler.py:404-409 over _try_admit_new (:335-395),
         as rs_admit_fifo launches over chunks of the waiting queue (packed
-        into a pinned, device-mapped arena: no copies, two round trips per
-        chunk).  An entry the C records cannot hold (e.g. a map_reduce range
+        into a pinned, device-mapped arena: no copies, one round trip per
+        chunk — the plan expansion follows the chain in stream order).  An entry the C records cannot hold (e.g. a map_reduce range
         starting at 0, memory.py:186-188) cuts the chunk before it; its error
         is raised only once it reaches the head of the queue, as the
         reference raises only for the entry it is admitting."""
@@ -323,12 +323,12 @@ class Scheduler:
             arena.profiles[:n] = np.frombuffer(b"".join(e[2] for e in entries), dtype=np.uint8).reshape(n, 16)
             arena.hasprof[:n] = [e[3] for e in entries]
             arena.qlen[:n] = [e[4] for e in entries]
-            m, stop = arena.admit(n, _b.params_c(self._sel), self.capacity_bytes, self.used_bytes,
-                                  p.model.max_context_tokens)
+            m, stop, planned = arena.admit_and_plan(n, _b.params_c(self._sel), self.capacity_bytes, self.used_bytes,
+                                                    p.model.max_context_tokens)
             cfg_all = arena.configs[: min(m + 1, n)].copy()
             if m:
-                plans = _mem.plans_from_host(*arena.plan_calls(m, _b.params_c(self._sel), p.model.max_context_tokens),
-                                             call_cls=k.LlmCall, plan_cls=k.CallPlan, kind_enum=k.CallKind)
+                plans = _mem.plans_from_host(*planned, call_cls=k.LlmCall, plan_cls=k.CallPlan,
+                                             kind_enum=k.CallKind)
                 infos = arena.info[:m].copy()
             for j in range(m):
                 pending = self.waiting[0]

@@ -104,6 +104,13 @@ class FakeArena:
         r = res.numpy().view(_lib.ADMIT_RESULT_DTYPE)[0]
         return int(r["admitted"]), int(r["stop"])
 
+    def admit_and_plan(self, n, params_c, capacity, used, max_ctx):
+        # the GPU arena runs the plan expansion over all n entries in stream
+        # order; the restated chain plans the admitted prefix (what the
+        # scheduler reads)
+        m, stop = self.admit(n, params_c, capacity, used, max_ctx)
+        return m, stop, (self.plan_calls(m, params_c, max_ctx) if m else None)
+
     def plan_calls(self, m, params_c, max_ctx):
         cfg = torch.from_numpy(self.configs[:m].view(np.uint8).reshape(m, 16))
         off, calls, tot, st = fake_plan_calls(cfg, torch.from_numpy(self.qlen[:m]), self._params(params_c), max_ctx)
