@@ -432,6 +432,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--burst-merge", default="auto", choices=("auto", "on", "off"),
                     help="pair kernel variant: automatic (default), always cooperative, always lean")
+    ap.add_argument("--probe", default="off", choices=("on", "off"),
+                    help="experiment: pair kernel probe pass seeding the admission bounds (slower at cfg1)")
     ap.add_argument("--exchange", default="peer", choices=["peer", "all_to_all", "all_gather"],
                     help="key exchange of the sharded path (N>1): the library's NVLink peer-memory kernels "
                          "(default) or NCCL")
@@ -472,6 +474,7 @@ def main():
     r0, r1 = rdist.shard_range(n, rank, world)
     index = IndexFlatL2(d, dtype=tdtype, capacity=r1 - r0, device=dev, id_base=r0)
     index.set_burst_merge(args.burst_merge)
+    index.set_probe(args.probe)
     if args.segment_rows:
         index.set_segment_rows(args.segment_rows)
     for a in range(r0, r1, 1 << 20):
@@ -665,6 +668,7 @@ def main():
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_total,
             "clocks": clk, "parity": parity, "plan": index.last_plan(),
             "burst_merge": {"mode": args.burst_merge, "cooperative_variant": index.burst_merge_active()},
+            "probe": {"mode": args.probe, "rows": index.last_probe_rows()},
         }
         print(json.dumps(line), flush=True)
     index.close()

@@ -361,6 +361,17 @@ int rs_index_set_segment_rows(rs_index* index, int32_t rows);
  * variants return bit-identical results; only the timing differs.
  * rs_index_burst_merge_active reports the variant the next search will use. */
 int rs_index_set_burst_merge(rs_index* index, int32_t mode);
+/* Probe pass of the CTA-pair kernel (an experiment, off by default): before
+ * the main launch, the same kernel scans the corpus's first rows (one 256-row
+ * tile per segment, one round of units) and seeds every query's shared
+ * admission bound with a valid upper bound of its final k-th distance, so the
+ * main launch's per-segment lists do not start cold.  mode 0 (default): off;
+ * 1: on whenever the shape allows (>= 4 probe lists per query).  Results are
+ * bit-identical either way; measured slower at cfg1.
+ * rs_index_last_probe_rows reports the rows the last search's probe scanned
+ * (0 = no probe). */
+int rs_index_set_probe(rs_index* index, int32_t mode);
+int rs_index_last_probe_rows(const rs_index* index, int32_t* rows);
 int rs_index_burst_merge_active(rs_index* index, int32_t* active);
 /* Preallocate the search workspace for up to nq_max queries of k results. */
 int rs_index_reserve(rs_index* index, int64_t nq_max, int32_t k);

@@ -124,6 +124,8 @@ SIGNATURES = {
     "rs_index_set_walk_bias": (ctypes.c_int, [_P, _I32]),
     "rs_index_set_segment_rows": (ctypes.c_int, [_P, _I32]),
     "rs_index_set_burst_merge": (ctypes.c_int, [_P, _I32]),
+    "rs_index_set_probe": (ctypes.c_int, [_P, _I32]),
+    "rs_index_last_probe_rows": (ctypes.c_int, [_P, _P]),
     "rs_index_burst_merge_active": (ctypes.c_int, [_P, _P]),
     "rs_index_reserve": (ctypes.c_int, [_P, _I64, _I32]),
     "rs_index_search": (ctypes.c_int, [_P, _P, _I64, _I32, _I64, _P, _P, _P, _P]),

@@ -747,6 +747,8 @@ struct rs_index {
   int32_t dim = 0, dtype = 0, device = 0, algo = RS_ALGO_AUTO;
   int32_t walk_bias = 0;  // test hook (rs_index_set_walk_bias)
   int32_t seg_rows_override = 0;  // tuning knob (rs_index_set_segment_rows): 0 = the planner's choice
+  int32_t probe_mode = 0;         // rs_index_set_probe: 0 off (default), 1 on (when the shape allows one)
+  int32_t last_probe_rows = 0;    // rows the last search's probe pass scanned (0 = none)
   int64_t capacity = 0, ntotal = 0;
   void* data = nullptr;
   float* norms = nullptr;
@@ -846,6 +848,36 @@ rs::SearchPlan make_plan(const rs_index* ix, int algo, int64_t nq, int64_t n, in
                      int64_t(ix->dim) * esize(ix->dtype), true);
 }
 
+// Probe pass of the CTA-pair kernel (rs_index_set_probe; measured and off by
+// default).  When every unit of a search runs in about one round (cfg1: 1,000
+// queries x 100k rows, 72 units of 22 tiles), every per-segment list starts
+// empty at the same time and a unit's first tiles admit nearly every column
+// (45% of cfg1's epilogue busy cycles).  The probe runs the same kernel first
+// over the corpus's first S rows, one tile per segment (one round of units),
+// and folds the kCas-th smallest of those lists' rank-ceil(k/kCas) distances
+// into qtau: a valid bound of every query's final k-th distance (>= k real
+// rows at or below it, distances bit-identical to the main launch's), so the
+// main launch's lists admit from their first tile.  Results are bit-identical
+// with or without it.  Measured at cfg1 (ncu launch list): the main launch
+// 641 -> 622 us, but the probe itself 105 us — its one-tile lists are all cold
+// start, the cost it was meant to remove — so the default is off.  Returns
+// the probe's plan (segments = 0: no probe).
+constexpr int kProbeMinLists = 4 * rs::kPairEpiGroups;  // the cascade needs kCas disjoint lists
+rs::SearchPlan probe_plan(const rs_index* ix, int algo, int64_t nq, const rs::SearchPlan& main) {
+  using namespace rs;
+  SearchPlan pp = main;
+  pp.segments = 0;
+  if (algo != RS_ALGO_TCGEN05 || ix->probe_mode != 1 || pair_small(nq) || kPairGroup != 1) return pp;
+  const int pairs = sm_count(ix->device) / 2;
+  const int64_t tiles = ix->ntotal / kTcBN;  // whole tiles only (no partial-tile rows)
+  const int64_t segs = std::min<int64_t>({int64_t(pairs / std::max(main.qtiles, 1)), 16, tiles / 16});
+  if (segs < kProbeMinLists) return pp;
+  pp.segments = int32_t(segs);
+  pp.seg_rows = kTcBN;
+  pp.ctas = int32_t(std::min<int64_t>(int64_t(main.qtiles) * segs, pairs));
+  return pp;
+}
+
 // Lean or cooperative pair-kernel variant (rs_index_set_burst_merge).  In the
 // automatic mode the previous launch's burst count (posted to pinned memory by
 // its last CTA; read without a synchronisation, so possibly one search stale) is normalised by
@@ -874,7 +906,9 @@ int run_partial(rs_index* ix, const void* queries, int64_t nq, int k, int64_t id
              "tcgen05 path needs 16-byte rows (bf16 dim %% 8, fp32 dim %% 4) and k <= %d", kTcMaxK);
   RS_REQUIRE(!(ix->algo == RS_ALGO_TCGEN05_1SM && ix->dtype != RS_BF16), "the single-CTA tcgen05 kernel is bf16-only");
   const SearchPlan plan = make_plan(ix, algo, nq, ix->ntotal, k);
-  const size_t part_bytes = size_t(nq) * plan.lists() * k * sizeof(uint64_t);
+  const SearchPlan pplan = probe_plan(ix, algo, nq, plan);
+  // the probe's lists go to the same buffer, overwritten by the main launch
+  const size_t part_bytes = size_t(nq) * std::max(plan.lists(), pplan.lists()) * k * sizeof(uint64_t);
   int rc = ensure_ws(ix, nq, part_bytes);
   if (rc) return rc;
   // 3xTF32 (fp32 corpus on the tensor cores): the same pass splits the queries
@@ -911,10 +945,19 @@ int run_partial(rs_index* ix, const void* queries, int64_t nq, int k, int64_t id
     if (pair) {
       const bool coop = burst_choice(ix);
       const bool count = ix->burst_mode < 0;  // automatic: this launch's count, for the next search's choice
+      const bool probe = pplan.segments > 0;
+      ix->last_probe_rows = probe ? int32_t(int64_t(pplan.segments) * pplan.seg_rows) : 0;
+      if (probe) {  // the same kernel over the first rows (probe_plan), then fold the bound
+        rc = launch_score_topk_pair(tmq, tf ? &tmql : nullptr, tmc, (tf && RS_TF32_STORED_LO) ? &tmcl : nullptr,
+                                    ix->qnorm, ix->norms, ix->cmin, nq, ix->last_probe_rows, ix->dim, k, id_base,
+                                    pplan, small, ix->part, ix->sched_counter, 0, ix->qtau, coop, nullptr, st);
+        if (rc == RS_OK) rc = launch_fold_probe_bounds(ix->qtau, nq, st);
+        if (rc) return rc;
+      }
       rc = launch_score_topk_pair(tmq, tf ? &tmql : nullptr, tmc, (tf && RS_TF32_STORED_LO) ? &tmcl : nullptr,
                                   ix->qnorm, ix->norms, ix->cmin, nq, ix->ntotal, ix->dim, k, id_base, plan, small,
                                   ix->part, ix->sched_counter, ix->walk_bias, ix->qtau, coop,
-                                  count ? ix->burst_host : nullptr, st);
+                                  count ? ix->burst_host : nullptr, st, probe);
       if (rc == RS_OK && count)
         ix->burst_tiles = double(plan.qtiles) * pair_tile_rows(small) / 32.0 * double(ceil_div(ix->ntotal, kTcBN));
     } else {
@@ -1085,6 +1128,19 @@ extern "C" int rs_index_data(const rs_index* ix, const void** emb, const float**
 extern "C" int rs_index_set_segment_rows(rs_index* ix, int32_t rows) {
   RS_REQUIRE(ix != nullptr && rows >= 0, "bad arguments");
   ix->seg_rows_override = rows;
+  return RS_OK;
+}
+
+extern "C" int rs_index_set_probe(rs_index* ix, int32_t mode) {
+  RS_REQUIRE(ix != nullptr, "index is NULL");
+  RS_REQUIRE(mode == 0 || mode == 1, "probe mode must be 0 or 1, got %d", mode);
+  ix->probe_mode = mode;
+  return RS_OK;
+}
+
+extern "C" int rs_index_last_probe_rows(const rs_index* ix, int32_t* rows) {
+  RS_REQUIRE(ix != nullptr && rows != nullptr, "NULL argument");
+  *rows = ix->last_probe_rows;
   return RS_OK;
 }
 

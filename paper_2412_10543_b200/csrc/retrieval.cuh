@@ -141,7 +141,9 @@ int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap* tmql, cons
                            const CUtensorMap* tmcl, const float* qn, const float* cn, const float* cmin, int64_t nq,
                            int64_t n, int dim, int k, int64_t id_base, const SearchPlan& plan, bool small,
                            uint64_t* part, int32_t* counter, int32_t walk_bias, uint32_t* qtau, bool coop,
-                           uint32_t* bursts_host, cudaStream_t st);
+                           uint32_t* bursts_host, cudaStream_t st, bool keep_tau = false);
+// qtau[q] = min(qtau[q], cascade slot kCas-1) after a probe launch
+int launch_fold_probe_bounds(uint32_t* qtau, int64_t nq, cudaStream_t st);
 // query rows per pair tile: 256, or 128 for the small-batch (M = 128) variant
 int pair_tile_rows(bool small);
 // 32-bit words of shared-bound state per query the pair kernel needs (qtau + cascade)

@@ -826,13 +826,33 @@ int launch_t(const CUtensorMap& tmq, const CUtensorMap& tmql, const CUtensorMap&
 
 }  // namespace
 
+// After the probe pass (the same kernel over the first rows of the corpus,
+// one tile per segment): fold each query's cascade bound into qtau.  Slot
+// kCas-1 is backed by kCas disjoint probe lists with >= cas_rank rows each at
+// or below it (>= k real rows), so it is a valid bound of the query's final
+// k-th distance by itself; the cascade is then restarted by the main launch,
+// whose lists overlap the probe's rows and must not combine with its entries.
+__global__ void fold_probe_bounds_kernel(uint32_t* __restrict__ qtau, int64_t nq) {
+  const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  const uint32_t b = qtau[nq + q * kCas + (kCas - 1)];
+  if (b < qtau[q]) qtau[q] = b;
+}
+
+int launch_fold_probe_bounds(uint32_t* qtau, int64_t nq, cudaStream_t st) {
+  if (nq <= 0) return RS_OK;
+  fold_probe_bounds_kernel<<<unsigned((nq + 255) / 256), 256, 0, st>>>(qtau, nq);
+  RS_CHECK_LAUNCH("fold_probe_bounds_kernel");
+  return RS_OK;
+}
+
 int pair_tile_rows(bool small) { return small ? Cfg<false, true>::PMv : Cfg<false, false>::PMv; }
 
 int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap* tmql, const CUtensorMap& tmc,
                            const CUtensorMap* tmcl, const float* qn, const float* cn, const float* cmin, int64_t nq,
                            int64_t n, int dim, int k, int64_t id_base, const SearchPlan& plan, bool small,
                            uint64_t* part, int32_t* counter, int32_t walk_bias, uint32_t* qtau, bool coop,
-                           uint32_t* bursts_host, cudaStream_t st) {
+                           uint32_t* bursts_host, cudaStream_t st, bool keep_tau) {
   const bool tf = tmql != nullptr;
   RS_REQUIRE(!tf || !RS_TF32_STORED_LO || tmcl != nullptr, "tf32 path with stored residuals needs the corpus lo map");
   RS_REQUIRE(!tf || G == 1, "the tf32 path has no multicast (RS_PAIR_GROUP) variant");
@@ -845,7 +865,10 @@ int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap* tmql, cons
   RS_REQUIRE(plan.segments >= 1 && plan.segments <= kMaxSegments, "segments out of range (%d)", plan.segments);
   RS_CHECK_CUDA(cudaMemsetAsync(counter, 0, sizeof(int32_t) * (3 + plan.segments), st),
                 "cudaMemsetAsync(unit counter, burst count, finished CTAs, segment frontiers)");
-  RS_CHECK_CUDA(cudaMemsetAsync(qtau, 0xff, sizeof(uint32_t) * size_t(nq) * (1 + kCas), st),
+  // keep_tau: qtau already holds a bound of this search's queries (the probe
+  // pass, fold_probe_bounds); only the cascade of finished lists restarts
+  RS_CHECK_CUDA(cudaMemsetAsync(keep_tau ? qtau + nq : qtau, 0xff,
+                                sizeof(uint32_t) * size_t(nq) * (keep_tau ? kCas : 1 + kCas), st),
                 "cudaMemsetAsync(shared bounds)");
   Params p{};
   p.qn = qn;

@@ -93,6 +93,20 @@ class IndexFlatL2:
         m = {"auto": -1, "off": 0, "on": 1}.get(mode, mode)
         _lib.check(self._lib.rs_index_set_burst_merge(self._h, int(m)))
 
+    def set_probe(self, mode: str | int) -> None:
+        """The pair kernel's probe pass (a first launch over the corpus's first
+        rows that seeds every query's admission bound; an experiment measured
+        slower at cfg1): "off"/0 (default) or "on"/1.  Results are
+        bit-identical either way."""
+        m = {"off": 0, "on": 1}.get(mode, mode)
+        _lib.check(self._lib.rs_index_set_probe(self._h, int(m)))
+
+    def last_probe_rows(self) -> int:
+        """Corpus rows the last search's probe pass scanned (0 = no probe)."""
+        v = ctypes.c_int32(0)
+        _lib.check(self._lib.rs_index_last_probe_rows(self._h, ctypes.byref(v)))
+        return int(v.value)
+
     def burst_merge_active(self) -> bool:
         """Whether the next search runs the cooperative variant."""
         v = ctypes.c_int32(0)

@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--corpus-rows", type=int, default=None)
     ap.add_argument("--segment-rows", type=int, default=0)
     ap.add_argument("--data", default="iso")
+    ap.add_argument("--probe", default="off", choices=("on", "off"))
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--reps", type=int, default=1)
     ap.add_argument("--persist-mb", type=int, default=0,
@@ -53,6 +54,7 @@ def main():
     dt = torch.bfloat16 if cfg["dtype"] == "bf16" else torch.float32
     dev = torch.device("cuda", 0)
     ix = IndexFlatL2(cfg["d"], dtype=dt, capacity=cfg["n"])
+    ix.set_probe(a.probe)
     if a.segment_rows:
         ix.set_segment_rows(a.segment_rows)
     for r in range(0, cfg["n"], 1 << 20):

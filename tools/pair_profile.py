@@ -44,6 +44,7 @@ def main():
     ap.add_argument("--rows", type=int, default=None)
     ap.add_argument("--queries", type=int, default=None)
     ap.add_argument("--k", type=int, default=35)
+    ap.add_argument("--probe", default="off", choices=("on", "off"))
     a = ap.parse_args()
     import bench
 
@@ -55,6 +56,7 @@ def main():
         raise SystemExit("needs the RS_PAIR_PROFILE=1 build (RAGSCHED_B200_LIB)")
     lib.rs_debug_pair_profile.argtypes = [ctypes.c_void_p, ctypes.c_int]
     ix = IndexFlatL2(d, dtype=dt, capacity=n)
+    ix.set_probe(a.probe)
     for r0 in range(0, n, 1 << 20):
         ix.add(synth.corpus_rows(r0, min(n, r0 + (1 << 20)), d, 0, dt, "cuda", a.data))
     q = synth.make_queries(nq, n, d, 0, dt, a.data).cuda()
@@ -79,8 +81,10 @@ def main():
             share = 100 * (rows[:, i] / denom).mean()
             out[label][nm] = round(share, 2)
             print(f"   {nm:34s} {share:5.1f}%")
-    # (query row, tile) visits: every row of every query tile meets every corpus tile once
-    tiles = -(-n // 256)
+    # (query row, tile) visits: every row of every query tile meets every corpus
+    # tile once (the counters also hold the probe launch's tiles, if any)
+    out["probe_rows"] = ix.last_probe_rows()
+    tiles = -(-n // 256) + out["probe_rows"] // 256
     rows_total = plan["qtiles"] * (256 if nq > 128 else 128)
     warp_tiles = rows_total / 32 * tiles
     c = arr[:, 8:13].sum(0)
