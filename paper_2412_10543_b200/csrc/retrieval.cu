@@ -753,7 +753,8 @@ struct rs_index {
   void* data = nullptr;
   float* norms = nullptr;
   float* norm_max = nullptr;  // device scalar: max squared norm over the shard
-  int32_t* sched_counter = nullptr;  // pair kernel: [0] units, [1] bursts, [2] finished CTAs, [3 + s] frontier of segment s
+  int32_t* sched_counter = nullptr;  // pair kernel: [0] units, [1] bursts, [2] finished CTAs, [3 + s] frontier of
+                                     // segment s, [3 + kMaxSegments + u] position of unit u (drift limiter)
   // burst merge (rs_index_set_burst_merge): mode, the automatic choice, and the
   // last pair launch's burst count, posted by its last CTA to pinned memory
   int32_t burst_mode = -1;
@@ -1013,7 +1014,8 @@ extern "C" int rs_index_create(int32_t dim, int32_t dtype, int64_t capacity, int
     // granules of norms past the last row of a partial tile
     if (e == cudaSuccess) e = cudaMalloc(&ix->norms, sizeof(float) * (capacity + rs::kTcBN));
     if (e == cudaSuccess) e = cudaMalloc(&ix->norm_max, sizeof(float));
-    if (e == cudaSuccess) e = cudaMalloc(&ix->sched_counter, sizeof(int32_t) * (3 + rs::kMaxSegments));
+    if (e == cudaSuccess) e = cudaMalloc(&ix->sched_counter,
+                                             sizeof(int32_t) * (3 + rs::kMaxSegments * (1 + rs::kSyncMaxQtiles)));
     if (e == cudaSuccess) e = cudaHostAlloc(&ix->burst_host, sizeof(uint32_t), cudaHostAllocDefault);
     if (e == cudaSuccess) *ix->burst_host = 0;
     if (e == cudaSuccess && dtype == RS_F32 && RS_TF32_STORED_LO && dim % 4 == 0)

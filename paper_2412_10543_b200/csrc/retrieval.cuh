@@ -99,6 +99,9 @@ int launch_merge_to_peers(const uint64_t* keys, int64_t nq, int nlists, int k_in
 
 // upper bound of SearchPlan::segments (plan_search never exceeds it)
 constexpr int kMaxSegments = 4096;
+// pair kernel drift limiter: query tiles per segment it covers (unit positions
+// live after the segment frontiers in the schedule counters)
+constexpr int kSyncMaxQtiles = 8;
 
 SearchPlan plan_search(int64_t nq, int64_t n, int bq, int bn, int ctas_capacity, int64_t row_bytes,
                        bool share_l2);

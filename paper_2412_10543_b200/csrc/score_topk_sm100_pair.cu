@@ -65,6 +65,16 @@ constexpr int HB = BN / 2;      // corpus rows staged per CTA
 #ifndef RS_PAIR_STAGES_TF32
 #define RS_PAIR_STAGES_TF32 3
 #endif
+// Drift limiter of the few-query-tile regime (2-8 query tiles: every unit of
+// a segment streams the same rows at once): a unit's producer does not start
+// a tile more than RS_PAIR_SYNC_TILES tiles past the slowest running unit of
+// its segment (bounded wait), so the segment's rows are read from DRAM once
+// instead of once per drifting pair.  0 = off.
+#ifndef RS_PAIR_SYNC_TILES
+#define RS_PAIR_SYNC_TILES 0
+#endif
+constexpr int32_t kSyncIdle = 0x7f7f7f7f;  // prog[] of a unit not running (memset 0x7f)
+constexpr uint64_t kSyncMaxWaitNs = 20000;  // per tile: a stalled partner never stalls a unit for long
 // corpus tiles prefetched into L2 ahead of the TMA loads (0 = off)
 #ifndef RS_PAIR_PREFETCH
 #define RS_PAIR_PREFETCH 0
@@ -198,6 +208,8 @@ struct Params {
   int32_t* done;     // CTAs finished (zeroed): the last one posts *bursts to bursts_host
   uint32_t* bursts_host;  // pinned host word (device-accessible under unified addressing) or null
   int32_t* seg_pos;  // per segment: absolute tile index the most advanced pair last started (zeroed)
+  int32_t* prog;     // drift limiter: per unit, the absolute tile it is loading (kSyncIdle when not running)
+  int32_t sync_tiles;  // drift limiter window (0 = off)
   int32_t walk_bias; // test hook: unit of query tile qt starts walk_bias*(qt+1) tiles past the frontier
   uint32_t* qtau;    // per query: best k-th distance bits published by any unit (memset 0xff per search)
   uint32_t* qcas;    // per query: the kCas smallest rank-r distances of finished lists (r = ceil(k/kCas))
@@ -415,6 +427,29 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         for (int64_t j = 0; j < walk.ntiles; ++j) {
           const int64_t c0 = walk.c0(j);
           if (scheduler) red_max_relaxed_gpu_s32(p.seg_pos + seg, start + int32_t(j));
+          if (RS_PAIR_SYNC_TILES > 0 && scheduler && p.sync_tiles > 0) {
+            // publish this unit's position, then wait while it is more than
+            // sync_tiles past the slowest running unit of the segment (the
+            // slowest never waits, so every unit progresses)
+            const int32_t pos = start + int32_t(j);
+            st_relaxed_gpu_s32(p.prog + u, pos);
+            uint64_t t0 = 0;
+            for (;;) {
+              int32_t m = kSyncIdle;
+              for (int q2 = 0; q2 < p.qtiles; ++q2) {
+                if (q2 == qt) continue;
+                const int32_t v = ld_relaxed_gpu_s32(p.prog + int64_t(seg) * p.qtiles + q2);
+                m = v < m ? v : m;
+              }
+              if (m == kSyncIdle || pos - m <= p.sync_tiles) break;
+              uint64_t t;
+              asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+              if (t0 == 0) t0 = t;
+              else if (t - t0 > kSyncMaxWaitNs) break;
+              __nanosleep(128);
+            }
+            if (j + 1 == walk.ntiles) st_relaxed_gpu_s32(p.prog + u, kSyncIdle);
+          }
           for (int kb = 0; kb < p.kblocks; ++kb) {
             PROF(0, mbar_wait(&tail->empty[stage], phase ^ 1));
             uint8_t* sa = smem + size_t(stage) * C::STAGE_BYTES;
@@ -891,6 +926,14 @@ int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap* tmql, cons
   p.done = counter + 2;
   p.bursts_host = bursts_host;
   p.seg_pos = counter + 3;
+  // drift limiter: only when 2-8 query tiles share each segment (G == 1)
+  p.sync_tiles = (RS_PAIR_SYNC_TILES > 0 && G == 1 && p.qtiles >= 2 && p.qtiles <= kSyncMaxQtiles &&
+                  int64_t(p.qtiles) * plan.segments <= int64_t(kSyncMaxQtiles) * kMaxSegments)
+                     ? RS_PAIR_SYNC_TILES : 0;
+  p.prog = counter + 3 + kMaxSegments;
+  if (p.sync_tiles > 0)
+    RS_CHECK_CUDA(cudaMemsetAsync(p.prog, 0x7f, sizeof(int32_t) * size_t(p.qtiles) * plan.segments, st),
+                  "cudaMemsetAsync(unit positions)");
   p.walk_bias = walk_bias;
   p.qtau = qtau;
   p.qcas = qtau + nq;  // the caller allocates nq * (1 + kCas) words
