@@ -842,6 +842,10 @@ rs::SearchPlan make_plan(const rs_index* ix, int algo, int64_t nq, int64_t n, in
       p.ctas = int32_t(std::min<int64_t>(int64_t(p.qtiles) * p.segments, sms / (2 * kPairGroup)));
     }
     p.lists_per_seg = small ? 2 : kPairEpiGroups;
+    const int pairs = sms / (2 * kPairGroup);
+    const int64_t units = int64_t(p.qtiles) * p.segments;
+    p.sync_tiles = (kPairGroup == 1 && !small && p.qtiles >= 2 && p.qtiles <= kSyncMaxQtiles && units == pairs)
+                       ? RS_PAIR_SYNC_TILES : 0;
     return p;
   }
   if (algo == RS_ALGO_TCGEN05_1SM) return plan_search(nq, n, kTcBM, kTcBN, sms, int64_t(ix->dim) * 2, true);
@@ -875,6 +879,7 @@ rs::SearchPlan probe_plan(const rs_index* ix, int algo, int64_t nq, const rs::Se
   if (segs < kProbeMinLists) return pp;
   pp.segments = int32_t(segs);
   pp.seg_rows = kTcBN;
+  pp.sync_tiles = 0;
   pp.ctas = int32_t(std::min<int64_t>(int64_t(main.qtiles) * segs, pairs));
   return pp;
 }

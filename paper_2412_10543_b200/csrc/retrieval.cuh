@@ -21,6 +21,7 @@ struct SearchPlan {
   int64_t seg_rows = 0;
   int32_t ctas = 0;
   int32_t lists_per_seg = 1;  // sorted lists a unit writes per query (epilogue groups)
+  int32_t sync_tiles = 0;     // pair kernel drift limiter window (0 = off)
   int32_t lists() const { return segments * lists_per_seg; }
 };
 
@@ -99,9 +100,25 @@ int launch_merge_to_peers(const uint64_t* keys, int64_t nq, int nlists, int k_in
 
 // upper bound of SearchPlan::segments (plan_search never exceeds it)
 constexpr int kMaxSegments = 4096;
-// pair kernel drift limiter: query tiles per segment it covers (unit positions
-// live after the segment frontiers in the schedule counters)
-constexpr int kSyncMaxQtiles = 8;
+// Pair kernel drift limiter.  With few query tiles every unit of a segment
+// streams the same corpus rows at once, but the dynamically scheduled pairs
+// drift apart by more than the segment's share of L2 and the laggard re-reads
+// the rows from DRAM (cfg4 corpus, nq 512: 1.39x the corpus).  A unit's
+// producer then waits (bounded, per tile) while it is more than
+// RS_PAIR_SYNC_TILES tiles past the slowest running unit of its segment.
+// Enabled by make_plan when 2 <= query tiles <= kSyncMaxQtiles and the units
+// are exactly one round of pairs (on B200: 2 query tiles x 37 segments).
+// Measured (cfg4 corpus, tools/r2d_gpu5-7.sh, profiles/r2_drift_limiter.md):
+// nq 512 DRAM 28.4 -> 20.7 GB per launch (1.01x the corpus), +3-11% q/s;
+// nq 384 +5-7%; with more rounds of units the waits cost about what the
+// re-reads do (nq 1024, 2 rounds: +0.5-4%) or more (nq 768, 3 rounds: -4 to
+// -6.5%; nq 2048: -6%), and cfg1 (72 units) gains nothing, so it stays off
+// there.  Unit positions live after the segment frontiers in the schedule
+// counters.
+#ifndef RS_PAIR_SYNC_TILES
+#define RS_PAIR_SYNC_TILES 2
+#endif
+constexpr int kSyncMaxQtiles = 4;
 
 SearchPlan plan_search(int64_t nq, int64_t n, int bq, int bn, int ctas_capacity, int64_t row_bytes,
                        bool share_l2);

@@ -65,14 +65,10 @@ constexpr int HB = BN / 2;      // corpus rows staged per CTA
 #ifndef RS_PAIR_STAGES_TF32
 #define RS_PAIR_STAGES_TF32 3
 #endif
-// Drift limiter of the few-query-tile regime (2-8 query tiles: every unit of
-// a segment streams the same rows at once): a unit's producer does not start
-// a tile more than RS_PAIR_SYNC_TILES tiles past the slowest running unit of
-// its segment (bounded wait), so the segment's rows are read from DRAM once
-// instead of once per drifting pair.  0 = off.
-#ifndef RS_PAIR_SYNC_TILES
-#define RS_PAIR_SYNC_TILES 0
-#endif
+// Drift limiter (RS_PAIR_SYNC_TILES, retrieval.cuh; the plan enables it):
+// a unit's producer does not start a tile more than sync_tiles tiles past the
+// slowest running unit of its segment (bounded wait), so the segment's rows
+// are read from DRAM once instead of once per drifting pair.
 constexpr int32_t kSyncIdle = 0x7f7f7f7f;  // prog[] of a unit not running (memset 0x7f)
 constexpr uint64_t kSyncMaxWaitNs = 20000;  // per tile: a stalled partner never stalls a unit for long
 // corpus tiles prefetched into L2 ahead of the TMA loads (0 = off)
@@ -926,10 +922,9 @@ int launch_score_topk_pair(const CUtensorMap& tmq, const CUtensorMap* tmql, cons
   p.done = counter + 2;
   p.bursts_host = bursts_host;
   p.seg_pos = counter + 3;
-  // drift limiter: only when 2-8 query tiles share each segment (G == 1)
-  p.sync_tiles = (RS_PAIR_SYNC_TILES > 0 && G == 1 && p.qtiles >= 2 && p.qtiles <= kSyncMaxQtiles &&
-                  int64_t(p.qtiles) * plan.segments <= int64_t(kSyncMaxQtiles) * kMaxSegments)
-                     ? RS_PAIR_SYNC_TILES : 0;
+  // drift limiter: the plan's choice (make_plan), G == 1 only
+  RS_REQUIRE(plan.sync_tiles == 0 || (G == 1 && p.qtiles <= kSyncMaxQtiles), "drift limiter plan out of range");
+  p.sync_tiles = RS_PAIR_SYNC_TILES > 0 ? plan.sync_tiles : 0;
   p.prog = counter + 3 + kMaxSegments;
   if (p.sync_tiles > 0)
     RS_CHECK_CUDA(cudaMemsetAsync(p.prog, 0x7f, sizeof(int32_t) * size_t(p.qtiles) * plan.segments, st),

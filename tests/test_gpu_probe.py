@@ -1,4 +1,4 @@
-"""The pair kernel's probe pass (rs_index_set_probe).
+"""The pair kernel's probe pass (rs_index_set_probe) and drift limiter.
 
 Before the main launch the same kernel scans the corpus's first rows (one
 256-row tile per segment) and folds the kCas-th smallest of those lists'
@@ -76,3 +76,30 @@ def test_probe_ties_inside_probed_rows(dtype, bias):
     np.testing.assert_array_equal(D1, D0)
     for r, s in enumerate(starts.tolist()):
         np.testing.assert_array_equal(I1[r], s + np.arange(k), err_msg=f"row {r}")
+
+
+@pytest.mark.parametrize("bias", [0, 3])
+def test_drift_limiter_shapes_match_oracle(bias):
+    """2 query tiles whose units are exactly one round of pairs: make_plan turns the
+    drift limiter on (a unit waits, bounded, while it runs ahead of its
+    segment's slowest unit).  With a walk bias the units of a segment run at
+    permanently different positions, so every wait times out: the results
+    must still equal the unbiased search and the oracle."""
+    n, d, k, nq = 1_000_000, 128, 35, 512
+    c = synth.corpus_rows(0, n, d, 13, torch.bfloat16, "cuda")
+    q = synth.make_queries(nq, n, d, 13, torch.bfloat16)
+    ix = IndexFlatL2(d, dtype=torch.bfloat16, capacity=n)
+    ix.add(c)
+    D0, I0 = ix.search(q.cuda(), k)
+    if bias:
+        ix.set_walk_bias(bias)
+    D1, I1 = ix.search(q.cuda(), k)
+    torch.cuda.synchronize()
+    plan = ix.last_plan()
+    ix.close()
+    pairs = torch.cuda.get_device_properties(0).multi_processor_count // 2
+    assert plan["qtiles"] == 2 and plan["qtiles"] * plan["segments"] == pairs, plan
+    np.testing.assert_array_equal(I1.cpu().numpy(), I0.cpu().numpy())
+    np.testing.assert_array_equal(D1.cpu().numpy(), D0.cpu().numpy())
+    res = ro.check_topk(D1[:64].cpu().numpy(), I1[:64].cpu().numpy(), q[:64], c.cpu(), k, 1e-3)
+    assert not res["violations"], res["violations"][:5]
