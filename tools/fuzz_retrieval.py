@@ -2,7 +2,7 @@
 duplicate rows, document blocks (consecutive rows around a shared center:
 candidate bursts), non-normalised and zero rows, id bases, ragged incremental
 adds, forced wrap-around walks, every algorithm and both pair-kernel variants
-(lean / cooperative burst merge), each compared with the
+(lean / cooperative burst merge), the probe pass on or off, each compared with the
 float64 oracle (oracle/retrieval_oracle.check_topk — test infrastructure).
 usage: python tools/fuzz_retrieval.py [seconds] [seed]"""
 import os
@@ -61,8 +61,11 @@ def case(rng):
     bias = int(rng.choice([0, 0, 0, int(rng.integers(1, 9))]))
     pieces = int(rng.integers(1, 4))
     burst = str(rng.choice(["auto", "on", "off"]))  # the pair kernel's lean / cooperative variant
+    # the probe pass (off by default) on half the cases, drawn outside rng so
+    # earlier seeds keep their case lists
+    probe = "on" if (n * 31 + nq * 7 + k) % 2 else "off"
     return dict(dtype=dtype, d=d, n=n, nq=nq, k=k, algo=algo, q=q, c=c, base=base, bias=bias, pieces=pieces,
-                burst=burst, doc_block=blk)
+                burst=burst, doc_block=blk, probe=probe)
 
 
 def run(cs):
@@ -71,6 +74,7 @@ def run(cs):
     if cs["bias"]:
         ix.set_walk_bias(cs["bias"])
     ix.set_burst_merge(cs["burst"])
+    ix.set_probe(cs["probe"])
     cuts = sorted(set([0, cs["n"]] + list(np.random.default_rng(cs["n"]).integers(0, cs["n"] + 1, cs["pieces"] - 1))))
     for a, b in zip(cuts, cuts[1:]):
         if b > a:
@@ -94,7 +98,7 @@ def main(seconds=300, seed=0, max_cases=None):
         res, plan = run(cs)
         n_cases += 1
         desc = {x: (str(cs[x]) if x == "dtype" else cs[x]) for x in ("dtype", "d", "n", "nq", "k", "algo", "base", "bias",
-                                                                      "pieces", "burst", "doc_block")}
+                                                                      "pieces", "burst", "doc_block", "probe")}
         # id differences inside oracle near-ties are allowed (check_topk); the
         # exact-row rate is only a smoke signal on batches large enough for it,
         # and not on document blocks (whole blocks tie, or nearly)
