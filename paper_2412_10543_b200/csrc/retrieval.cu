@@ -844,7 +844,7 @@ rs::SearchPlan make_plan(const rs_index* ix, int algo, int64_t nq, int64_t n, in
     p.lists_per_seg = small ? 2 : kPairEpiGroups;
     const int pairs = sms / (2 * kPairGroup);
     const int64_t units = int64_t(p.qtiles) * p.segments;
-#ifndef RS_PAIR_SYNC_PARTIAL_ROUND  // experiment: also a single round with up to qtiles - 1 idle pairs
+#ifndef RS_PAIR_SYNC_PARTIAL_ROUND  // experiment: also a single round with up to qtiles - 1 idle pairs (measured: no gain, profiles/r2_drift_limiter.md)
 #define RS_PAIR_SYNC_PARTIAL_ROUND 0
 #endif
     const bool one_round = RS_PAIR_SYNC_PARTIAL_ROUND ? (units <= pairs && units > pairs - p.qtiles) : units == pairs;
